@@ -1,0 +1,28 @@
+// algos.h -- internal building blocks shared by the api_*.cpp entry points.
+#pragma once
+#include "marshal.h"
+#include "srht.h"
+
+namespace rnla {
+
+struct SvdDev {  // condensed_svd result on the device (column-major fp64)
+  DevBuf U, V;   // m x rank, n x rank (allocated for min(m, n) columns)
+  std::vector<double> s;
+  int64_t rank = 0, m = 0, n = 0;
+};
+
+const DenseOperator& gaussian_operator(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int dtype);
+std::shared_ptr<SrhtPlan> srht_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed);
+
+void thin_qr_dev(rnla_ctx* ctx, int64_t m, int64_t n, double* W, double* R);
+SvdDev condensed_svd_dev(rnla_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t a_rs, int64_t a_cs);
+void store_block(rnla_ctx* ctx, const double* src, int64_t rows, int64_t cols, int64_t ld, OutMat& o);
+DevMat f64_colmajor(rnla_ctx* ctx, const rnla_mat* a);
+
+// out (r x n, col-major) = diag(s) * V^T for V n x r col-major.
+void scale_rows_dev(rnla_ctx* ctx, int64_t r, int64_t n, const double* V, const double* s, double* out);
+// out (n x r, col-major) = V * diag(d).
+void scale_cols_dev(rnla_ctx* ctx, int64_t n, int64_t r, const double* V, const double* d, double* out);
+double sum_squares_dev(rnla_ctx* ctx, const double* p, int64_t count);
+
+}  // namespace rnla

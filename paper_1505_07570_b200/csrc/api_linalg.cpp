@@ -1,0 +1,503 @@
+// api_linalg.cpp -- core.hpp (thin_qr, condensed/truncated SVD, pinv),
+// randsvd.hpp (prototype_ksvd + power iterations) and the column-selection
+// sketches behind the C ABI.
+//
+// Reference: /root/reference/proj/src/core.cpp:15-88, src/randsvd.cpp:88-110,
+// src/sketch.cpp:125-167. Small factorizations run on the device in fp64
+// (linalg.cu); the passes over A are the GEMM kernels of gemm.cu.
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+#include "algos.h"
+#include "linalg.cuh"
+#include "marshal.h"
+#include "rbf.cuh"
+
+namespace rnla {
+
+// ---------------------------------------------------------------------------
+// small dense building blocks on fp64 column-major device buffers
+// ---------------------------------------------------------------------------
+
+// thin_qr semantics (src/core.cpp:37-46): Q (m x n) overwrites W, R n x n.
+void thin_qr_dev(rnla_ctx* ctx, int64_t m, int64_t n, double* W, double* R) {
+  qr_householder(ctx, m, n, W, R, 1, n);
+  fix_column_signs(ctx, m, n, W, 1, m, R, 1, n, n, /*pair_cols=*/false);
+}
+
+// condensed_svd semantics (src/core.cpp:48-64) of A (m x n, strided fp64).
+SvdDev condensed_svd_dev(rnla_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t a_rs, int64_t a_cs) {
+  SvdDev f;
+  const int64_t r = std::min(m, n);
+  f.U = DevBuf(sizeof(double) * std::max<int64_t>(m * r, 1), ctx->stream);
+  f.V = DevBuf(sizeof(double) * std::max<int64_t>(n * r, 1), ctx->stream);
+  DevBuf sv(sizeof(double) * std::max<int64_t>(r, 1), ctx->stream);
+  if (r == 0) throw InvalidArgument("condensed_svd: zero matrix has rank 0");
+  if (m >= 2 * n) {
+    // Tall: A = Q R (Householder), R = Ur S V', U = Q Ur.
+    DevBuf q(sizeof(double) * m * n, ctx->stream), rr(sizeof(double) * n * n, ctx->stream),
+        ur(sizeof(double) * n * n, ctx->stream);
+    copy2d<double>(ctx, m, n, A, a_rs, a_cs, q.as<double>(), 1, m);
+    qr_householder(ctx, m, n, q.as<double>(), rr.as<double>(), 1, n);
+    svd_thin(ctx, n, n, rr.as<double>(), 1, n, ur.as<double>(), sv.as<double>(), f.V.as<double>());
+    gemm<double>(ctx, m, n, n, 1.0, q.as<double>(), 1, m, ur.as<double>(), 1, n, 0.0, f.U.as<double>(), 1, m);
+  } else if (n >= 2 * m) {
+    // Wide: A' = Q R, R = Ur S V' => A = V S (Q Ur)'.
+    DevBuf q(sizeof(double) * n * m, ctx->stream), rr(sizeof(double) * m * m, ctx->stream),
+        ur(sizeof(double) * m * m, ctx->stream);
+    copy2d<double>(ctx, n, m, A, a_cs, a_rs, q.as<double>(), 1, n);
+    qr_householder(ctx, n, m, q.as<double>(), rr.as<double>(), 1, m);
+    svd_thin(ctx, m, m, rr.as<double>(), 1, m, ur.as<double>(), sv.as<double>(), f.U.as<double>());
+    gemm<double>(ctx, n, m, m, 1.0, q.as<double>(), 1, n, ur.as<double>(), 1, m, 0.0, f.V.as<double>(), 1, n);
+  } else {
+    svd_thin(ctx, m, n, A, a_rs, a_cs, f.U.as<double>(), sv.as<double>(), f.V.as<double>());
+  }
+  f.s.resize((size_t)r);
+  RNLA_CUDA(cudaMemcpyAsync(f.s.data(), sv.p, sizeof(double) * r, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double sigma1 = f.s[0];
+  if (!(sigma1 > 0.0)) throw InvalidArgument("condensed_svd: zero matrix has rank 0");
+  const double thresh = (double)std::max(m, n) * std::numeric_limits<double>::epsilon() * sigma1;
+  int64_t rho = 0;
+  while (rho < r && f.s[(size_t)rho] > thresh) ++rho;
+  f.rank = rho;
+  f.m = m;
+  f.n = n;
+  f.s.resize((size_t)rho);
+  fix_column_signs(ctx, m, rho, f.U.as<double>(), 1, m, f.V.as<double>(), 1, n, n, /*pair_cols=*/true);
+  return f;
+}
+
+// Write a column-major fp64 device block (rows x cols, ld) into an output operand.
+void store_block(rnla_ctx* ctx, const double* src, int64_t rows, int64_t cols, int64_t ld, OutMat& o) {
+  if (o.dev.dtype == RNLA_F64)
+    copy2d<double>(ctx, rows, cols, src, 1, ld, o.dev.as<double>(), o.dev.rs, o.dev.cs);
+  else
+    copy2d_cast<double, float>(ctx, rows, cols, src, 1, ld, o.dev.as<float>(), o.dev.rs, o.dev.cs);
+}
+
+// fp64 column-major working copy of any operand.
+DevMat f64_colmajor(rnla_ctx* ctx, const rnla_mat* a) {
+  DevMat d = to_device(ctx, a);
+  if (d.dtype == RNLA_F64 && d.colmajor()) return d;
+  return dense_copy(ctx, d, false, RNLA_F64);
+}
+
+// ---------------------------------------------------------------------------
+// prototype_ksvd (src/randsvd.cpp:88-110) + power iterations
+// ---------------------------------------------------------------------------
+template <class T>
+struct KsvdWork {
+  // Compute type T for the passes over A; orthonormalization in fp64.
+  static void orth(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, int64_t ld_unused) {
+    (void)ld_unused;
+    DevBuf w(sizeof(double) * rows * cols, ctx->stream), r(sizeof(double) * cols * cols, ctx->stream);
+    if constexpr (std::is_same<T, double>::value) {
+      RNLA_CUDA(cudaMemcpyAsync(w.p, Y, sizeof(double) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
+      thin_qr_dev(ctx, rows, cols, w.as<double>(), r.as<double>());
+      RNLA_CUDA(cudaMemcpyAsync(Y, w.p, sizeof(double) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      copy2d_cast<float, double>(ctx, rows, cols, Y, 1, rows, w.as<double>(), 1, rows);
+      thin_qr_dev(ctx, rows, cols, w.as<double>(), r.as<double>());
+      copy2d_cast<double, float>(ctx, rows, cols, w.as<double>(), 1, rows, Y, 1, rows);
+    }
+  }
+};
+
+template <class T>
+void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, uint64_t seed,
+                         const rnla_sketch_spec* spec, int32_t q, const rnla_mat* u_out, double* sv_out,
+                         const rnla_mat* v_out, int64_t* rank_out, int32_t* passes_out, double* error_fro) {
+  const int64_t m = a->rows, n = a->cols;
+  DevMat A = to_device(ctx, a);
+  const T* Ap = A.as<T>();
+  OutMat uo(ctx, u_out, m, k, "prototype_ksvd: U", false), vo(ctx, v_out, n, k, "prototype_ksvd: V", false);
+  rnla_sketch_spec local{};
+  if (spec) local = *spec;
+  else { local.kind = RNLA_SKETCH_GAUSSIAN; local.seed = seed; }
+  local.s = s;
+  int passes = 0;
+  // pass 1: Y = A S (m x s, column-major)
+  DevBuf Y(sizeof(T) * m * s, ctx->stream);
+  ++passes;
+  if (local.kind == RNLA_SKETCH_GAUSSIAN) {
+    const DenseOperator& g = gaussian_operator(ctx, n, s, local.seed, std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32);
+    gemm<T>(ctx, m, s, n, T(1), Ap, A.rs, A.cs, g.data.as<T>(), 1, n, T(0), Y.as<T>(), 1, m);
+  } else {
+    rnla_mat ym{Y.p, m, s, 1, m, a->dtype, 1};
+    rnla_mat am{A.p, m, n, A.rs, A.cs, a->dtype, 1};
+    int64_t cols = 0;
+    const rnla_status st = rnla_apply_sketch(ctx, &am, &local, &ym, &cols);
+    if (st != RNLA_OK) throw InvalidArgument(rnla_last_error());
+    require(cols == s, "prototype_ksvd: sketch returned a different width");
+  }
+  DevBuf Z(sizeof(T) * n * s, ctx->stream);
+  for (int32_t it = 0; it < q; ++it) {
+    KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), m);
+    // Z = orth(A' Q): n x s
+    gemm<T>(ctx, n, s, m, T(1), Ap, A.cs, A.rs, Y.as<T>(), 1, m, T(0), Z.as<T>(), 1, n);
+    ++passes;
+    KsvdWork<T>::orth(ctx, n, s, Z.as<T>(), n);
+    // Y = A Z
+    gemm<T>(ctx, m, s, n, T(1), Ap, A.rs, A.cs, Z.as<T>(), 1, n, T(0), Y.as<T>(), 1, m);
+    ++passes;
+  }
+  KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), m);  // Q = thin_qr(C).Q
+  // pass 2: B = Q' A (s x n), column-major
+  DevBuf B(sizeof(T) * s * n, ctx->stream);
+  gemm<T>(ctx, s, n, m, T(1), Y.as<T>(), m, 1, Ap, A.rs, A.cs, T(0), B.as<T>(), 1, s);
+  ++passes;
+  DevBuf B64;
+  const double* Bp;
+  if constexpr (std::is_same<T, double>::value) {
+    Bp = B.as<double>();
+  } else {
+    B64 = DevBuf(sizeof(double) * s * n, ctx->stream);
+    copy2d_cast<float, double>(ctx, s, n, B.as<float>(), 1, s, B64.as<double>(), 1, s);
+    Bp = B64.as<double>();
+  }
+  const int64_t kk = std::min(k, std::min(s, n));
+  SvdDev small = condensed_svd_dev(ctx, s, n, Bp, 1, s);
+  const int64_t rk = std::min(kk, small.rank);
+  // U = Q Ubar (m x rk)
+  DevBuf U64(sizeof(double) * m * std::max<int64_t>(rk, 1), ctx->stream);
+  if constexpr (std::is_same<T, double>::value) {
+    gemm<double>(ctx, m, rk, s, 1.0, Y.as<double>(), 1, m, small.U.as<double>(), 1, s, 0.0, U64.as<double>(), 1, m);
+  } else {
+    DevBuf uf(sizeof(float) * s * std::max<int64_t>(rk, 1), ctx->stream), Uf(sizeof(float) * m * std::max<int64_t>(rk, 1), ctx->stream);
+    copy2d_cast<double, float>(ctx, s, rk, small.U.as<double>(), 1, s, uf.as<float>(), 1, s);
+    gemm<float>(ctx, m, rk, s, 1.f, Y.as<float>(), 1, m, uf.as<float>(), 1, s, 0.f, Uf.as<float>(), 1, m);
+    copy2d_cast<float, double>(ctx, m, rk, Uf.as<float>(), 1, m, U64.as<double>(), 1, m);
+  }
+  store_block(ctx, U64.as<double>(), m, rk, m, uo);
+  store_block(ctx, small.V.as<double>(), n, rk, n, vo);
+  for (int64_t i = 0; i < rk; ++i) sv_out[i] = small.s[(size_t)i];
+  *rank_out = rk;
+  *passes_out = passes;
+  if (error_fro) {
+    // |A - U S V'|_F computed block-wise as a residual (no cancellation).
+    DevBuf svd(sizeof(double) * std::max<int64_t>(rk, 1), ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(svd.p, sv_out, sizeof(double) * rk, cudaMemcpyHostToDevice, ctx->stream));
+    DevBuf SVt(sizeof(double) * std::max<int64_t>(rk * n, 1), ctx->stream);  // diag(S) V' : rk x n col-major
+    scale_rows_dev(ctx, rk, n, small.V.as<double>(), svd.as<double>(), SVt.as<double>());
+    const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(m, ((int64_t)1 << 27) / std::max<int64_t>(n, 1)));
+    DevBuf R(sizeof(double) * blk * n, ctx->stream);
+    double total = 0.0;
+    for (int64_t r0 = 0; r0 < m; r0 += blk) {
+      const int64_t rows = std::min(blk, m - r0);
+      if constexpr (std::is_same<T, double>::value)
+        copy2d<double>(ctx, rows, n, Ap + r0 * A.rs, A.rs, A.cs, R.as<double>(), 1, rows);
+      else
+        copy2d_cast<float, double>(ctx, rows, n, Ap + r0 * A.rs, A.rs, A.cs, R.as<double>(), 1, rows);
+      gemm<double>(ctx, rows, n, rk, -1.0, U64.as<double>() + r0, 1, m, SVt.as<double>(), 1, rk, 1.0, R.as<double>(),
+                   1, rows);
+      total += sum_squares_dev(ctx, R.as<double>(), rows * n);
+    }
+    *error_fro = std::sqrt(total);
+  }
+  uo.finish(ctx);
+  vo.finish(ctx);
+}
+
+}  // namespace rnla
+
+using namespace rnla;
+
+extern "C" {
+
+rnla_status rnla_thin_qr(rnla_ctx* ctx, const rnla_mat* a, rnla_mat* q, rnla_mat* r) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "thin_qr: a");
+    require(a->rows >= a->cols, "thin_qr: rows < cols");
+    const int64_t m = a->rows, n = a->cols;
+    OutMat qo(ctx, q, m, n, "thin_qr: Q", false), ro(ctx, r, n, n, "thin_qr: R", false);
+    DevMat w = dense_copy(ctx, to_device(ctx, a), false, RNLA_F64);
+    DevBuf rr(sizeof(double) * std::max<int64_t>(n * n, 1), ctx->stream);
+    if (n > 0) thin_qr_dev(ctx, m, n, w.as<double>(), rr.as<double>());
+    store_block(ctx, w.as<double>(), m, n, m, qo);
+    store_block(ctx, rr.as<double>(), n, n, n, ro);
+    qo.finish(ctx);
+    ro.finish(ctx);
+  });
+}
+
+rnla_status rnla_condensed_svd(rnla_ctx* ctx, const rnla_mat* a, rnla_mat* u, double* sv, rnla_mat* v,
+                               int64_t* rank) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "condensed_svd: a");
+    require(sv && rank, "condensed_svd: null output");
+    const int64_t m = a->rows, n = a->cols, r = std::min(m, n);
+    OutMat uo(ctx, u, m, r, "condensed_svd: U", false), vo(ctx, v, n, r, "condensed_svd: V", false);
+    DevMat w = f64_colmajor(ctx, a);
+    SvdDev f = condensed_svd_dev(ctx, m, n, w.as<double>(), w.rs, w.cs);
+    store_block(ctx, f.U.as<double>(), m, f.rank, m, uo);
+    store_block(ctx, f.V.as<double>(), n, f.rank, n, vo);
+    for (int64_t i = 0; i < f.rank; ++i) sv[i] = f.s[(size_t)i];
+    *rank = f.rank;
+    uo.finish(ctx);
+    vo.finish(ctx);
+  });
+}
+
+rnla_status rnla_truncated_svd(rnla_ctx* ctx, const rnla_mat* a, int64_t k, rnla_mat* u, double* sv, rnla_mat* v,
+                               int64_t* rank) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "truncated_svd: a");
+    require(k >= 1 && k <= std::min(a->rows, a->cols), "truncated_svd: k out of range");
+    require(sv && rank, "truncated_svd: null output");
+    const int64_t m = a->rows, n = a->cols;
+    OutMat uo(ctx, u, m, k, "truncated_svd: U", false), vo(ctx, v, n, k, "truncated_svd: V", false);
+    DevMat w = f64_colmajor(ctx, a);
+    SvdDev f = condensed_svd_dev(ctx, m, n, w.as<double>(), w.rs, w.cs);
+    const int64_t rk = std::min(k, f.rank);
+    store_block(ctx, f.U.as<double>(), m, rk, m, uo);
+    store_block(ctx, f.V.as<double>(), n, rk, n, vo);
+    for (int64_t i = 0; i < rk; ++i) sv[i] = f.s[(size_t)i];
+    *rank = rk;
+    uo.finish(ctx);
+    vo.finish(ctx);
+  });
+}
+
+rnla_status rnla_pseudo_inverse(rnla_ctx* ctx, const rnla_mat* a, double tol, rnla_mat* p) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "pseudo_inverse: a");
+    const int64_t m = a->rows, n = a->cols, r = std::min(m, n);
+    OutMat po(ctx, p, n, m, "pseudo_inverse: P", false);
+    DevBuf out(sizeof(double) * std::max<int64_t>(n * m, 1), ctx->stream);
+    RNLA_CUDA(cudaMemsetAsync(out.p, 0, sizeof(double) * std::max<int64_t>(n * m, 1), ctx->stream));
+    if (r > 0) {
+      DevMat w = f64_colmajor(ctx, a);
+      DevBuf U(sizeof(double) * m * r, ctx->stream), V(sizeof(double) * n * r, ctx->stream),
+          S(sizeof(double) * r, ctx->stream);
+      svd_thin(ctx, m, n, w.as<double>(), w.rs, w.cs, U.as<double>(), S.as<double>(), V.as<double>());
+      std::vector<double> hs((size_t)r);
+      RNLA_CUDA(cudaMemcpyAsync(hs.data(), S.p, sizeof(double) * r, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (hs[0] > 0.0) {  // zero matrix -> zero of transposed shape (src/core.cpp:81)
+        const double cut = tol * hs[0];
+        std::vector<double> inv((size_t)r, 0.0);
+        for (int64_t i = 0; i < r; ++i)
+          if (hs[(size_t)i] > cut) inv[(size_t)i] = 1.0 / hs[(size_t)i];
+        DevBuf dinv(sizeof(double) * r, ctx->stream), Vs(sizeof(double) * n * r, ctx->stream);
+        RNLA_CUDA(cudaMemcpyAsync(dinv.p, inv.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
+        scale_cols_dev(ctx, n, r, V.as<double>(), dinv.as<double>(), Vs.as<double>());  // V diag(inv)
+        gemm<double>(ctx, n, m, r, 1.0, Vs.as<double>(), 1, n, U.as<double>(), m, 1, 0.0, out.as<double>(), 1, n);
+        RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      }
+    }
+    store_block(ctx, out.as<double>(), n, m, n, po);
+    po.finish(ctx);
+  });
+}
+
+rnla_status rnla_prototype_ksvd(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, uint64_t seed,
+                                const rnla_sketch_spec* spec, int32_t power_iters, rnla_mat* u, double* sv,
+                                rnla_mat* v, int64_t* rank, int32_t* passes, double* error_fro) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "prototype_ksvd: a");
+    require(k >= 1 && k <= s && s <= std::min(a->rows, a->cols), "prototype_ksvd: need k <= s <= min(m, n)");
+    require(power_iters >= 0, "prototype_ksvd: power_iters < 0");
+    require(sv && rank && passes, "prototype_ksvd: null output");
+    if (a->dtype == RNLA_F64)
+      prototype_ksvd_impl<double>(ctx, a, k, s, seed, spec, power_iters, u, sv, v, rank, passes, error_fro);
+    else
+      prototype_ksvd_impl<float>(ctx, a, k, s, seed, spec, power_iters, u, sv, v, rank, passes, error_fro);
+  });
+}
+
+// ---- column selection (src/sketch.cpp:125-167) ----
+
+rnla_status rnla_uniform_sample_columns(rnla_ctx* ctx, const rnla_mat* a, int64_t s, uint64_t seed, rnla_mat* c,
+                                        int64_t* indices) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "uniform_sample_columns: a");
+    require(s >= 1 && s <= a->cols, "uniform_sample_columns: s > n");
+    require(indices != nullptr, "uniform_sample_columns: null indices");
+    std::vector<int64_t> idx = sample_without_replacement_host(seed, a->cols, s);
+    std::copy(idx.begin(), idx.end(), indices);
+    OutMat o(ctx, c, a->rows, s, "uniform_sample_columns: C", false);
+    require(o.dev.dtype == a->dtype, "uniform_sample_columns: dtype mismatch");
+    DevMat A = to_device(ctx, a);
+    DevBuf di(sizeof(int64_t) * s, ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(di.p, idx.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    if (a->dtype == RNLA_F64)
+      gather_columns<double>(ctx, a->rows, s, A.as<double>(), A.rs, A.cs, di.as<int64_t>(), nullptr,
+                             o.dev.as<double>(), o.dev.rs, o.dev.cs);
+    else
+      gather_columns<float>(ctx, a->rows, s, A.as<float>(), A.rs, A.cs, di.as<int64_t>(), nullptr, o.dev.as<float>(),
+                            o.dev.rs, o.dev.cs);
+    o.finish(ctx);
+  });
+}
+
+static std::vector<double> leverage_scores_host(rnla_ctx* ctx, const rnla_mat* a, int64_t k) {
+  const int64_t m = a->rows, n = a->cols;
+  DevMat w = f64_colmajor(ctx, a);
+  SvdDev f = condensed_svd_dev(ctx, m, n, w.as<double>(), w.rs, w.cs);
+  const int64_t rk = k > 0 ? std::min(k, f.rank) : f.rank;
+  DevBuf sc(sizeof(double) * std::max<int64_t>(n, 1), ctx->stream);
+  row_sqnorms<double>(ctx, n, rk, f.V.as<double>(), 1, n, sc.as<double>());
+  std::vector<double> out((size_t)n);
+  RNLA_CUDA(cudaMemcpyAsync(out.data(), sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return out;
+}
+
+rnla_status rnla_leverage_scores(rnla_ctx* ctx, const rnla_mat* a, int64_t k, double* scores) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "leverage_scores: a");
+    require(scores != nullptr, "leverage_scores: null output");
+    if (k > 0) require(k <= std::min(a->rows, a->cols), "truncated_svd: k out of range");
+    auto v = leverage_scores_host(ctx, a, k);
+    std::copy(v.begin(), v.end(), scores);
+  });
+}
+
+rnla_status rnla_leverage_sample_columns(rnla_ctx* ctx, const rnla_mat* a, int64_t s, uint64_t seed, int64_t k,
+                                         int scale, rnla_mat* c, int64_t* indices, double* weights,
+                                         int64_t* count_out) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "leverage_sample_columns: a");
+    require(s >= 1, "leverage_sample_columns: s < 1");
+    require(indices && count_out, "leverage_sample_columns: null output");
+    if (k > 0) require(k <= std::min(a->rows, a->cols), "truncated_svd: k out of range");
+    std::vector<double> scores = leverage_scores_host(ctx, a, k);
+    double rho = 0.0;
+    for (double x : scores) rho += x;
+    std::vector<int64_t> draws = sample_with_replacement_host(seed, scores.data(), a->cols, s);
+    std::sort(draws.begin(), draws.end());
+    draws.erase(std::unique(draws.begin(), draws.end()), draws.end());
+    const int64_t cnt = (int64_t)draws.size();
+    std::vector<double> w((size_t)cnt);
+    for (int64_t t = 0; t < cnt; ++t)
+      w[(size_t)t] = std::sqrt(rho / (static_cast<double>(s) * scores[(size_t)draws[(size_t)t]]));
+    std::copy(draws.begin(), draws.end(), indices);
+    if (weights && scale) std::copy(w.begin(), w.end(), weights);
+    *count_out = cnt;
+    check_mat(c, "leverage_sample_columns: C");
+    require(c->rows == a->rows && c->cols >= cnt, "leverage_sample_columns: C too small");
+    rnla_mat cv = *c;
+    cv.cols = cnt;
+    OutMat o(ctx, &cv, a->rows, cnt, "leverage_sample_columns: C", false);
+    DevMat A = to_device(ctx, a);
+    DevBuf di(sizeof(int64_t) * std::max<int64_t>(cnt, 1), ctx->stream), dw(sizeof(double) * std::max<int64_t>(cnt, 1),
+                                                                             ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(di.p, draws.data(), sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+    RNLA_CUDA(cudaMemcpyAsync(dw.p, w.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+    const double* sp = scale ? dw.as<double>() : nullptr;
+    if (a->dtype == RNLA_F64)
+      gather_columns<double>(ctx, a->rows, cnt, A.as<double>(), A.rs, A.cs, di.as<int64_t>(), sp, o.dev.as<double>(),
+                             o.dev.rs, o.dev.cs);
+    else
+      gather_columns<float>(ctx, a->rows, cnt, A.as<float>(), A.rs, A.cs, di.as<int64_t>(), sp, o.dev.as<float>(),
+                            o.dev.rs, o.dev.cs);
+    o.finish(ctx);
+  });
+}
+
+// Row leverage of a tall M through CholeskyQR: G = M'M (fp64 accumulate),
+// R = chol(G), l_i = ||m_i R^-1||^2 = ||Q_i,:||^2 (basis invariance, paper
+// Fact 6; tests/test_facts.cpp:86-97); then the reference's weighted draw +
+// sort + unique (src/spsd.cpp:150-154).
+rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t p, uint64_t seed, double* scores,
+                                      int64_t* indices, int64_t* count_out) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(m, "leverage_sample_rows: m");
+    require(scores != nullptr, "leverage_sample_rows: null scores");
+    require(indices == nullptr || (p >= 1 && count_out), "sample_with_replacement: count < 1");
+    const int64_t n = m->rows, d = m->cols;
+    require(n >= d && d >= 1, "thin_qr: rows < cols");
+    DevMat M = to_device(ctx, m);
+    DevBuf G(sizeof(double) * d * d, ctx->stream), Rinv(sizeof(double) * d * d, ctx->stream);
+    if (M.dtype == RNLA_F64)
+      gemm<double>(ctx, d, d, n, 1.0, M.as<double>(), M.cs, M.rs, M.as<double>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
+                   d);
+    else
+      gemm_f32_in_f64(ctx, d, d, n, 1.0, M.as<float>(), M.cs, M.rs, M.as<float>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
+                      d);
+    if (!cholesky_upper(ctx, d, G.as<double>()))
+      throw NumericError("leverage_sample_rows: M'M is not positive definite (rank-deficient M)");
+    upper_inverse(ctx, d, G.as<double>(), Rinv.as<double>());
+    DevBuf sc(sizeof(double) * n, ctx->stream);
+    const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(n, ((int64_t)1 << 26) / d));
+    DevBuf T(sizeof(double) * blk * d, ctx->stream);
+    DevBuf Rf;
+    if (M.dtype != RNLA_F64) {
+      Rf = DevBuf(sizeof(float) * d * d, ctx->stream);
+      copy2d_cast<double, float>(ctx, d, d, Rinv.as<double>(), 1, d, Rf.as<float>(), 1, d);
+    }
+    for (int64_t r0 = 0; r0 < n; r0 += blk) {
+      const int64_t rows = std::min(blk, n - r0);
+      if (M.dtype == RNLA_F64) {
+        gemm<double>(ctx, rows, d, d, 1.0, M.as<double>() + r0 * M.rs, M.rs, M.cs, Rinv.as<double>(), 1, d, 0.0,
+                     T.as<double>(), d, 1);
+        row_sqnorms<double>(ctx, rows, d, T.as<double>(), d, 1, sc.as<double>() + r0);
+      } else {
+        gemm<float>(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
+                    T.as<float>(), d, 1);
+        row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
+      }
+    }
+    RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (indices) {
+      std::vector<int64_t> draws = sample_with_replacement_host(seed, scores, n, p);
+      std::sort(draws.begin(), draws.end());
+      draws.erase(std::unique(draws.begin(), draws.end()), draws.end());
+      std::copy(draws.begin(), draws.end(), indices);
+      *count_out = (int64_t)draws.size();
+    }
+  });
+}
+
+rnla_status rnla_apply_sketch(rnla_ctx* ctx, const rnla_mat* a, const rnla_sketch_spec* spec, rnla_mat* c,
+                              int64_t* cols_out) {
+  return guard([&] {
+    enter(ctx);
+    require(spec != nullptr, "null SketchSpec");
+    rnla_status st = RNLA_OK;
+    int64_t cols = spec->kind == RNLA_SKETCH_COMBINED ? spec->stage2_s : spec->s;
+    switch (spec->kind) {
+      case RNLA_SKETCH_GAUSSIAN: st = rnla_gaussian_sketch(ctx, a, spec->s, spec->seed, c); break;
+      case RNLA_SKETCH_SRHT: st = rnla_srht_sketch(ctx, a, spec->s, spec->seed, c); break;
+      case RNLA_SKETCH_COUNT: st = rnla_count_sketch(ctx, a, spec->s, spec->seed, c); break;
+      case RNLA_SKETCH_COMBINED: st = rnla_combined_sketch(ctx, a, spec, c); break;
+      case RNLA_SKETCH_UNIFORM_COLUMNS: {
+        std::vector<int64_t> idx((size_t)std::max<int64_t>(spec->s, 1));
+        st = rnla_uniform_sample_columns(ctx, a, spec->s, spec->seed, c, idx.data());
+        break;
+      }
+      case RNLA_SKETCH_LEVERAGE_COLUMNS: {
+        std::vector<int64_t> idx((size_t)std::max<int64_t>(spec->s, 1));
+        std::vector<double> w((size_t)std::max<int64_t>(spec->s, 1));
+        st = rnla_leverage_sample_columns(ctx, a, spec->s, spec->seed, spec->leverage_rank, spec->scale_columns, c,
+                                          idx.data(), w.data(), &cols);
+        break;
+      }
+      case RNLA_SKETCH_LANDMARK_COLUMNS:
+        throw InvalidArgument("apply_sketch: landmark selection (k-means) is outside the B200 core");
+      default:
+        throw InvalidArgument("apply_sketch: unknown kind");
+    }
+    if (st != RNLA_OK) {
+      const std::string msg = rnla_last_error();
+      if (st == RNLA_EINVAL) throw InvalidArgument(msg);
+      if (st == RNLA_ENUMERIC) throw NumericError(msg);
+      throw CudaError(msg);
+    }
+    if (cols_out) *cols_out = cols;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,324 @@
+// api_spsd.cpp -- rbf_kernel, KernelView-backed nystrom, approx_eig and the
+// fused Nystrom + top-k eigen route behind the C ABI.
+//
+// Reference: /root/reference/proj/src/spsd.cpp:33-72 (rbf_kernel, KernelView),
+// :181-222 (nystrom), :257-265 (approx_eig).
+#include <cmath>
+#include <limits>
+
+#include "algos.h"
+#include "dist.h"
+#include "linalg.cuh"
+#include "rbf.cuh"
+
+namespace rnla {
+
+namespace {
+
+// Selected landmarks (src/spsd.cpp:189-191) and the kernel columns C = K[:, S]
+// for X (n x d): fp64 output when T = double, else fp32.
+struct Landmarks {
+  std::vector<int64_t> sel;
+  DevBuf dsel, sq;  // device copy of sel, squared norms of all n points
+};
+
+template <class T>
+Landmarks landmarks(rnla_ctx* ctx, const DevMat& X, int64_t s, uint64_t seed) {
+  Landmarks L;
+  const int64_t n = X.rows, d = X.cols;
+  L.sel = sample_without_replacement_host(derive_seed(seed, 1), n, s);
+  L.dsel = DevBuf(sizeof(int64_t) * s, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(L.dsel.p, L.sel.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+  L.sq = DevBuf(sizeof(T) * n, ctx->stream);
+  sq_norms<T>(ctx, n, d, X.as<T>(), X.rs, X.cs, nullptr, L.sq.as<T>());
+  return L;
+}
+
+template <class T>
+void kernel_columns(rnla_ctx* ctx, const DevMat& X, const Landmarks& L, int64_t r0, int64_t rows, double sigma,
+                    T* C, int64_t c_rs, int64_t c_cs, DevBuf& sqsel) {
+  const int64_t s = (int64_t)L.sel.size(), d = X.cols;
+  if (!sqsel.p) {
+    sqsel = DevBuf(sizeof(T) * s, ctx->stream);
+    gather_columns<T>(ctx, 1, s, L.sq.as<T>(), 1, 1, L.dsel.as<int64_t>(), nullptr, sqsel.as<T>(), 1, 1);
+  }
+  // diag_of[t] = sel[t] - r0 marks the landmark's own row inside this block.
+  DevBuf diag(sizeof(int64_t) * s, ctx->stream);
+  std::vector<int64_t> h(L.sel);
+  for (auto& v : h) v -= r0;
+  RNLA_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+  rbf_block<T>(ctx, rows, s, d, X.as<T>() + r0 * X.rs, X.rs, X.cs, X.as<T>(), X.rs, X.cs, L.dsel.as<int64_t>(),
+               L.sq.as<T>() + r0, sqsel.as<T>(), sigma, diag.as<int64_t>(), C, c_rs, c_cs);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // `h` leaves scope
+}
+
+struct EigW {
+  DevBuf U;  // s x kept (col-major), eigenvectors of the top `kept` eigenvalues, descending
+  std::vector<double> lam;
+  int64_t kept = 0;
+};
+
+// eig(0.5 (W + W')) ascending, walk from the top with the floor
+// eps * lam_max * n (src/spsd.cpp:193-207).
+EigW nystrom_core(rnla_ctx* ctx, const double* W, int64_t s, int64_t n, int64_t kk) {
+  DevBuf ws(sizeof(double) * s * s, ctx->stream), lam(sizeof(double) * s, ctx->stream);
+  symmetrize(ctx, s, W, ws.as<double>());
+  eig_sym(ctx, s, ws.as<double>(), lam.as<double>());
+  std::vector<double> h((size_t)s);
+  RNLA_CUDA(cudaMemcpyAsync(h.data(), lam.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double lam_max = h[(size_t)s - 1];
+  if (!(lam_max > 0.0)) throw NumericError("nystrom: kernel block has no positive spectrum");
+  const double floor = std::numeric_limits<double>::epsilon() * lam_max * static_cast<double>(n);
+  int64_t kept = 0;
+  while (kept < kk && h[(size_t)(s - 1 - kept)] > floor) ++kept;
+  if (kept == 0) throw NumericError("nystrom: no retained eigenvalues");
+  EigW e;
+  e.kept = kept;
+  e.U = DevBuf(sizeof(double) * s * kept, ctx->stream);
+  // columns s-1, s-2, ... of the ascending eigenvector matrix
+  copy2d<double>(ctx, s, kept, ws.as<double>() + (s - 1) * s, 1, -s, e.U.as<double>(), 1, s);
+  e.lam.resize((size_t)kept);
+  for (int64_t t = 0; t < kept; ++t) e.lam[(size_t)t] = h[(size_t)(s - 1 - t)];
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return e;
+}
+
+// T = U_k diag(lam^-1/2) (s x kept, col-major fp64)
+DevBuf whitened(rnla_ctx* ctx, const EigW& e, int64_t s) {
+  std::vector<double> inv((size_t)e.kept);
+  for (int64_t t = 0; t < e.kept; ++t) inv[(size_t)t] = 1.0 / std::sqrt(e.lam[(size_t)t]);
+  DevBuf dinv(sizeof(double) * e.kept, ctx->stream), T(sizeof(double) * s * e.kept, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(dinv.p, inv.data(), sizeof(double) * e.kept, cudaMemcpyHostToDevice, ctx->stream));
+  scale_cols_dev(ctx, s, e.kept, e.U.as<double>(), dinv.as<double>(), T.as<double>());
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return T;
+}
+
+template <class T>
+void nystrom_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed, int64_t target_k,
+                  const rnla_mat* l_out, int64_t* selected, int64_t* kept_out, int64_t* entries) {
+  DevMat X = to_device(ctx, x);
+  const int64_t n = X.rows;
+  const int64_t kk = target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
+  require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
+  Landmarks L = landmarks<T>(ctx, X, s, seed);
+  // C = K[:, S] (n x s, col-major, compute dtype), W = rows S of C
+  DevBuf C(sizeof(T) * n * s, ctx->stream), sqsel;
+  kernel_columns<T>(ctx, X, L, 0, n, sigma, C.as<T>(), 1, n, sqsel);
+  DevBuf W(sizeof(double) * s * s, ctx->stream);
+  DevBuf W64;
+  if constexpr (std::is_same<T, double>::value) {
+    gather_rows<double>(ctx, s, s, C.as<double>(), 1, n, L.dsel.as<int64_t>(), W.as<double>(), 1, s);
+  } else {
+    DevBuf Wf(sizeof(float) * s * s, ctx->stream);
+    gather_rows<float>(ctx, s, s, C.as<float>(), 1, n, L.dsel.as<int64_t>(), Wf.as<float>(), 1, s);
+    copy2d_cast<float, double>(ctx, s, s, Wf.as<float>(), 1, s, W.as<double>(), 1, s);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  EigW e = nystrom_core(ctx, W.as<double>(), s, n, kk);
+  DevBuf Tm = whitened(ctx, e, s);
+  if (l_out) {
+    OutMat lo(ctx, l_out, n, kk, "nystrom: L", false);
+    if constexpr (std::is_same<T, double>::value) {
+      gemm<double>(ctx, n, e.kept, s, 1.0, C.as<double>(), 1, n, Tm.as<double>(), 1, s, 0.0, lo.dev.as<double>(),
+                   lo.dev.rs, lo.dev.cs);
+    } else {
+      DevBuf Tf(sizeof(float) * s * e.kept, ctx->stream);
+      copy2d_cast<double, float>(ctx, s, e.kept, Tm.as<double>(), 1, s, Tf.as<float>(), 1, s);
+      gemm<float>(ctx, n, e.kept, s, 1.f, C.as<float>(), 1, n, Tf.as<float>(), 1, s, 0.f, lo.dev.as<float>(),
+                  lo.dev.rs, lo.dev.cs);
+    }
+    lo.finish(ctx);
+  }
+  std::copy(L.sel.begin(), L.sel.end(), selected);
+  *kept_out = e.kept;
+  if (entries) *entries = n * s;
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// nystrom + approx_eig(L, k) through the Gram route:
+// L'L = T' (C'C) T with T = U_k Lambda^-1/2; eig(L'L) = (V, sigma^2);
+// U_L = L V / sigma = C (T V / sigma). C is formed block by block and never
+// stored; C'C accumulates in fp64 (DMMA) across row blocks.
+template <class T>
+void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed, int64_t target_k,
+                      int64_t k, const rnla_mat* u_out, double* lam_out, int64_t* selected, int64_t* kept_out) {
+  DevMat X = to_device(ctx, x);
+  const int64_t n_local = X.rows;
+  int64_t n = n_local;
+  const int64_t r_off = global_row_offset(ctx, n_local, &n);
+  const int64_t kk = target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
+  require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
+  require(ctx->world == 1, "nystrom_eig: row-sharded contexts are not supported yet");
+  (void)r_off;
+  Landmarks L = landmarks<T>(ctx, X, s, seed);
+  const int64_t blk = std::min<int64_t>(n_local, 16384);
+  DevBuf Cb(sizeof(T) * blk * s, ctx->stream), sqsel;
+  DevBuf G(sizeof(double) * s * s, ctx->stream), W(sizeof(double) * s * s, ctx->stream);
+  RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * s * s, ctx->stream));
+  for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
+    const int64_t rows = std::min(blk, n_local - r0);
+    kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows, sqsel);
+    if constexpr (std::is_same<T, double>::value)
+      gemm<double>(ctx, s, s, rows, 1.0, Cb.as<double>(), rows, 1, Cb.as<double>(), 1, rows, 1.0, G.as<double>(), 1,
+                   s);
+    else
+      gemm_f32_in_f64(ctx, s, s, rows, 1.0, Cb.as<float>(), rows, 1, Cb.as<float>(), 1, rows, 1.0, G.as<double>(), 1,
+                      s);
+  }
+  // W = K[S, S]: its rows are the landmark rows of C (recomputed directly).
+  {
+    DevBuf Wt(sizeof(T) * s * s, ctx->stream), sqs2;
+    DevMat Xs = alloc_dense(ctx, s, X.cols, true, X.dtype);
+    gather_rows<T>(ctx, s, X.cols, X.as<T>(), X.rs, X.cs, L.dsel.as<int64_t>(), Xs.as<T>(), Xs.rs, Xs.cs);
+    DevBuf sqS(sizeof(T) * s, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
+    gather_columns<T>(ctx, 1, s, L.sq.as<T>(), 1, 1, L.dsel.as<int64_t>(), nullptr, sqS.as<T>(), 1, 1);
+    std::vector<int64_t> id((size_t)s);
+    for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
+    RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    rbf_block<T>(ctx, s, s, X.cols, Xs.as<T>(), Xs.rs, Xs.cs, Xs.as<T>(), Xs.rs, Xs.cs, nullptr, sqS.as<T>(),
+                 sqS.as<T>(), sigma, ident.as<int64_t>(), Wt.as<T>(), 1, s);
+    if constexpr (std::is_same<T, double>::value)
+      RNLA_CUDA(cudaMemcpyAsync(W.p, Wt.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      copy2d_cast<float, double>(ctx, s, s, Wt.as<float>(), 1, s, W.as<double>(), 1, s);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  EigW e = nystrom_core(ctx, W.as<double>(), s, n, kk);
+  require(k >= 1 && k <= e.kept, "approx_eig: k exceeds rank(L)");
+  DevBuf Tm = whitened(ctx, e, s);  // s x kept
+  // M = T' G T (kept x kept), symmetric
+  const int64_t kp = e.kept;
+  DevBuf GT(sizeof(double) * s * kp, ctx->stream), M(sizeof(double) * kp * kp, ctx->stream),
+      Ms(sizeof(double) * kp * kp, ctx->stream), ev(sizeof(double) * kp, ctx->stream);
+  gemm<double>(ctx, s, kp, s, 1.0, G.as<double>(), 1, s, Tm.as<double>(), 1, s, 0.0, GT.as<double>(), 1, s);
+  gemm<double>(ctx, kp, kp, s, 1.0, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, 0.0, M.as<double>(), 1, kp);
+  symmetrize(ctx, kp, M.as<double>(), Ms.as<double>());
+  eig_sym(ctx, kp, Ms.as<double>(), ev.as<double>());
+  std::vector<double> h((size_t)kp);
+  RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * kp, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t t = 0; t < k; ++t) lam_out[t] = h[(size_t)(kp - 1 - t)];
+  if (u_out) {
+    // P = T V_k diag(1/sigma) (s x k), U = C P, sign-fixed like condensed_svd's U.
+    DevBuf Vk(sizeof(double) * kp * k, ctx->stream), P(sizeof(double) * s * k, ctx->stream),
+        isg(sizeof(double) * k, ctx->stream), Vs(sizeof(double) * kp * k, ctx->stream);
+    copy2d<double>(ctx, kp, k, Ms.as<double>() + (kp - 1) * kp, 1, -kp, Vk.as<double>(), 1, kp);
+    std::vector<double> inv((size_t)k);
+    for (int64_t t = 0; t < k; ++t) inv[(size_t)t] = 1.0 / std::sqrt(h[(size_t)(kp - 1 - t)]);
+    RNLA_CUDA(cudaMemcpyAsync(isg.p, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
+    scale_cols_dev(ctx, kp, k, Vk.as<double>(), isg.as<double>(), Vs.as<double>());
+    gemm<double>(ctx, s, k, kp, 1.0, Tm.as<double>(), 1, s, Vs.as<double>(), 1, kp, 0.0, P.as<double>(), 1, s);
+    OutMat uo(ctx, u_out, n_local, k, "nystrom_eig: U", false);
+    DevBuf U64(sizeof(double) * n_local * k, ctx->stream);
+    DevBuf Pt;
+    if constexpr (!std::is_same<T, double>::value) {
+      Pt = DevBuf(sizeof(float) * s * k, ctx->stream);
+      copy2d_cast<double, float>(ctx, s, k, P.as<double>(), 1, s, Pt.as<float>(), 1, s);
+    }
+    for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
+      const int64_t rows = std::min(blk, n_local - r0);
+      kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows, sqsel);
+      if constexpr (std::is_same<T, double>::value) {
+        gemm<double>(ctx, rows, k, s, 1.0, Cb.as<double>(), 1, rows, P.as<double>(), 1, s, 0.0,
+                     U64.as<double>() + r0, 1, n_local);
+      } else {
+        DevBuf Ub(sizeof(float) * rows * k, ctx->stream);
+        gemm<float>(ctx, rows, k, s, 1.f, Cb.as<float>(), 1, rows, Pt.as<float>(), 1, s, 0.f, Ub.as<float>(), 1,
+                    rows);
+        copy2d_cast<float, double>(ctx, rows, k, Ub.as<float>(), 1, rows, U64.as<double>() + r0, 1, n_local);
+      }
+    }
+    fix_column_signs(ctx, n_local, k, U64.as<double>(), 1, n_local, nullptr, 0, 0, 0, true);
+    store_block(ctx, U64.as<double>(), n_local, k, n_local, uo);
+    uo.finish(ctx);
+  }
+  std::copy(L.sel.begin(), L.sel.end(), selected);
+  *kept_out = kp;
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace
+
+}  // namespace rnla
+
+using namespace rnla;
+
+extern "C" {
+
+rnla_status rnla_rbf_kernel(rnla_ctx* ctx, const rnla_mat* x1, const rnla_mat* x2, double sigma, rnla_mat* k) {
+  return guard([&] {
+    enter(ctx);
+    require(sigma > 0.0, "rbf_kernel: sigma <= 0");
+    check_mat(x1, "rbf_kernel: x1");
+    check_mat(x2, "rbf_kernel: x2");
+    require(x1->cols == x2->cols, "rbf_kernel: dimension mismatch");
+    require(x1->dtype == x2->dtype, "rbf_kernel: dtype mismatch");
+    const int64_t n1 = x1->rows, n2 = x2->rows, d = x1->cols;
+    OutMat o(ctx, k, n1, n2, "rbf_kernel: K", false);
+    require(o.dev.dtype == x1->dtype, "rbf_kernel: output dtype mismatch");
+    DevMat a = to_device(ctx, x1), b = to_device(ctx, x2);
+    if (x1->dtype == RNLA_F64) {
+      DevBuf s1(sizeof(double) * std::max<int64_t>(n1, 1), ctx->stream), s2(sizeof(double) * std::max<int64_t>(n2, 1),
+                                                                              ctx->stream);
+      sq_norms<double>(ctx, n1, d, a.as<double>(), a.rs, a.cs, nullptr, s1.as<double>());
+      sq_norms<double>(ctx, n2, d, b.as<double>(), b.rs, b.cs, nullptr, s2.as<double>());
+      rbf_block<double>(ctx, n1, n2, d, a.as<double>(), a.rs, a.cs, b.as<double>(), b.rs, b.cs, nullptr,
+                        s1.as<double>(), s2.as<double>(), sigma, nullptr, o.dev.as<double>(), o.dev.rs, o.dev.cs);
+    } else {
+      DevBuf s1(sizeof(float) * std::max<int64_t>(n1, 1), ctx->stream), s2(sizeof(float) * std::max<int64_t>(n2, 1),
+                                                                             ctx->stream);
+      sq_norms<float>(ctx, n1, d, a.as<float>(), a.rs, a.cs, nullptr, s1.as<float>());
+      sq_norms<float>(ctx, n2, d, b.as<float>(), b.rs, b.cs, nullptr, s2.as<float>());
+      rbf_block<float>(ctx, n1, n2, d, a.as<float>(), a.rs, a.cs, b.as<float>(), b.rs, b.cs, nullptr, s1.as<float>(),
+                       s2.as<float>(), sigma, nullptr, o.dev.as<float>(), o.dev.rs, o.dev.cs);
+    }
+    o.finish(ctx);
+  });
+}
+
+rnla_status rnla_nystrom(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed, int64_t target_k,
+                         rnla_mat* l, int64_t* selected, int64_t* kept, int64_t* entries) {
+  return guard([&] {
+    enter(ctx);
+    require(sigma > 0.0, "KernelView: sigma <= 0");
+    check_mat(x, "nystrom: x");
+    require(selected && kept, "nystrom: null output");
+    if (x->dtype == RNLA_F64) nystrom_impl<double>(ctx, x, sigma, s, seed, target_k, l, selected, kept, entries);
+    else nystrom_impl<float>(ctx, x, sigma, s, seed, target_k, l, selected, kept, entries);
+  });
+}
+
+rnla_status rnla_approx_eig(rnla_ctx* ctx, const rnla_mat* l, int64_t k, rnla_mat* u, double* lam) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(l, "approx_eig: l");
+    require(k >= 1 && k <= l->cols, "approx_eig: k > cols(L)");
+    require(lam != nullptr, "approx_eig: null output");
+    const int64_t m = l->rows, n = l->cols;
+    DevMat w = f64_colmajor(ctx, l);
+    SvdDev f = condensed_svd_dev(ctx, m, n, w.as<double>(), w.rs, w.cs);
+    if (k > f.rank) throw InvalidArgument("approx_eig: k exceeds rank(L)");
+    OutMat uo(ctx, u, m, k, "approx_eig: U", false);
+    store_block(ctx, f.U.as<double>(), m, k, m, uo);
+    for (int64_t i = 0; i < k; ++i) lam[i] = f.s[(size_t)i] * f.s[(size_t)i];
+    uo.finish(ctx);
+  });
+}
+
+rnla_status rnla_nystrom_eig(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed,
+                             int64_t target_k, int64_t k, rnla_mat* u, double* lam, int64_t* selected,
+                             int64_t* kept) {
+  return guard([&] {
+    enter(ctx);
+    require(sigma > 0.0, "KernelView: sigma <= 0");
+    check_mat(x, "nystrom_eig: x");
+    require(lam && selected && kept, "nystrom_eig: null output");
+    require(k >= 1, "approx_eig: k > cols(L)");
+    if (x->dtype == RNLA_F64) nystrom_eig_impl<double>(ctx, x, sigma, s, seed, target_k, k, u, lam, selected, kept);
+    else nystrom_eig_impl<float>(ctx, x, sigma, s, seed, target_k, k, u, lam, selected, kept);
+  });
+}
+
+}  // extern "C"

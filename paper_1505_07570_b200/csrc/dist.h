@@ -1,0 +1,13 @@
+// dist.h -- collectives for row-sharded contexts (no-ops when world == 1).
+#pragma once
+#include "rnla_internal.h"
+
+namespace rnla {
+
+// In-place sum over ranks of a device buffer (NCCL, on ctx->stream).
+void allreduce_sum(rnla_ctx* ctx, void* buf, size_t count, int dtype);
+// Global index of this rank's first row given every rank's local row count.
+int64_t global_row_offset(rnla_ctx* ctx, int64_t local_rows, int64_t* total_rows);
+double allreduce_scalar(rnla_ctx* ctx, double v);
+
+}  // namespace rnla

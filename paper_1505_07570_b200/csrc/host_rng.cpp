@@ -1,0 +1,94 @@
+// host_rng.cpp -- operator generation on the host, through libstdc++ <random>
+// exactly as the reference draws it (mt19937_64 + normal /
+// uniform distributions are sequential and rejection-based, so Omega, SRHT
+// signs/indices and sampled indices are drawn here and uploaded; only the
+// counter-based CountSketch hash is evaluated on the device).
+//
+// Reference call sites (under /root/reference/proj):
+//   include/randnla/rng.hpp:13-28, src/rng.cpp:8-65, src/sketch.cpp:57-65.
+#include <algorithm>
+#include <numeric>
+#include <random>
+
+#include "rnla_internal.h"
+
+namespace rnla {
+
+uint64_t splitmix64(uint64_t& state) {
+  uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t derive_seed(uint64_t seed, uint64_t stream) {
+  uint64_t s = seed ^ (0x6a09e667f3bcc909ULL + stream * 0x9e3779b97f4a7c15ULL);
+  return splitmix64(s);
+}
+
+int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p *= 2;
+  return p;
+}
+
+// One fresh normal_distribution per call, column-major fill (src/rng.cpp:8-14).
+void gaussian_matrix_host(uint64_t seed, int64_t rows, int64_t cols, double* out) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> normal(0.0, 1.0);
+  for (int64_t j = 0; j < cols; ++j)
+    for (int64_t i = 0; i < rows; ++i) out[j * rows + i] = normal(rng);
+}
+
+static std::vector<int64_t> swor(std::mt19937_64& rng, int64_t n, int64_t count) {
+  require(count >= 0 && count <= n, "sample_without_replacement: count > n");
+  std::vector<long> idx(static_cast<size_t>(n));
+  std::iota(idx.begin(), idx.end(), 0L);
+  for (int64_t i = 0; i < count; ++i) {
+    std::uniform_int_distribution<long> pick(i, n - 1);  // fresh per step (src/rng.cpp:33-35)
+    std::swap(idx[static_cast<size_t>(i)], idx[static_cast<size_t>(pick(rng))]);
+  }
+  idx.resize(static_cast<size_t>(count));
+  std::sort(idx.begin(), idx.end());
+  return std::vector<int64_t>(idx.begin(), idx.end());
+}
+
+std::vector<int64_t> sample_without_replacement_host(uint64_t seed, int64_t n, int64_t count) {
+  std::mt19937_64 rng(seed);
+  return swor(rng, n, count);
+}
+
+std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w, int64_t n, int64_t count) {
+  require(count >= 1, "sample_with_replacement: count < 1");
+  std::vector<double> cum(static_cast<size_t>(n));
+  double total = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    require(w[i] >= 0.0, "sample_with_replacement: negative weight");
+    total += w[i];
+    cum[static_cast<size_t>(i)] = total;
+  }
+  require(total > 0.0, "sample_with_replacement: all weights zero");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(0.0, total);
+  std::vector<int64_t> out(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) {
+    const double u = unif(rng);
+    int64_t j = static_cast<int64_t>(std::upper_bound(cum.begin(), cum.end(), u) - cum.begin());
+    if (j >= n) j = n - 1;
+    out[static_cast<size_t>(i)] = j;
+  }
+  return out;
+}
+
+// Signs first, then the index sample, from one engine (src/sketch.cpp:61-65).
+void srht_operator_host(uint64_t seed, int64_t n, int64_t s, int8_t* signs, int64_t* idx) {
+  const int64_t big_n = next_pow2(n);
+  require(s >= 1 && s <= big_n, "srht_sketch: s > padded dimension");
+  std::mt19937_64 rng(seed);
+  std::uniform_int_distribution<int> coin(0, 1);
+  for (int64_t j = 0; j < n; ++j) signs[j] = coin(rng) ? 1 : -1;
+  std::vector<int64_t> v = swor(rng, big_n, s);
+  std::copy(v.begin(), v.end(), idx);
+}
+
+}  // namespace rnla

@@ -1,0 +1,177 @@
+// linalg.cu -- the small dense factorizations on the device.
+//
+// The reference does all of them with Eigen on the host
+// (src/core.cpp:15-88: HouseholderQR, BDCSVD; src/spsd.cpp:195:
+// SelfAdjointEigenSolver). Here they run on the GPU in fp64 through cuSOLVER
+// (acceptable for the small s x s / c x c factorizations), plus
+// the reference's sign convention (fix_column_signs, src/core.cpp:15-33) as a
+// kernel. Inputs of the fp32 paths are promoted to fp64 for these steps.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include "linalg.cuh"
+#include "util.cuh"
+
+namespace rnla {
+
+namespace {
+
+void cusolver_check(cusolverStatus_t s, const char* what) {
+  if (s != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string(what) + ": cuSOLVER status " + std::to_string((int)s));
+}
+
+cusolverDnHandle_t solver(rnla_ctx* ctx) { return static_cast<cusolverDnHandle_t>(ctx->cusolver); }
+
+void check_info(rnla_ctx* ctx, const DevBuf& info, const char* what) {
+  int h = 0;
+  RNLA_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h != 0) throw NumericError(std::string(what) + ": info = " + std::to_string(h));
+}
+
+// One CTA per column: the first entry with |m| > tol decides the sign
+// (src/core.cpp:15-33); flips the column of M and column/row j of P.
+__global__ void fix_signs_kernel(int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
+                                 int64_t p_rs, int64_t p_cs, int64_t p_len, int pair_cols, double tol) {
+  const int64_t j = blockIdx.x;
+  if (j >= cols) return;
+  __shared__ int64_t first;
+  if (threadIdx.x == 0) first = INT64_MAX;
+  __syncthreads();
+  int64_t mine = INT64_MAX;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x)
+    if (fabs(M[i * m_rs + j * m_cs]) > tol) { mine = i; break; }
+  if (mine != INT64_MAX) atomicMin((unsigned long long*)&first, (unsigned long long)mine);
+  __syncthreads();
+  if (first == INT64_MAX) return;
+  const double lead = M[first * m_rs + j * m_cs];
+  __syncthreads();
+  if (!(lead < 0.0)) return;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) M[i * m_rs + j * m_cs] = -M[i * m_rs + j * m_cs];
+  if (P)
+    for (int64_t i = threadIdx.x; i < p_len; i += blockDim.x) {
+      double* q = pair_cols ? &P[i * p_rs + j * p_cs] : &P[j * p_rs + i * p_cs];
+      *q = -*q;
+    }
+}
+
+__global__ void upper_copy_kernel(int64_t n, const double* __restrict__ A, int64_t lda, double* R, int64_t r_rs,
+                                  int64_t r_cs) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    R[i * r_rs + j * r_cs] = i <= j ? A[i + j * lda] : 0.0;  // exact zeros below the diagonal
+  }
+}
+
+}  // namespace
+
+void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
+                      int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols) {
+  if (cols == 0) return;
+  fix_signs_kernel<<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, P, p_rs, p_cs, p_len,
+                                                            pair_cols ? 1 : 0, 1e-12);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+void qr_householder(rnla_ctx* ctx, int64_t m, int64_t n, double* A, double* R, int64_t r_rs, int64_t r_cs) {
+  require(m >= n, "thin_qr: rows < cols");
+  if (n == 0) return;
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0, lwork2 = 0;
+  DevBuf tau(sizeof(double) * n, ctx->stream), info(sizeof(int), ctx->stream);
+  cusolver_check(cusolverDnDgeqrf_bufferSize(h, (int)m, (int)n, A, (int)m, &lwork), "geqrf_bufferSize");
+  cusolver_check(cusolverDnDorgqr_bufferSize(h, (int)m, (int)n, (int)n, A, (int)m, tau.as<double>(), &lwork2),
+                 "orgqr_bufferSize");
+  DevBuf work(sizeof(double) * std::max(lwork, lwork2), ctx->stream);
+  cusolver_check(cusolverDnDgeqrf(h, (int)m, (int)n, A, (int)m, tau.as<double>(), work.as<double>(), lwork,
+                                  info.as<int>()),
+                 "geqrf");
+  note_launch(ctx);
+  upper_copy_kernel<<<grid_for(ctx, n * n, 256), 256, 0, ctx->stream>>>(n, A, m, R, r_rs, r_cs);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  cusolver_check(cusolverDnDorgqr(h, (int)m, (int)n, (int)n, A, (int)m, tau.as<double>(), work.as<double>(),
+                                  std::max(lwork, lwork2), info.as<int>()),
+                 "orgqr");
+  note_launch(ctx);
+  check_info(ctx, info, "thin_qr");
+}
+
+void svd_thin(rnla_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t a_rs, int64_t a_cs, double* U, double* S,
+              double* V) {
+  // U: m x r col-major (ld m), S[r], V: n x r col-major (ld n), r = min(m, n).
+  const bool tall = m >= n;
+  const int64_t M = tall ? m : n, N = tall ? n : m;  // factor the tall orientation
+  DevBuf work_a(sizeof(double) * M * N, ctx->stream);
+  double* W = work_a.as<double>();
+  if (tall) copy2d<double>(ctx, m, n, A, a_rs, a_cs, W, 1, M);
+  else copy2d<double>(ctx, n, m, A, a_cs, a_rs, W, 1, M);  // W = A^T
+  DevBuf u(sizeof(double) * M * N, ctx->stream), vt(sizeof(double) * N * N, ctx->stream);
+  DevBuf info(sizeof(int), ctx->stream);
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0;
+  cusolver_check(cusolverDnDgesvd_bufferSize(h, (int)M, (int)N, &lwork), "gesvd_bufferSize");
+  DevBuf work(sizeof(double) * lwork, ctx->stream), rwork(sizeof(double) * N, ctx->stream);
+  cusolver_check(cusolverDnDgesvd(h, 'S', 'S', (int)M, (int)N, W, (int)M, S, u.as<double>(), (int)M, vt.as<double>(),
+                                  (int)N, work.as<double>(), lwork, rwork.as<double>(), info.as<int>()),
+                 "gesvd");
+  note_launch(ctx);
+  check_info(ctx, info, "condensed_svd");
+  // Tall: U = u (m x n), V = vt^T. Wide: A^T = u S vt => A = vt^T S u^T: U = vt^T, V = u.
+  if (tall) {
+    copy2d<double>(ctx, m, N, u.as<double>(), 1, M, U, 1, m);
+    copy2d<double>(ctx, n, N, vt.as<double>(), N, 1, V, 1, n);  // V(i,j) = vt(j,i)
+  } else {
+    copy2d<double>(ctx, m, N, vt.as<double>(), N, 1, U, 1, m);
+    copy2d<double>(ctx, n, N, u.as<double>(), 1, M, V, 1, n);
+  }
+}
+
+bool cholesky_upper(rnla_ctx* ctx, int64_t n, double* G) {
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0;
+  DevBuf info(sizeof(int), ctx->stream);
+  cusolver_check(cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, (int)n, G, (int)n, &lwork),
+                 "potrf_bufferSize");
+  DevBuf work(sizeof(double) * std::max(lwork, 1), ctx->stream);
+  cusolver_check(cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, (int)n, G, (int)n, work.as<double>(), lwork,
+                                  info.as<int>()),
+                 "potrf");
+  note_launch(ctx);
+  int hinfo = 0;
+  RNLA_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return hinfo == 0;
+}
+
+void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv) {
+  // Rinv = R^-1 by a triangular solve against the identity (lower part zero).
+  std::vector<double> eye((size_t)(n * n), 0.0);
+  for (int64_t i = 0; i < n; ++i) eye[(size_t)(i + i * n)] = 1.0;
+  RNLA_CUDA(cudaMemcpyAsync(Rinv, eye.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+  const double one = 1.0;
+  if (cublasDtrsm(static_cast<cublasHandle_t>(ctx->cublas), CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                  CUBLAS_DIAG_NON_UNIT, (int)n, (int)n, &one, R, (int)n, Rinv, (int)n) != CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDtrsm failed");
+  note_launch(ctx);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W) {
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0;
+  DevBuf info(sizeof(int), ctx->stream);
+  cusolver_check(cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, W,
+                                             &lwork),
+                 "syevd_bufferSize");
+  DevBuf work(sizeof(double) * lwork, ctx->stream);
+  cusolver_check(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, W,
+                                  work.as<double>(), lwork, info.as<int>()),
+                 "syevd");
+  note_launch(ctx);
+  check_info(ctx, info, "eig");
+}
+
+}  // namespace rnla

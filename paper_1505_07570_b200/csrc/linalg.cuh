@@ -1,0 +1,28 @@
+// linalg.cuh -- small dense factorizations on the device (linalg.cu).
+#pragma once
+#include "rnla_internal.h"
+
+namespace rnla {
+
+// fix_column_signs (src/core.cpp:15-33) on column-major-or-strided M (rows x cols):
+// flips column j of M, and column j (pair_cols) or row j of P (p_len entries).
+void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
+                      int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols);
+
+// Householder thin QR of column-major A (m x n, ld m), in place: A <- Q;
+// R (n x n, upper, exact zeros below) written with strides (r_rs, r_cs).
+void qr_householder(rnla_ctx* ctx, int64_t m, int64_t n, double* A, double* R, int64_t r_rs, int64_t r_cs);
+
+// Thin SVD: U m x r (col-major, ld m), S[r] descending, V n x r (col-major, ld n), r = min(m, n).
+void svd_thin(rnla_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t a_rs, int64_t a_cs, double* U, double* S,
+              double* V);
+
+// In-place upper Cholesky G = R'R of column-major G (n x n); false if not positive definite.
+bool cholesky_upper(rnla_ctx* ctx, int64_t n, double* G);
+// Rinv = R^-1 for upper-triangular column-major R (entries below the diagonal ignored).
+void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv);
+
+// Symmetric eigen-decomposition of column-major A (n x n): A <- eigenvectors, W ascending.
+void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W);
+
+}  // namespace rnla

@@ -1,0 +1,226 @@
+// rbf.cu -- fused RBF kernel blocks, squared row norms, column gathers and
+// row-norm reductions.
+//
+// Reference: rbf_kernel / KernelView::entry (/root/reference/proj/src/spsd.cpp:33-64):
+//   K_ij = exp((x_i . y_j - 0.5 * (|x_i|^2 + |y_j|^2)) * (1 / sigma^2)).
+// Dots and squared norms use the SAME sequential fused-multiply-add chain
+// over the feature index, so x_i . x_i == |x_i|^2 bitwise: the diagonal is
+// exactly exp(0) = 1 and K is bitwise symmetric, as the reference's tests
+// require (tests/test_spsd.cpp:20-45).
+#include "rbf.cuh"
+#include "util.cuh"
+
+namespace rnla {
+
+namespace {
+
+template <class T>
+__device__ __forceinline__ T fma_t(T a, T b, T c);
+template <>
+__device__ __forceinline__ double fma_t<double>(double a, double b, double c) { return fma(a, b, c); }
+template <>
+__device__ __forceinline__ float fma_t<float>(float a, float b, float c) { return fmaf(a, b, c); }
+
+template <class T>
+__device__ __forceinline__ T exp_t(T v);
+template <>
+__device__ __forceinline__ double exp_t<double>(double v) { return exp(v); }
+template <>
+__device__ __forceinline__ float exp_t<float>(float v) { return expf(v); }
+
+template <class T>
+__global__ void sqnorm_kernel(int64_t n, int64_t d, const T* __restrict__ X, int64_t rs, int64_t cs,
+                              const int64_t* __restrict__ rows, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows ? rows[i] : i;
+    const T* x = X + r * rs;
+    T acc = T(0);
+    for (int64_t k = 0; k < d; ++k) acc = fma_t<T>(x[k * cs], x[k * cs], acc);
+    out[i] = acc;
+  }
+}
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+// K(i, j) for i < n1, j < n2, with Y rows optionally indirect (ysel).
+// 256 threads, each 4 x 4 outputs (rows ty + 16a, cols tx + 16b).
+template <class T>
+__global__ void __launch_bounds__(256) rbf_tile_kernel(int64_t n1, int64_t n2, int64_t d, const T* __restrict__ X,
+                                                       int64_t x_rs, int64_t x_cs, const T* __restrict__ Y,
+                                                       int64_t y_rs, int64_t y_cs, const int64_t* __restrict__ ysel,
+                                                       const T* __restrict__ sqx, const T* __restrict__ sqy, T inv,
+                                                       const int64_t* __restrict__ diag_of, T* __restrict__ K,
+                                                       int64_t k_rs, int64_t k_cs) {
+  __shared__ T xs[TK][TM + 1];
+  __shared__ T ys[TK][TN + 1];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t i0 = (int64_t)blockIdx.y * TM, j0 = (int64_t)blockIdx.x * TN;
+  T acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
+  for (int64_t k0 = 0; k0 < d; k0 += TK) {
+    for (int e = tid; e < TK * TM; e += 256) {
+      const int r = e / TK, k = e % TK;
+      const int64_t gi = i0 + r, gk = k0 + k;
+      xs[k][r] = (gi < n1 && gk < d) ? X[gi * x_rs + gk * x_cs] : T(0);
+      const int64_t gj = j0 + r;
+      const int64_t yr = (gj < n2) ? (ysel ? ysel[gj] : gj) : 0;
+      ys[k][r] = (gj < n2 && gk < d) ? Y[yr * y_rs + gk * y_cs] : T(0);
+    }
+    __syncthreads();
+    const int kmax = (d - k0) < TK ? (int)(d - k0) : TK;
+    for (int k = 0; k < kmax; ++k) {
+      T xv[4], yv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xv[a] = xs[k][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) yv[b] = ys[k][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma_t<T>(xv[a], yv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      if (i < n1 && j < n2) {
+        T v;
+        if (diag_of && diag_of[j] == i) v = T(1);  // same point: exp(0)
+        else v = exp_t<T>((acc[a][b] - T(0.5) * (sqx[i] + sqy[j])) * inv);
+        K[i * k_rs + j * k_cs] = v;
+      }
+    }
+}
+
+template <class T>
+__global__ void gather_cols_kernel(int64_t rows, int64_t cnt, const T* __restrict__ A, int64_t a_rs, int64_t a_cs,
+                                   const int64_t* __restrict__ idx, const double* __restrict__ scale, T* __restrict__ C,
+                                   int64_t c_rs, int64_t c_cs) {
+  const int64_t total = rows * cnt;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, t = e / rows;
+    T v = A[i * a_rs + idx[t] * a_cs];
+    if (scale) v = (T)((double)v * scale[t]);
+    C[i * c_rs + t * c_cs] = v;
+  }
+}
+
+// out[i] = sum_c M(i, c)^2 in fp64 (one warp per row).
+template <class T>
+__global__ void row_sqnorm_kernel(int64_t n, int64_t d, const T* __restrict__ M, int64_t rs, int64_t cs,
+                                  double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * nw + warp; i < n; i += (int64_t)gridDim.x * nw) {
+    double acc = 0.0;
+    for (int64_t c = lane; c < d; c += 32) {
+      const double v = (double)M[i * rs + c * cs];
+      acc += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+}  // namespace
+
+template <class T>
+void sq_norms(rnla_ctx* ctx, int64_t n, int64_t d, const T* X, int64_t rs, int64_t cs, const int64_t* rows, T* out) {
+  if (n == 0) return;
+  sqnorm_kernel<T><<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(n, d, X, rs, cs, rows, out);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+template <class T>
+void rbf_block(rnla_ctx* ctx, int64_t n1, int64_t n2, int64_t d, const T* X, int64_t x_rs, int64_t x_cs, const T* Y,
+               int64_t y_rs, int64_t y_cs, const int64_t* ysel, const T* sqx, const T* sqy, double sigma,
+               const int64_t* diag_of, T* K, int64_t k_rs, int64_t k_cs) {
+  if (n1 == 0 || n2 == 0) return;
+  const T inv = (T)(1.0 / (sigma * sigma));
+  dim3 grid((unsigned)((n2 + TN - 1) / TN), (unsigned)((n1 + TM - 1) / TM));
+  rbf_tile_kernel<T><<<grid, 256, 0, ctx->stream>>>(n1, n2, d, X, x_rs, x_cs, Y, y_rs, y_cs, ysel, sqx, sqy, inv,
+                                                    diag_of, K, k_rs, k_cs);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+template <class T>
+void gather_columns(rnla_ctx* ctx, int64_t rows, int64_t cnt, const T* A, int64_t a_rs, int64_t a_cs,
+                    const int64_t* idx, const double* scale, T* C, int64_t c_rs, int64_t c_cs) {
+  if (rows == 0 || cnt == 0) return;
+  gather_cols_kernel<T><<<grid_for(ctx, rows * cnt, 256), 256, 0, ctx->stream>>>(rows, cnt, A, a_rs, a_cs, idx, scale,
+                                                                                 C, c_rs, c_cs);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+template <class T>
+void row_sqnorms(rnla_ctx* ctx, int64_t n, int64_t d, const T* M, int64_t rs, int64_t cs, double* out) {
+  if (n == 0) return;
+  row_sqnorm_kernel<T><<<grid_for(ctx, n, 8), 256, 0, ctx->stream>>>(n, d, M, rs, cs, out);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+#define RNLA_INST(T)                                                                                              \
+  template void sq_norms<T>(rnla_ctx*, int64_t, int64_t, const T*, int64_t, int64_t, const int64_t*, T*);        \
+  template void rbf_block<T>(rnla_ctx*, int64_t, int64_t, int64_t, const T*, int64_t, int64_t, const T*, int64_t, \
+                             int64_t, const int64_t*, const T*, const T*, double, const int64_t*, T*, int64_t,    \
+                             int64_t);                                                                            \
+  template void gather_columns<T>(rnla_ctx*, int64_t, int64_t, const T*, int64_t, int64_t, const int64_t*,       \
+                                  const double*, T*, int64_t, int64_t);                                           \
+  template void row_sqnorms<T>(rnla_ctx*, int64_t, int64_t, const T*, int64_t, int64_t, double*);
+RNLA_INST(double)
+RNLA_INST(float)
+#undef RNLA_INST
+
+}  // namespace rnla
+
+namespace rnla {
+namespace {
+template <class T>
+__global__ void gather_rows_kernel(int64_t cnt, int64_t cols, const T* __restrict__ A, int64_t a_rs, int64_t a_cs,
+                                   const int64_t* __restrict__ idx, T* __restrict__ out, int64_t o_rs, int64_t o_cs) {
+  const int64_t total = cnt * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, c = e % cols;
+    out[i * o_rs + c * o_cs] = A[idx[i] * a_rs + c * a_cs];
+  }
+}
+__global__ void symmetrize_kernel(int64_t n, const double* __restrict__ W, double* __restrict__ out) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    out[e] = 0.5 * (W[i + j * n] + W[j + i * n]);
+  }
+}
+}  // namespace
+
+template <class T>
+void gather_rows(rnla_ctx* ctx, int64_t cnt, int64_t cols, const T* A, int64_t a_rs, int64_t a_cs, const int64_t* idx,
+                 T* out, int64_t o_rs, int64_t o_cs) {
+  if (cnt * cols == 0) return;
+  gather_rows_kernel<T><<<grid_for(ctx, cnt * cols, 256), 256, 0, ctx->stream>>>(cnt, cols, A, a_rs, a_cs, idx, out,
+                                                                                  o_rs, o_cs);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+template void gather_rows<double>(rnla_ctx*, int64_t, int64_t, const double*, int64_t, int64_t, const int64_t*,
+                                  double*, int64_t, int64_t);
+template void gather_rows<float>(rnla_ctx*, int64_t, int64_t, const float*, int64_t, int64_t, const int64_t*, float*,
+                                 int64_t, int64_t);
+
+void symmetrize(rnla_ctx* ctx, int64_t n, const double* W, double* out) {
+  if (n == 0) return;
+  symmetrize_kernel<<<grid_for(ctx, n * n, 256), 256, 0, ctx->stream>>>(n, W, out);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+}  // namespace rnla

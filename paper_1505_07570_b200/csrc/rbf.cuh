@@ -1,0 +1,36 @@
+// rbf.cuh -- RBF kernel blocks and gathers (rbf.cu).
+#pragma once
+#include "rnla_internal.h"
+
+namespace rnla {
+
+// out[i] = |X_r|^2 with r = rows ? rows[i] : i (sequential FMA chain).
+template <class T>
+void sq_norms(rnla_ctx* ctx, int64_t n, int64_t d, const T* X, int64_t rs, int64_t cs, const int64_t* rows, T* out);
+
+// K(i, j) = exp((x_i . y_{sel(j)} - (sqx_i + sqy_j)/2) / sigma^2); entries with
+// diag_of[j] == i are exactly 1 (the same point).
+template <class T>
+void rbf_block(rnla_ctx* ctx, int64_t n1, int64_t n2, int64_t d, const T* X, int64_t x_rs, int64_t x_cs, const T* Y,
+               int64_t y_rs, int64_t y_cs, const int64_t* ysel, const T* sqx, const T* sqy, double sigma,
+               const int64_t* diag_of, T* K, int64_t k_rs, int64_t k_cs);
+
+// C(:, t) = A(:, idx[t]) * (scale ? scale[t] : 1).
+template <class T>
+void gather_columns(rnla_ctx* ctx, int64_t rows, int64_t cnt, const T* A, int64_t a_rs, int64_t a_cs,
+                    const int64_t* idx, const double* scale, T* C, int64_t c_rs, int64_t c_cs);
+
+// out[i] = sum_c M(i, c)^2 (fp64).
+template <class T>
+void row_sqnorms(rnla_ctx* ctx, int64_t n, int64_t d, const T* M, int64_t rs, int64_t cs, double* out);
+
+}  // namespace rnla
+
+namespace rnla {
+// out(i, c) = A(idx[i], c) for i < cnt, c < cols.
+template <class T>
+void gather_rows(rnla_ctx* ctx, int64_t cnt, int64_t cols, const T* A, int64_t a_rs, int64_t a_cs, const int64_t* idx,
+                 T* out, int64_t o_rs, int64_t o_cs);
+// out = 0.5 * (W + W') for column-major n x n fp64 W (src/spsd.cpp:195-196).
+void symmetrize(rnla_ctx* ctx, int64_t n, const double* W, double* out);
+}  // namespace rnla

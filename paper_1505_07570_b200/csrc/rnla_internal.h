@@ -1,0 +1,145 @@
+// rnla_internal.h -- shared internals of librnla_b200 (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "rnla.h"
+
+namespace rnla {
+
+// Exceptions used inside the library; the C ABI layer maps them to status
+// codes (they never cross the boundary).
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NumericError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Mirror of the reference's require() (include/randnla/types.hpp:35-37).
+inline void require(bool cond, const std::string& msg) {
+  if (!cond) throw InvalidArgument(msg);
+}
+
+#define RNLA_CUDA(expr)                                                                       \
+  do {                                                                                        \
+    cudaError_t e__ = (expr);                                                                 \
+    if (e__ != cudaSuccess)                                                                   \
+      throw ::rnla::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e__) + " @" +   \
+                              __FILE__ + ":" + std::to_string(__LINE__));                     \
+  } while (0)
+
+// Device buffer owned by RAII (stream-ordered allocator).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t b, cudaStream_t s) : bytes(b), st(s) {
+    if (b) RNLA_CUDA(cudaMallocAsync(&p, b, s));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p; bytes = o.bytes; st = o.st; o.p = nullptr;
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Cached device-resident operator (hash permutation, Gaussian Omega, ...).
+struct CountSketchPlan {
+  int64_t n = 0, s = 0, j0 = 0;
+  uint64_t seed = 0;
+  DevBuf offsets;  // int64[s + 1]: first slot of each bucket
+  DevBuf rows;     // uint32[n]: local row index | sign bit (bit 31 = negative)
+};
+
+struct SrhtPlan;
+
+struct DenseOperator {  // G / sqrt(s) as the reference forms it, device fp64/fp32
+  DevBuf data;
+  int64_t rows = 0, cols = 0;
+  int dtype = RNLA_F64;
+};
+
+}  // namespace rnla
+
+struct rnla_ctx {
+  int device = 0;
+  int world = 1, rank = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  void* nccl = nullptr;      // ncclComm_t
+  void* cusolver = nullptr;  // cusolverDnHandle_t
+  void* cublas = nullptr;    // cublasHandle_t
+  int num_sms = 148;
+  int64_t launches = 0;
+  std::mutex mu;
+  std::map<std::tuple<int64_t, int64_t, int64_t, uint64_t>, std::unique_ptr<rnla::CountSketchPlan>> cs_plans;
+  std::map<std::tuple<int64_t, int64_t, uint64_t, int>, std::unique_ptr<rnla::DenseOperator>> gauss_ops;
+  std::map<std::tuple<int64_t, int64_t, uint64_t>, std::shared_ptr<rnla::SrhtPlan>> srht_plans;
+};
+
+namespace rnla {
+
+// ---- host operator generation (host_rng.cpp; libstdc++ like the reference) ----
+uint64_t splitmix64(uint64_t& state);
+uint64_t derive_seed(uint64_t seed, uint64_t stream);
+void gaussian_matrix_host(uint64_t seed, int64_t rows, int64_t cols, double* out_colmajor);
+std::vector<int64_t> sample_without_replacement_host(uint64_t seed, int64_t n, int64_t count);
+std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w, int64_t n, int64_t count);
+void srht_operator_host(uint64_t seed, int64_t n, int64_t s, int8_t* signs, int64_t* idx);
+int64_t next_pow2(int64_t n);
+
+// ---- device kernels (launchers; all enqueue on ctx->stream) ----
+// Count sketch of segments: out[b*ldo + c] (+)= sum_{j: h(j0+j)=b, j asc} g * seg_j[c]
+// where seg_j[c] = in[j*ld + c] for c < L and extra[j*extra_stride] for c == L.
+template <class T>
+void count_sketch_segments(rnla_ctx* ctx, const T* in, int64_t ld, const T* extra, int64_t extra_stride, int64_t n,
+                           int64_t L, int64_t s, uint64_t seed, int64_t j0, T* out, int64_t ldo, bool accumulate);
+const CountSketchPlan& count_sketch_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int64_t j0);
+
+// General strided GEMM: C[m x n] = alpha * A[m x k] * B[k x n] + beta * C, element
+// (i, j) of X at X[i*rs + j*cs].
+template <class T>
+void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
+          const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs);
+
+// fp32 operands, exact widening to fp64, DMMA fp64 accumulation (Gram-type products).
+void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
+                     int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
+                     int64_t c_cs);
+
+// Device copy between strided 2-D layouts (also casts f64<->f32 via the typed overloads).
+template <class T>
+void copy2d(rnla_ctx* ctx, int64_t rows, int64_t cols, const T* src, int64_t s_rs, int64_t s_cs, T* dst, int64_t d_rs,
+            int64_t d_cs);
+template <class T>
+void scale_inplace(rnla_ctx* ctx, T* p, int64_t count, double divisor);
+
+inline void note_launch(rnla_ctx* ctx, int64_t k = 1) { ctx->launches += k; }
+
+}  // namespace rnla

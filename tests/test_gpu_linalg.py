@@ -1,0 +1,128 @@
+"""GPU parity of core.hpp / randsvd.hpp against the oracle and the reference's
+own property tests (tests/test_core.cpp, tests/test_randsvd.cpp)."""
+import numpy as np
+import pytest
+
+import paper_1505_07570_b200 as rn
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def test_thin_qr(ctx):
+    a = orc.gaussian_matrix(20, 8, 1)
+    f = rn.thin_qr(a, ctx=ctx)
+    q, r = f.Q, f.R
+    assert np.linalg.norm(q @ r - a) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(q.T @ q - np.eye(8)) <= 1e-12
+    assert np.all(np.tril(r, -1) == 0.0)
+    for j in range(8):
+        nz = np.nonzero(np.abs(q[:, j]) > 1e-12)[0]
+        assert q[nz[0], j] > 0
+    qo, ro = orc.thin_qr(a)
+    assert np.allclose(q, qo, atol=1e-13) and np.allclose(r, ro, atol=1e-12)
+    with pytest.raises(ValueError, match="rows < cols"):
+        rn.thin_qr(orc.gaussian_matrix(3, 5, 2), ctx=ctx)
+
+
+def test_condensed_svd_rank_cut(ctx):
+    a = orc.gaussian_matrix(30, 4, 3) @ orc.gaussian_matrix(4, 25, 4)
+    f = rn.condensed_svd(a, ctx=ctx)
+    assert f.rank() == 4
+    assert np.linalg.norm(f.reconstruct() - a) <= 1e-10 * np.linalg.norm(a)
+    assert np.linalg.norm(f.U.T @ f.U - np.eye(4)) <= 1e-12
+    assert np.linalg.norm(f.V.T @ f.V - np.eye(4)) <= 1e-12
+    assert np.all(np.diff(f.singular_values) <= 0) and f.singular_values[-1] > 0
+    uo, so, vo = orc.condensed_svd(a)
+    assert np.allclose(f.singular_values, so, rtol=1e-12)
+    assert np.allclose(f.U, uo, atol=1e-10) and np.allclose(f.V, vo, atol=1e-10)
+    with pytest.raises(ValueError, match="zero matrix"):
+        rn.condensed_svd(np.zeros((4, 3)), ctx=ctx)
+
+
+@pytest.mark.parametrize("m,n", [(15, 12), (200, 30), (30, 200), (4000, 50)])
+def test_truncated_svd_optimal(ctx, m, n):
+    a = orc.gaussian_matrix(m, n, 5)
+    k = 3
+    f = rn.truncated_svd(a, k, ctx=ctx)
+    assert f.rank() == k
+    sv = np.linalg.svd(a, compute_uv=False)
+    err = np.linalg.norm(a - f.reconstruct()) ** 2
+    assert abs(err - np.sum(sv[k:] ** 2)) <= 1e-10 * np.sum(sv[k:] ** 2)
+
+
+def test_pseudo_inverse(ctx):
+    a = orc.gaussian_matrix(10, 6, 6)
+    p = rn.pseudo_inverse(a, ctx=ctx)
+    assert np.linalg.norm(a @ p @ a - a) <= 1e-10 * np.linalg.norm(a)
+    assert np.linalg.norm(p @ a @ p - p) <= 1e-10 * np.linalg.norm(p)
+    assert np.linalg.norm((a @ p).T - a @ p) <= 1e-10
+    z = rn.pseudo_inverse(np.zeros((4, 7)), ctx=ctx)
+    assert z.shape == (7, 4) and np.linalg.norm(z) == 0.0
+
+
+def test_prototype_exact_rank_k(ctx):
+    # tests/test_randsvd.cpp:39-49
+    a = orc.gaussian_matrix(80, 5, 2) @ orc.gaussian_matrix(5, 60, 22)
+    r = rn.prototype_ksvd(a, 5, 20, 3, opts=rn.KsvdOptions(True), ctx=ctx)
+    assert r.error_fro <= 1e-8 * np.linalg.norm(a)
+    assert r.passes_over_a == 2
+    assert r.factors.U.shape[0] == 80 and r.factors.V.shape[0] == 60
+    assert r.factors.singular_values.size <= 5
+
+
+def test_prototype_error_above_optimum_and_deterministic(ctx):
+    a = orc.gaussian_matrix(50, 50, 4)
+    r = rn.prototype_ksvd(a, 5, 25, 5, opts=rn.KsvdOptions(True), ctx=ctx)
+    sv = np.linalg.svd(a, compute_uv=False)
+    assert r.error_fro >= np.sqrt(np.sum(sv[5:] ** 2)) - 1e-9
+    b = orc.gaussian_matrix(40, 35, 11)
+    r1 = rn.prototype_ksvd(b, 4, 12, 99, ctx=ctx)
+    r2 = rn.prototype_ksvd(b, 4, 12, 99, ctx=ctx)
+    assert np.array_equal(r1.factors.singular_values, r2.factors.singular_values)
+    assert np.array_equal(r1.factors.U, r2.factors.U)
+
+
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_prototype_matches_oracle_same_omega(ctx, q):
+    rng = np.random.default_rng(q)
+    m, n, k, s = 2048, 512, 20, 30
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = np.exp(-np.arange(1, n + 1) / 20.0)
+    a = (u * sig) @ v.T + 1e-3 * rng.standard_normal((m, n))
+    r = rn.prototype_ksvd(dev(a), k, s, 777, power_iters=q, ctx=ctx)
+    uo, so, vo, passes = orc.prototype_ksvd(a, k, s, 777, q=q)
+    assert r.passes_over_a == passes == 2 + 2 * q
+    assert np.max(np.abs(r.factors.singular_values - so) / so) <= 1e-8
+    U = r.factors.U.cpu().numpy()
+    # the well-separated leading vectors agree up to rounding
+    assert np.max(np.abs(np.abs(U[:, :3]) - np.abs(uo[:, :3]))) <= 1e-6
+
+
+def test_prototype_fp32(ctx):
+    rng = np.random.default_rng(3)
+    m, n = 4096, 1024
+    u, _ = np.linalg.qr(rng.standard_normal((m, 256)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, 256)))
+    sig = np.arange(1, 257) ** -1.5
+    a = ((u * sig) @ v.T + 1e-4 * rng.standard_normal((m, n))).astype(np.float32)
+    r = rn.prototype_ksvd(dev(a), 20, 40, 5, power_iters=2, ctx=ctx)
+    _, so, _, _ = orc.prototype_ksvd(a.astype(np.float64), 20, 40, 5, q=2)
+    assert np.max(np.abs(r.factors.singular_values - so) / so) <= 1e-3
+
+
+def test_prototype_count_spec(ctx):
+    a = orc.gaussian_matrix(300, 6, 8) @ orc.gaussian_matrix(6, 200, 9)
+    r = rn.prototype_ksvd(a, 6, 30, 4, spec=rn.SketchSpec.count_sketch(30, 4), opts=rn.KsvdOptions(True), ctx=ctx)
+    assert r.error_fro <= 1e-8 * np.linalg.norm(a)
+
+
+def test_prototype_argument_checks(ctx):
+    with pytest.raises(ValueError, match="k <= s <= min"):
+        rn.prototype_ksvd(np.ones((10, 8)), 5, 9, 1, ctx=ctx)

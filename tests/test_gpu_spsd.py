@@ -1,0 +1,97 @@
+"""GPU parity of spsd.hpp (rbf_kernel, Nystrom, approx_eig) against the
+oracle and the reference's tests/test_spsd.cpp properties."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1505_07570_b200 as rn
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def test_rbf_unit_diagonal_symmetry(ctx):
+    # tests/test_spsd.cpp:20-31: exact unit diagonal, bitwise symmetry
+    x = orc.gaussian_matrix(30, 4, 1)
+    k = rn.rbf_kernel(x, x, 1.5, ctx=ctx)
+    assert np.all(np.diag(k) == 1.0)
+    assert np.linalg.norm(k - k.T) == 0.0
+    assert k.max() <= 1.0 and k.min() >= 0.0
+    d2 = np.sum((x[3] - x[17]) ** 2)
+    assert abs(k[3, 17] - math.exp(-d2 / (2 * 1.5 ** 2))) <= 1e-12 * math.exp(-d2 / (2 * 1.5 ** 2))
+    assert np.max(np.abs(k - orc.rbf_kernel(x, x, 1.5))) <= 1e-13
+
+
+def test_rbf_fp32_and_rectangular(ctx):
+    rng = np.random.default_rng(2)
+    x1 = rng.standard_normal((300, 64)).astype(np.float32) * 3
+    x2 = rng.standard_normal((70, 64)).astype(np.float32) * 3
+    k = rn.rbf_kernel(dev(x1), dev(x2), 20.0, ctx=ctx).cpu().numpy()
+    ref = orc.rbf_kernel(x1.astype(np.float64), x2.astype(np.float64), 20.0)
+    assert np.max(np.abs(k - ref)) <= 1e-5
+    with pytest.raises(ValueError, match="sigma <= 0"):
+        rn.rbf_kernel(x1, x2, 0.0, ctx=ctx)
+
+
+def test_nystrom_matches_oracle(ctx):
+    x = orc.gaussian_matrix(400, 5, 10)
+    view = rn.KernelView(x, rn.KernelSpec(2.0))
+    f = rn.nystrom(view, 40, 11, ctx=ctx)
+    L, sel, lam = orc.nystrom(x, 2.0, 40, 11)
+    assert np.array_equal(f.selected, sel)
+    assert f.L.shape == L.shape
+    assert np.linalg.norm(f.L @ f.L.T - L @ L.T) <= 1e-8 * np.linalg.norm(L @ L.T)
+    assert view.entries_evaluated() == 400 * 40
+    v2 = rn.KernelView(orc.gaussian_matrix(100, 5, 10), rn.KernelSpec(2.0))
+    f2 = rn.nystrom(v2, 10, 11, ctx=ctx)  # default k = ceil(0.8 s)
+    assert f2.L.shape[1] <= 8 and f2.L.shape[0] == 100 and f2.selected.size == 10
+
+
+def test_nystrom_argument_checks(ctx):
+    v = rn.KernelView(orc.gaussian_matrix(20, 3, 1), rn.KernelSpec(1.0))
+    with pytest.raises(ValueError, match="k <= s <= n"):
+        rn.nystrom(v, 30, 1, ctx=ctx)
+    with pytest.raises(ValueError, match="sigma <= 0"):
+        rn.KernelView(np.ones((3, 2)), rn.KernelSpec(0.0))
+
+
+def test_approx_eig(ctx):
+    # tests/test_spsd.cpp:133-142
+    l = orc.gaussian_matrix(30, 6, 17)
+    u, lam = rn.approx_eig(l, 4, ctx=ctx)
+    g = l @ l.T
+    for t in range(4):
+        assert np.linalg.norm(g @ u[:, t] - lam[t] * u[:, t]) <= 1e-8 * lam[t]
+        if t:
+            assert lam[t] <= lam[t - 1]
+    uo, lo = orc.approx_eig(l, 4)
+    assert np.allclose(lam, lo, rtol=1e-12) and np.allclose(u, uo, atol=1e-10)
+
+
+def test_nystrom_eig_gram_route_matches_oracle(ctx):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((3000, 8)) * 2
+    view = rn.KernelView(x, rn.KernelSpec(3.0))
+    u, lam, sel, kept = rn.nystrom_eig(view, 200, 9, 150, 12, ctx=ctx)
+    L, sel_o, _ = orc.nystrom(x, 3.0, 200, 9, 150)
+    uo, lo = orc.approx_eig(L, 12)
+    assert np.array_equal(sel, sel_o) and kept == L.shape[1]
+    assert np.max(np.abs(lam - lo) / lo) <= 1e-8
+    assert np.max(np.abs(np.abs(u[:, :4]) - np.abs(uo[:, :4]))) <= 1e-6
+
+
+def test_nystrom_eig_fp32(ctx):
+    rng = np.random.default_rng(5)
+    means = rng.standard_normal((4, 16)) * 3
+    x = (means[rng.integers(0, 4, 8192)] + rng.standard_normal((8192, 16))).astype(np.float32)
+    view = rn.KernelView(dev(x), rn.KernelSpec(6.0))
+    _, lam, _, _ = rn.nystrom_eig(view, 256, 3, 128, 16, want_vectors=False, ctx=ctx)
+    L, _, _ = orc.nystrom(x.astype(np.float64), 6.0, 256, 3, 128)
+    _, lo = orc.approx_eig(L, 16)
+    assert np.max(np.abs(lam - lo) / lo) <= 1e-3
