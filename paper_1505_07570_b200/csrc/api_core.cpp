@@ -251,6 +251,7 @@ void rnla_ctx_destroy(rnla_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->cs_plans.clear();
   ctx->gauss_ops.clear();
+  ctx->srht_plans.clear();
   cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
@@ -277,6 +278,7 @@ void rnla_ctx_clear_cache(rnla_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->cs_plans.clear();
   ctx->gauss_ops.clear();
+  ctx->srht_plans.clear();
   cudaStreamSynchronize(ctx->stream);
 }
 
