@@ -46,6 +46,18 @@ rnla_status guard(const std::function<void()>& f) {
   }
 }
 
+StreamScope::StreamScope(rnla_ctx* c, cudaStream_t s) : ctx(c), saved(c->stream) {
+  ctx->stream = s;
+  if (ctx->cusolver) cusolverDnSetStream(static_cast<cusolverDnHandle_t>(ctx->cusolver), s);
+  if (ctx->cublas) cublasSetStream(static_cast<cublasHandle_t>(ctx->cublas), s);
+}
+
+StreamScope::~StreamScope() {
+  ctx->stream = saved;
+  if (ctx->cusolver) cusolverDnSetStream(static_cast<cusolverDnHandle_t>(ctx->cusolver), saved);
+  if (ctx->cublas) cublasSetStream(static_cast<cublasHandle_t>(ctx->cublas), saved);
+}
+
 void enter(rnla_ctx* ctx) {
   require(ctx != nullptr, "null rnla_ctx");
   RNLA_CUDA(cudaSetDevice(ctx->device));
@@ -192,6 +204,10 @@ static void ctx_init(rnla_ctx* c, int device) {
   RNLA_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   RNLA_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   RNLA_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  RNLA_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  // Higher priority: its CTAs are dispatched first when the streaming kernel frees SM slots.
+  RNLA_CUDA(cudaStreamCreateWithPriority(&c->aux_stream, cudaStreamNonBlocking, prio_hi));
   cudaMemPool_t pool;
   RNLA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thresh = UINT64_MAX;  // keep freed blocks for reuse across calls
@@ -257,6 +273,7 @@ void rnla_ctx_destroy(rnla_ctx* ctx) {
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   cudaStreamDestroy(ctx->copy_stream);
+  cudaStreamDestroy(ctx->aux_stream);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -60,12 +60,100 @@ std::shared_ptr<SrhtPlan> srht_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_
 // ---- segment-form operators: n segments of length L (segment j at in + j*ld)
 // to s segments (segment t at out + t*out_rs, element c at + c*out_cs). ----
 
+// The Gaussian stage out(t, c) = sum_j Gs(j, t) in(j, c) (A = Gs^T, Gs col-major
+// n x s) is accumulated over canonical K-chunks of kGaussKC segments in
+// chunk order, one GEMM launch per chunk. The standalone call and the
+// pipelined combined sketch (which runs chunk c while the count sketch
+// produces chunk c+1) therefore produce bit-identical results, keeping
+// combined == gaussian(count) exact (tests/test_sketch.cpp:88-98).
+// Canonical K-chunk: the whole K on one GPU (measured: splitting the
+// Gaussian stage under the count sketch does not overlap, the gather kernel
+// holds the register file), s / world on a row-sharded job so each rank
+// multiplies the chunks it owns after a per-chunk ncclReduce.
+static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k) {
+  if (const char* e = std::getenv("RNLA_GAUSS_KC")) return std::max<int64_t>(16, std::atoll(e));
+  const int64_t w = std::max(1, ctx->world);
+  return std::max<int64_t>(16, (k + w - 1) / w);
+}
+template <class T>
+void gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s,
+                    int64_t k0, bool first, T* out, int64_t out_rs, int64_t out_cs) {
+  const int64_t kc = std::min(gauss_kc_for(ctx, n), n - k0);
+  gemm<T>(ctx, s, L, kc, T(1), g.data.as<T>() + k0, n, 1, in + k0 * ld, ld, 1, first ? T(0) : T(1), out, out_rs,
+          out_cs);
+}
+
 template <class T>
 void gaussian_segments(rnla_ctx* ctx, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s, uint64_t seed, T* out,
                        int64_t out_rs, int64_t out_cs) {
   const DenseOperator& g = gaussian_operator(ctx, n, s, seed, std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32);
-  // out(t, c) = sum_j Gs(j, t) * in(j, c): A = Gs^T (s x n), Gs col-major n x s.
-  gemm<T>(ctx, s, L, n, T(1), g.data.as<T>(), n, 1, in, ld, 1, T(0), out, out_rs, out_cs);
+  if (n == 0) {  // empty sum
+    DevBuf z(sizeof(T) * (size_t)std::max<int64_t>(s * L, 1), ctx->stream);
+    RNLA_CUDA(cudaMemsetAsync(z.p, 0, sizeof(T) * (size_t)(s * L), ctx->stream));
+    copy2d<T>(ctx, s, L, z.as<T>(), L, 1, out, out_rs, out_cs);
+    return;
+  }
+  const int64_t kc = gauss_kc_for(ctx, n);
+  for (int64_t k0 = 0; k0 < n; k0 += kc) gaussian_chunk<T>(ctx, g, in, ld, n, L, s, k0, k0 == 0, out, out_rs, out_cs);
+}
+
+// Combined count -> Gaussian row sketch with the Gaussian stage pipelined
+// under the count sketch: bucket chunk c is gathered on the main stream while
+// the aux stream (higher priority) multiplies chunk c-1 on the DMMA units.
+// Row-sharded contexts reduce each finished chunk onto an owner rank
+// (c % world, ncclReduce), the owner multiplies it, and one allreduce of the
+// s2 x Lo result finishes (SURVEY §7 hard part 10).
+template <class T>
+void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int64_t xs, int64_t n,
+                                 int64_t L, const rnla_sketch_spec* spec, int64_t row_offset, T* out, int64_t o_rs,
+                                 int64_t o_cs) {
+  const int dt = std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32;
+  const int64_t Lo = L + (extra ? 1 : 0), s = spec->s, s2 = spec->stage2_s;
+  const DenseOperator& g = gaussian_operator(ctx, s, s2, spec->stage2_seed, dt);
+  if (n > 0) count_sketch_plan(ctx, n, s, spec->seed, row_offset);
+  DevBuf mid(sizeof(T) * (size_t)(s * Lo), ctx->stream);
+  DevBuf acc(sizeof(T) * (size_t)(s2 * Lo), ctx->stream);
+  const int64_t KC = gauss_kc_for(ctx, s);
+  const int64_t chunks = (s + KC - 1) / KC;
+  std::vector<cudaEvent_t> ev((size_t)chunks + 2);
+  for (auto& e : ev) RNLA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t start = ev[(size_t)chunks], done = ev[(size_t)chunks + 1];
+  RNLA_CUDA(cudaEventRecord(start, ctx->stream));
+  RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, start, 0));
+  RNLA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
+  bool first = true;
+  // Gather chunks alternate between two streams so one chunk's last partial
+  // wave overlaps the next chunk instead of draining the GPU.
+  cudaStream_t gather_st[2] = {ctx->stream, ctx->copy_stream};
+  try {
+    for (int64_t c = 0; c < chunks; ++c) {
+      const int64_t b0 = c * KC, b1 = std::min(s, b0 + KC);
+      {
+        StreamScope on_gather(ctx, gather_st[c & 1]);
+        count_sketch_segments<T>(ctx, M, ld, extra, xs, n, L, s, spec->seed, row_offset, mid.as<T>(), Lo, false, b0,
+                                 b1);
+        RNLA_CUDA(cudaEventRecord(ev[(size_t)c], ctx->stream));
+      }
+      RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ev[(size_t)c], 0));
+      StreamScope on_aux(ctx, ctx->aux_stream);
+      const int owner = (int)(c % ctx->world);
+      if (ctx->world > 1) reduce_to(ctx, mid.as<T>() + b0 * Lo, (size_t)((b1 - b0) * Lo), dt, owner);
+      if (owner == ctx->rank) {
+        gaussian_chunk<T>(ctx, g, mid.as<T>(), Lo, s, Lo, s2, b0, first, acc.as<T>(), Lo, 1);
+        first = false;
+      }
+    }
+    if (first) RNLA_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(T) * (size_t)(s2 * Lo), ctx->aux_stream));
+    RNLA_CUDA(cudaEventRecord(done, ctx->aux_stream));
+    RNLA_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+  } catch (...) {
+    cudaStreamSynchronize(ctx->aux_stream);
+    for (auto& e : ev) cudaEventDestroy(e);
+    throw;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);  // destruction is deferred until the events complete
+  if (ctx->world > 1) allreduce_sum(ctx, acc.p, (size_t)(s2 * Lo), dt);
+  copy2d<T>(ctx, s2, Lo, acc.as<T>(), Lo, 1, out, o_rs, o_cs);
 }
 
 template <class T>
@@ -104,6 +192,10 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
   const int64_t Lo = L + (extra ? 1 : 0);
   const int kind = spec->kind;
   const bool sharded = ctx->world > 1;
+  if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN) {
+    combined_gaussian_pipelined<T>(ctx, M, ld, extra, xs, n, L, spec, row_offset, out, o_rs, o_cs);
+    return;
+  }
   if (kind == RNLA_SKETCH_COUNT || kind == RNLA_SKETCH_COMBINED) {
     const int64_t s = spec->s;
     const bool direct = kind == RNLA_SKETCH_COUNT && o_cs == 1;

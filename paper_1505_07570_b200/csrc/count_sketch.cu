@@ -59,12 +59,12 @@ template <class T, int TEAM, int CPT, int U>
 __global__ void __launch_bounds__(128) cs_gather_kernel(const T* __restrict__ in, int64_t ld,
                                                         const T* __restrict__ extra, int64_t extra_stride, int64_t L,
                                                         int64_t Lo, const uint32_t* __restrict__ offsets,
-                                                        const uint32_t* __restrict__ rows, int64_t s,
+                                                        const uint32_t* __restrict__ rows, int64_t b0, int64_t s,
                                                         T* __restrict__ out, int64_t ldo, int accumulate) {
   constexpr int kTeams = 128 / TEAM;
   const int team = threadIdx.x / TEAM;
   const int t = threadIdx.x % TEAM;
-  const int64_t b = (int64_t)blockIdx.x * kTeams + team;
+  const int64_t b = b0 + (int64_t)blockIdx.x * kTeams + team;  // buckets [b0, s) of this launch
   if (b >= s) return;
   const int64_t col0 = (int64_t)blockIdx.y * (TEAM * CPT);
 
@@ -113,12 +113,13 @@ __global__ void __launch_bounds__(128) cs_gather_kernel(const T* __restrict__ in
 
 template <class T, int TEAM, int CPT>
 void launch_gather(rnla_ctx* ctx, const T* in, int64_t ld, const T* extra, int64_t xs, int64_t L, int64_t Lo,
-                   const CountSketchPlan& plan, T* out, int64_t ldo, bool acc) {
+                   const CountSketchPlan& plan, T* out, int64_t ldo, bool acc, int64_t b0, int64_t b1) {
   constexpr int U = (CPT <= 2) ? 8 : (CPT <= 4 ? 6 : 4);
   constexpr int kTeams = 128 / TEAM;
-  dim3 grid((unsigned)((plan.s + kTeams - 1) / kTeams), (unsigned)((Lo + TEAM * CPT - 1) / (TEAM * CPT)));
+  if (b1 <= b0) return;
+  dim3 grid((unsigned)((b1 - b0 + kTeams - 1) / kTeams), (unsigned)((Lo + TEAM * CPT - 1) / (TEAM * CPT)));
   cs_gather_kernel<T, TEAM, CPT, U><<<grid, 128, 0, ctx->stream>>>(
-      in, ld, extra, xs, L, Lo, plan.offsets.as<uint32_t>(), plan.rows.as<uint32_t>(), plan.s, out, ldo, acc ? 1 : 0);
+      in, ld, extra, xs, L, Lo, plan.offsets.as<uint32_t>(), plan.rows.as<uint32_t>(), b0, b1, out, ldo, acc ? 1 : 0);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
@@ -170,27 +171,34 @@ const CountSketchPlan& count_sketch_plan(rnla_ctx* ctx, int64_t n, int64_t s, ui
 
 template <class T>
 void count_sketch_segments(rnla_ctx* ctx, const T* in, int64_t ld, const T* extra, int64_t extra_stride, int64_t n,
-                           int64_t L, int64_t s, uint64_t seed, int64_t j0, T* out, int64_t ldo, bool accumulate) {
+                           int64_t L, int64_t s, uint64_t seed, int64_t j0, T* out, int64_t ldo, bool accumulate,
+                           int64_t b0, int64_t b1) {
   const int64_t Lo = L + (extra ? 1 : 0);
+  if (b1 < 0 || b1 > s) b1 = s;
+  if (b0 < 0) b0 = 0;
+  if (b1 <= b0) return;
   if (n == 0 || Lo == 0) {
     if (!accumulate && Lo > 0) {
-      RNLA_CUDA(cudaMemset2DAsync(out, sizeof(T) * ldo, 0, sizeof(T) * Lo, s, ctx->stream));
+      RNLA_CUDA(cudaMemset2DAsync(out + b0 * ldo, sizeof(T) * ldo, 0, sizeof(T) * Lo, b1 - b0, ctx->stream));
     }
     return;
   }
   const CountSketchPlan& plan = count_sketch_plan(ctx, n, s, seed, j0);
-  if (Lo <= 32) launch_gather<T, 32, 1>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
-  else if (Lo <= 64) launch_gather<T, 32, 2>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
-  else if (Lo <= 128) launch_gather<T, 32, 4>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
-  else if (Lo <= 256) launch_gather<T, 128, 2>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
-  else if (Lo <= 512) launch_gather<T, 128, 4>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
-  else if (Lo <= 640) launch_gather<T, 128, 5>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
-  else launch_gather<T, 128, 8>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate);
+#define RNLA_G(TEAM, CPT) \
+  launch_gather<T, TEAM, CPT>(ctx, in, ld, extra, extra_stride, L, Lo, plan, out, ldo, accumulate, b0, b1)
+  if (Lo <= 32) RNLA_G(32, 1);
+  else if (Lo <= 64) RNLA_G(32, 2);
+  else if (Lo <= 128) RNLA_G(32, 4);
+  else if (Lo <= 256) RNLA_G(128, 2);
+  else if (Lo <= 512) RNLA_G(128, 4);
+  else if (Lo <= 640) RNLA_G(128, 5);
+  else RNLA_G(128, 8);
+#undef RNLA_G
 }
 
 template void count_sketch_segments<double>(rnla_ctx*, const double*, int64_t, const double*, int64_t, int64_t, int64_t,
-                                            int64_t, uint64_t, int64_t, double*, int64_t, bool);
+                                            int64_t, uint64_t, int64_t, double*, int64_t, bool, int64_t, int64_t);
 template void count_sketch_segments<float>(rnla_ctx*, const float*, int64_t, const float*, int64_t, int64_t, int64_t,
-                                           int64_t, uint64_t, int64_t, float*, int64_t, bool);
+                                           int64_t, uint64_t, int64_t, float*, int64_t, bool, int64_t, int64_t);
 
 }  // namespace rnla

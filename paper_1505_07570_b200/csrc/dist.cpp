@@ -17,6 +17,13 @@ void allreduce_sum(rnla_ctx* ctx, void* buf, size_t count, int dtype) {
              "ncclAllReduce");
 }
 
+void reduce_to(rnla_ctx* ctx, void* buf, size_t count, int dtype, int root) {
+  if (ctx->world <= 1 || count == 0) return;
+  nccl_check(ncclReduce(buf, buf, count, dtype == RNLA_F64 ? ncclFloat64 : ncclFloat32, ncclSum, root,
+                        static_cast<ncclComm_t>(ctx->nccl), ctx->stream),
+             "ncclReduce");
+}
+
 int64_t global_row_offset(rnla_ctx* ctx, int64_t local_rows, int64_t* total_rows) {
   if (ctx->world <= 1) {
     if (total_rows) *total_rows = local_rows;

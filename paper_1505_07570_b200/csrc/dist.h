@@ -6,6 +6,8 @@ namespace rnla {
 
 // In-place sum over ranks of a device buffer (NCCL, on ctx->stream).
 void allreduce_sum(rnla_ctx* ctx, void* buf, size_t count, int dtype);
+// In-place sum over ranks onto `root` (NCCL, on ctx->stream).
+void reduce_to(rnla_ctx* ctx, void* buf, size_t count, int dtype, int root);
 // Global index of this rank's first row given every rank's local row count.
 int64_t global_row_offset(rnla_ctx* ctx, int64_t local_rows, int64_t* total_rows);
 double allreduce_scalar(rnla_ctx* ctx, double v);

@@ -241,7 +241,7 @@ __global__ void splitk_reduce(int64_t m, int64_t n, int splits, const T* __restr
 
 template <class T>
 void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
-          const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs) {
+          const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs, int max_splits) {
   if (m == 0 || n == 0) return;
   const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   // Split K until there are ~4 CTAs per SM, keeping >= 256 k per split.
@@ -250,7 +250,7 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
   if (tiles < want && k >= 512) {
     splits = std::min<int64_t>((want + tiles - 1) / tiles, k / 256);
     splits = std::max<int64_t>(splits, 1);
-    splits = std::min<int64_t>(splits, 64);
+    splits = std::min<int64_t>(splits, std::max(1, max_splits));
   }
   int64_t kchunk = (k + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
@@ -312,8 +312,8 @@ void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alph
 }
 
 template void gemm<double>(rnla_ctx*, int64_t, int64_t, int64_t, double, const double*, int64_t, int64_t,
-                           const double*, int64_t, int64_t, double, double*, int64_t, int64_t);
+                           const double*, int64_t, int64_t, double, double*, int64_t, int64_t, int);
 template void gemm<float>(rnla_ctx*, int64_t, int64_t, int64_t, float, const float*, int64_t, int64_t, const float*,
-                          int64_t, int64_t, float, float*, int64_t, int64_t);
+                          int64_t, int64_t, float, float*, int64_t, int64_t, int);
 
 }  // namespace rnla

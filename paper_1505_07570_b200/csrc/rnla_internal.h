@@ -92,6 +92,7 @@ struct rnla_ctx {
   int world = 1, rank = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // concurrent compute (e.g. Gaussian stage under the count sketch)
   void* nccl = nullptr;      // ncclComm_t
   void* cusolver = nullptr;  // cusolverDnHandle_t
   void* cublas = nullptr;    // cublasHandle_t
@@ -119,14 +120,23 @@ int64_t next_pow2(int64_t n);
 // where seg_j[c] = in[j*ld + c] for c < L and extra[j*extra_stride] for c == L.
 template <class T>
 void count_sketch_segments(rnla_ctx* ctx, const T* in, int64_t ld, const T* extra, int64_t extra_stride, int64_t n,
-                           int64_t L, int64_t s, uint64_t seed, int64_t j0, T* out, int64_t ldo, bool accumulate);
+                           int64_t L, int64_t s, uint64_t seed, int64_t j0, T* out, int64_t ldo, bool accumulate,
+                           int64_t b0 = 0, int64_t b1 = -1);
 const CountSketchPlan& count_sketch_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int64_t j0);
 
 // General strided GEMM: C[m x n] = alpha * A[m x k] * B[k x n] + beta * C, element
 // (i, j) of X at X[i*rs + j*cs].
 template <class T>
 void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
-          const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs);
+          const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs, int max_splits = 64);
+
+// Temporarily route ctx launches to another stream (RAII).
+struct StreamScope {
+  rnla_ctx* ctx;
+  cudaStream_t saved;
+  StreamScope(rnla_ctx* c, cudaStream_t s);
+  ~StreamScope();
+};
 
 // fp32 operands, exact widening to fp64, DMMA fp64 accumulation (Gram-type products).
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
