@@ -243,6 +243,12 @@ template <class T>
 void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
           const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs, int max_splits) {
   if (m == 0 || n == 0) return;
+  if constexpr (std::is_same<T, float>::value) {
+    if (tc_gemm_enabled()) {  // fp32: tcgen05 BF16x3 (gemm_tc.cu)
+      gemm_f32_tc(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs);
+      return;
+    }
+  }
   const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   // Split K until there are ~4 CTAs per SM, keeping >= 256 k per split.
   int64_t splits = 1;

@@ -1,0 +1,353 @@
+// gemm_tc.cu -- fp32 GEMM on the 5th-generation tensor cores (tcgen05, TMEM)
+// with the BF16x3 split: x = hi + lo (hi = bf16(x), lo = bf16(x - hi)),
+// A*B ~= Ahi*Bhi + Ahi*Blo + Alo*Bhi, fp32 accumulation in TMEM.
+//
+// Used for the fp32 projections of BASELINE configs 2-4 (rSVD A*Omega,
+// A'*Q, A*Z, Q'*A; Gram products). The split costs 3 MMAs but keeps the
+// relative error at ~1e-6 (SURVEY §7 hard part 5 measured 4.4e-6 rel-F at the
+// config 3 shape; 1-pass BF16 2.3e-3 and 1-pass TF32 2.9e-4 fail the 1e-4
+// gate), at an effective 1/3 of the BF16 tensor peak (~550 TF measured).
+//
+// CTA = one 128 x BN output tile (BN <= 256, multiple of 16) over a K range:
+//   warps 0-7  : producers -- load fp32 A/B tiles (64 k per stage) from global,
+//                split to bf16 hi/lo and store them in the canonical K-major
+//                SWIZZLE_128B smem layout; mbarrier `full[stage]`;
+//   warp 8     : one elected lane issues 4 k-steps x 3 tcgen05.mma
+//                (kind::f16, M=128, N=BN, K=16) per stage and commits to
+//                `empty[stage]`; a final commit signals the epilogue;
+//   warps 8-11 : epilogue -- tcgen05.ld (32x32b) from TMEM, alpha/beta, store.
+// Global operands may be K-contiguous or MN-contiguous; the converting
+// loader always produces K-major smem, so only the K-major descriptor is used.
+// The fp32 data is read through registers because it has to be split before
+// the MMA anyway (a TMA copy would add an smem round trip).
+#include <cuda_bf16.h>
+
+#include "rnla_internal.h"
+#include "util.cuh"
+
+namespace rnla {
+
+namespace {
+
+constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES_MAX = 4;
+constexpr int TC_PRODUCERS = 256;  // warps 0-7
+constexpr int TC_THREADS = 384;    // + warps 8-11
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, K-major SWIZZLE_128B: rows of 128 B,
+// 8-row atoms of 1024 B (SBO), LBO unused (1), version 1 (sm_100).
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: next 8-row group
+  d |= (uint64_t)1 << 46;            // version = 1
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Split 8 fp32 values into 16-B bf16 hi and lo chunks.
+__device__ __forceinline__ void split8(const float* f, uint4& hi, uint4& lo) {
+  float r[8];
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = pack_bf16(f[2 * i], f[2 * i + 1]);
+    __nv_bfloat162 hb = *reinterpret_cast<__nv_bfloat162*>(&h[i]);
+    r[2 * i] = f[2 * i] - __low2float(hb);
+    r[2 * i + 1] = f[2 * i + 1] - __high2float(hb);
+    l[i] = pack_bf16(r[2 * i], r[2 * i + 1]);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// One operand tile: R rows (MN) x 64 k of X(r, k) = X[r*rs + k*ks] with rows
+// [r0, r0 + R) valid below `rows`, k valid below `kend`, into K-major SW128
+// hi/lo tiles (row r at r*128 B, 16-B chunk q at (q ^ (r & 7)) * 16).
+template <bool KCONTIG>
+__device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
+                                                int64_t r0, int64_t k0, int64_t kend, int R, uint8_t* hi,
+                                                uint8_t* lo, int tid) {
+  const int units = R * 8;  // (row, 8-k chunk)
+  for (int u = tid; u < units; u += TC_PRODUCERS) {
+    int r, q;
+    if (KCONTIG) {  // 8 lanes cover one row's 64 k: 256 B contiguous
+      r = u >> 3;
+      q = u & 7;
+    } else {  // lanes run along rows (MN-contiguous in global)
+      r = (u % R);
+      q = u / R;
+    }
+    const int64_t gr = r0 + r, gk = k0 + 8 * q;
+    float f[8];
+    if (gr < rows && gk + 8 <= kend) {
+      const float* p = X + gr * rs + gk * ks;
+      if (KCONTIG && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) f[t] = __ldg(p + t * ks);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) f[t] = (gr < rows && gk + t < kend) ? __ldg(X + gr * rs + (gk + t) * ks) : 0.f;
+    }
+    uint4 h, l;
+    split8(f, h, l);
+    const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(hi + off) = h;
+    *reinterpret_cast<uint4*>(lo + off) = l;
+  }
+}
+
+template <bool A_KC, bool B_KC, int BN, int STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_bf16x3_kernel(int64_t M, int64_t N, int64_t K, int64_t kchunk, const float* __restrict__ A, int64_t a_rs,
+                       int64_t a_cs, const float* __restrict__ B, int64_t b_rs, int64_t b_cs, float alpha,
+                       float beta, float* C, int64_t c_rs, int64_t c_cs, float* ws) {
+  constexpr int A_TILE = TC_BM * 128;  // bytes per bf16 tile (128 rows x 64 k)
+  constexpr int B_TILE = BN * 128;
+  constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;
+  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);  // full[S], empty[S], accum
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * TC_BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
+  const int nkb = (int)((kend - kbeg + TC_BK - 1) / TC_BK);
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&bars[s]), TC_PRODUCERS);
+      mbar_init(smem_u32(&bars[STAGES + s]), 1);
+    }
+    mbar_init(smem_u32(&bars[2 * STAGES]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 8) {  // TMEM accumulator: 128 lanes x TMEM_COLS fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 8) {
+    // ---------------- producers ----------------
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
+      uint8_t* base = smem + st * STAGE;
+      const int64_t k0 = kbeg + (int64_t)kb * TC_BK;
+      load_split_tile<A_KC>(A, a_rs, a_cs, M, m0, k0, kend, TC_BM, base, base + A_TILE, tid);
+      load_split_tile<B_KC>(B, b_cs, b_rs, N, n0, k0, kend, BN, base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, tid);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(smem_u32(&bars[st]));
+    }
+  } else {
+    if (warp == 8) {
+      // ---------------- MMA issuer ----------------
+      if (lane == 0) {
+        constexpr uint32_t idesc = idesc_bf16_f32(BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int st = kb % STAGES;
+          mbar_wait(smem_u32(&bars[st]), (uint32_t)((kb / STAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t base = smem_u32(smem + st * STAGE);
+          const uint32_t ahi = base, alo = base + A_TILE, bhi = base + 2 * A_TILE, blo = bhi + B_TILE;
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            const uint32_t koff = kk * 32;  // 16 bf16 per UMMA_K
+            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+            mma_bf16(tmem, kmajor_sw128_desc(ahi + koff), kmajor_sw128_desc(bhi + koff), idesc, acc0);
+            mma_bf16(tmem, kmajor_sw128_desc(ahi + koff), kmajor_sw128_desc(blo + koff), idesc, 1u);
+            mma_bf16(tmem, kmajor_sw128_desc(alo + koff), kmajor_sw128_desc(bhi + koff), idesc, 1u);
+          }
+          mma_commit(smem_u32(&bars[STAGES + st]));  // frees the stage when these MMAs finish
+        }
+        mma_commit(smem_u32(&bars[2 * STAGES]));  // accumulator complete
+      }
+      __syncwarp();
+    }
+    // ---------------- epilogue (warps 8-11) ----------------
+    mbar_wait(smem_u32(&bars[2 * STAGES]), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+    const int64_t row = m0 + quarter * 32 + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr + (uint32_t)c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (nkb == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K range: the sum is zero
+      }
+      if (row < M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t col = n0 + c0 + j;
+          if (col < N) {
+            const float acc = __uint_as_float(v[j]);
+            if (ws) {
+              ws[(int64_t)blockIdx.z * M * N + row * N + col] = acc;
+            } else {
+              float* cp = C + row * c_rs + col * c_cs;
+              *cp = beta == 0.f ? alpha * acc : alpha * acc + beta * *cp;
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 8) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+template <bool A_KC, bool B_KC, int BN, int STAGES>
+void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
+               int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float alpha, float beta,
+               float* C, int64_t c_rs, int64_t c_cs, float* ws) {
+  constexpr size_t STAGE = 2 * TC_BM * 128 + 2 * BN * 128;
+  const size_t smem = STAGES * STAGE + 1024 + 8 * (2 * STAGES + 2);
+  auto kern = gemm_bf16x3_kernel<A_KC, B_KC, BN, STAGES>;
+  RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)((n + BN - 1) / BN), (unsigned)splits);
+  kern<<<grid, TC_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs,
+                                                 c_cs, ws);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+template <bool A_KC, bool B_KC>
+void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
+                 int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float alpha, float beta,
+                 float* C, int64_t c_rs, int64_t c_cs, float* ws) {
+#define RNLA_TC(BNV, ST) \
+  launch_tc<A_KC, B_KC, BNV, ST>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws)
+  if (bn <= 32) RNLA_TC(32, 4);
+  else if (bn <= 64) RNLA_TC(64, 4);
+  else if (bn <= 96) RNLA_TC(96, 4);
+  else if (bn <= 128) RNLA_TC(128, 3);
+  else if (bn <= 160) RNLA_TC(160, 3);
+  else if (bn <= 192) RNLA_TC(192, 2);
+  else RNLA_TC(256, 2);
+#undef RNLA_TC
+}
+
+__global__ void splitk_reduce_f32(int64_t m, int64_t n, int splits, const float* __restrict__ ws, float alpha,
+                                  float beta, float* C, int64_t c_rs, int64_t c_cs) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    float s = ws[e];
+    for (int z = 1; z < splits; ++z) s += ws[(int64_t)z * total + e];
+    const int64_t i = e / n, j = e % n;
+    float* cp = C + i * c_rs + j * c_cs;
+    *cp = beta == 0.f ? alpha * s : alpha * s + beta * *cp;
+  }
+}
+
+}  // namespace
+
+bool tc_gemm_enabled() {
+  static const bool on = std::getenv("RNLA_DISABLE_TCGEN05") == nullptr;
+  return on;
+}
+
+// C[m x n] = alpha * A[m x k] * B[k x n] + beta * C on tcgen05 (BF16x3).
+void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
+                 int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
+                 int64_t c_cs) {
+  if (m == 0 || n == 0) return;
+  const int bn_full = (int)std::min<int64_t>(256, ((n + 15) / 16) * 16);
+  const int64_t ntiles = (n + bn_full - 1) / bn_full;
+  const int64_t tiles = ((m + TC_BM - 1) / TC_BM) * ntiles;
+  // split K until every SM has a tile (K ranges stay multiples of 64)
+  int64_t splits = 1;
+  if (tiles < ctx->num_sms && k >= 2 * TC_BK)
+    splits = std::min<int64_t>((ctx->num_sms + tiles - 1) / tiles, k / TC_BK);
+  int64_t kchunk = ((k + splits - 1) / splits + TC_BK - 1) / TC_BK * TC_BK;
+  if (k == 0) kchunk = TC_BK;
+  splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
+  DevBuf wsb;
+  float* ws = nullptr;
+  if (splits > 1) {
+    wsb = DevBuf(sizeof(float) * (size_t)(splits * m * n), ctx->stream);
+    ws = wsb.as<float>();
+  }
+  const bool a_kc = (a_cs == 1), b_kc = (b_rs == 1);
+  if (a_kc && b_kc) dispatch_bn<true, true>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
+  else if (a_kc) dispatch_bn<true, false>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
+  else if (b_kc) dispatch_bn<false, true>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
+  else dispatch_bn<false, false>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
+  if (splits > 1) {
+    splitk_reduce_f32<<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, n, (int)splits, ws, alpha, beta, C, c_rs,
+                                                                           c_cs);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+}
+
+}  // namespace rnla

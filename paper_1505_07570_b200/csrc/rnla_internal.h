@@ -138,6 +138,13 @@ struct StreamScope {
   ~StreamScope();
 };
 
+// fp32 GEMM on tcgen05 with the BF16x3 split (gemm_tc.cu); RNLA_DISABLE_TCGEN05
+// selects the SIMT fp32 kernel instead (A/B comparison only).
+bool tc_gemm_enabled();
+void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
+                 int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
+                 int64_t c_cs);
+
 // fp32 operands, exact widening to fp64, DMMA fp64 accumulation (Gram-type products).
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                      int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,

@@ -94,6 +94,178 @@ __global__ void __launch_bounds__(256) srht_hi_kernel(const T* __restrict__ scra
   }
 }
 
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
+// Register-blocked pass over R = 2^LOGR logical rows x W columns, 256 threads.
+//  phase A: thread (c = tid % W, rb = tid / W) loads logical rows rb*E..rb*E+E-1
+//           of column c straight from global (sign flip fused for the low pass),
+//           runs the log2(E) lowest stages in registers, stores to smem;
+//  phase B: thread owns groups (lo, c) = logical rows lo + E*m, m < R/E, and
+//           runs the remaining stages in registers.
+// Low pass (HI = false): logical row i of CTA blk is physical row blk*R + i of
+// the input; the result goes to the scratch strip. High pass (HI = true):
+// logical row i is physical row i*2^qlo + il (il = blockIdx.x) of the scratch;
+// only sampled outputs with low bits il are written (x 1/sqrt(s)). Stages run
+// h = 1, 2, 4, ... with x+y / x-y exactly like fwht_inplace.
+template <class T>
+constexpr int fwht_rows_per_thread() { return sizeof(T) == 8 ? 32 : 64; }
+template <class T, int LOGR, int W>
+constexpr int fwht_threads() { return (1 << LOGR) * W / fwht_rows_per_thread<T>(); }
+
+template <class T, int LOGR, int W, bool HI>
+__global__ void __launch_bounds__(fwht_threads<T, LOGR, W>()) fwht_reg_kernel(const T* __restrict__ src, int64_t ld, int64_t n, int64_t L,
+                                                       const int8_t* __restrict__ signs, int qlo, int64_t c0,
+                                                       T* __restrict__ scratch, int64_t big_n,
+                                                       const int32_t* __restrict__ grp_off,
+                                                       const int32_t* __restrict__ grp_t,
+                                                       const int32_t* __restrict__ grp_hi, double scale,
+                                                       T* __restrict__ out, int64_t out_rs, int64_t out_cs) {
+  constexpr int R = 1 << LOGR;
+  constexpr int NT = fwht_threads<T, LOGR, W>();
+  constexpr int E = R * W / NT;  // rows per thread in phase A
+  constexpr int G = R / E;        // rows per group in phase B
+  constexpr int NG = E * W;               // groups in phase B
+  constexpr int GPT = (NG + NT - 1) / NT;
+  // 16-bank shift per E-row block when a row chunk is narrower than the 32 banks
+  constexpr int PADB = W * (int)sizeof(T) >= 128 ? 0 : 64 / (int)sizeof(T);
+  static_assert(E >= 1 && G >= 1 && GPT >= 1, "bad tile");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  auto sidx = [](int i, int c) { return i * W + c + (i / E) * PADB; };
+  const int tile = blockIdx.y;
+  int g0 = 0, g1 = 0;
+  if (HI) {
+    g0 = grp_off[blockIdx.x];
+    g1 = grp_off[blockIdx.x + 1];
+    if (g0 == g1) return;  // no sampled output has these low bits (uniform per CTA)
+  }
+  const int64_t col_base = c0 + (int64_t)tile * W;
+  const T* tsrc = HI ? src + (int64_t)tile * big_n * W : src;
+  {
+    const int c = threadIdx.x % W, rb = threadIdx.x / W;
+    T v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = rb * E + e;
+      if (HI) {
+        const int64_t j = ((int64_t)i << qlo) + blockIdx.x;
+        v[e] = tsrc[j * W + c];
+      } else {
+        const int64_t j = (int64_t)blockIdx.x * R + i, col = col_base + c;
+        v[e] = (j < n && col < L) ? __ldcs(src + j * ld + col) * (T)signs[j] : T(0);
+      }
+    }
+#pragma unroll
+    for (int h = 1; h < E; h <<= 1)
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (!(e & h)) {
+          const T x = v[e], y = v[e + h];
+          v[e] = x + y;
+          v[e + h] = x - y;
+        }
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[sidx(rb * E + e, c)] = v[e];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < GPT; ++k) {
+    const int g = threadIdx.x + NT * k;
+    if (g >= NG) break;
+    const int c = g % W, lo = g / W;
+    T u[G];
+#pragma unroll
+    for (int m = 0; m < G; ++m) u[m] = sm[sidx(lo + E * m, c)];
+#pragma unroll
+    for (int h = 1; h < G; h <<= 1)
+#pragma unroll
+      for (int m = 0; m < G; ++m)
+        if (!(m & h)) {
+          const T x = u[m], y = u[m + h];
+          u[m] = x + y;
+          u[m + h] = x - y;
+        }
+    if (HI) {
+#pragma unroll
+      for (int m = 0; m < G; ++m) sm[sidx(lo + E * m, c)] = u[m];
+    } else {
+      T* dst = scratch + ((int64_t)tile * big_n + (int64_t)blockIdx.x * R) * W;
+#pragma unroll
+      for (int m = 0; m < G; ++m) dst[(int64_t)(lo + E * m) * W + c] = u[m];
+    }
+  }
+  if (HI) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < (g1 - g0) * W; e += NT) {
+      const int g = g0 + e / W, c = e % W;
+      const int64_t col = col_base + c;
+      if (col < L) out[(int64_t)grp_t[g] * out_rs + col * out_cs] = (T)((double)sm[sidx(grp_hi[g], c)] * scale);
+    }
+  }
+}
+
+template <class T, int LOGR, int W, bool HI>
+size_t fwht_reg_smem() {
+  constexpr int R = 1 << LOGR, E = fwht_rows_per_thread<T>();
+  constexpr int PADB = W * (int)sizeof(T) >= 128 ? 0 : 64 / (int)sizeof(T);
+  return sizeof(T) * ((size_t)R * W + (size_t)(R / E) * PADB);
+}
+
+template <class T, int LOGR, int W, bool HI>
+void launch_fwht_reg(rnla_ctx* ctx, dim3 grid, const T* src, int64_t ld, int64_t n, int64_t L,
+                     const int8_t* signs, int qlo, int64_t c0, T* scratch, int64_t big_n, const SrhtPlan& plan,
+                     double scale, T* out, int64_t out_rs, int64_t out_cs) {
+  const size_t smem = fwht_reg_smem<T, LOGR, W, HI>();
+  auto kern = fwht_reg_kernel<T, LOGR, W, HI>;
+  RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, fwht_threads<T, LOGR, W>(), smem, ctx->stream>>>(src, ld, n, L, signs, qlo, c0, scratch, big_n, plan.grp_off.as<int32_t>(),
+                                         plan.grp_t.as<int32_t>(), plan.grp_hi.as<int32_t>(), scale, out, out_rs,
+                                         out_cs);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+// Fast register path for log2 R in {9, 10, 11} (padded dimension 2^18 .. 2^22).
+template <class T, int W>
+void srht_fast_w(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int64_t L, T* out, int64_t out_rs,
+                 int64_t out_cs) {
+  const int64_t big_n = plan.big_n;
+  const int64_t tile_bytes = big_n * W * (int64_t)sizeof(T);
+  int64_t tiles_per_strip = std::max<int64_t>(1, ((int64_t)64 << 20) / tile_bytes);
+  const int64_t total_tiles = (L + W - 1) / W;
+  tiles_per_strip = std::min(tiles_per_strip, total_tiles);
+  DevBuf scratch(sizeof(T) * (size_t)(big_n * W * tiles_per_strip), ctx->stream);
+  const double scale = 1.0 / std::sqrt((double)plan.s);
+  for (int64_t t0 = 0; t0 < total_tiles; t0 += tiles_per_strip) {
+    const int64_t nt = std::min(tiles_per_strip, total_tiles - t0);
+    const int64_t c0 = t0 * W;
+    const dim3 g1((unsigned)(big_n >> plan.qlo), (unsigned)nt), g2((unsigned)((int64_t)1 << plan.qlo), (unsigned)nt);
+#define RNLA_PASS(LOGR, HI, GRID)                                                                                 \
+  launch_fwht_reg<T, LOGR, W, HI>(ctx, GRID, HI ? scratch.as<T>() : in, ld, plan.n, L, plan.signs.as<int8_t>(), \
+                                  plan.qlo, c0, scratch.as<T>(), big_n, plan, scale, out, out_rs, out_cs)
+    if (plan.qlo == 9) RNLA_PASS(9, false, g1);
+    else if (plan.qlo == 10) RNLA_PASS(10, false, g1);
+    else RNLA_PASS(11, false, g1);
+    if (plan.qhi == 9) RNLA_PASS(9, true, g2);
+    else if (plan.qhi == 10) RNLA_PASS(10, true, g2);
+    else RNLA_PASS(11, true, g2);
+#undef RNLA_PASS
+  }
+}
+
+// Fast register path for log2 R in {9, 10, 11} (padded dimension 2^18 .. 2^22).
+// One tile width for both passes (the scratch layout is [tile][N][W]).
+template <class T>
+bool srht_fast(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int64_t L, T* out, int64_t out_rs,
+               int64_t out_cs) {
+  auto ok = [](int q) { return q >= 9 && q <= 11; };
+  if (!ok(plan.qlo) || !ok(plan.qhi)) return false;
+  constexpr int W = 128 / sizeof(T);  // 128-B row chunks: no DRAM over-fetch on the strided rows
+  if (plan.qlo == 11 || plan.qhi == 11) srht_fast_w<T, W / 2>(ctx, plan, in, ld, L, out, out_rs, out_cs);
+  else srht_fast_w<T, W>(ctx, plan, in, ld, L, out, out_rs, out_cs);
+  return true;
+}
+
 }  // namespace
 
 SrhtPlan::SrhtPlan(rnla_ctx* ctx, int64_t n_, int64_t s_, uint64_t seed_) : n(n_), s(s_), seed(seed_) {
@@ -134,6 +306,7 @@ template <class T>
 void srht_segments(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int64_t L, T* out, int64_t out_rs,
                    int64_t out_cs) {
   if (L == 0) return;
+  if (!std::getenv("RNLA_SRHT_GENERIC") && srht_fast<T>(ctx, plan, in, ld, L, out, out_rs, out_cs)) return;
   constexpr int W = sizeof(T) == 8 ? 8 : 16;
   const int64_t big_n = plan.big_n;
   // Column tiles per strip: keep the strip's scratch (big_n * W * tiles) within ~48 MB of L2.

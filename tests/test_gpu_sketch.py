@@ -128,6 +128,22 @@ def test_srht_sketch_fp64_bit_exact(ctx, m, n, s):
     assert np.array_equal(got, orc.srht_sketch(a, s, 11 + s))
 
 
+@pytest.mark.parametrize("n,L,s", [(1 << 18, 20, 1000), (300000, 9, 4096), ((1 << 21) - 5, 3, 333)])
+def test_srht_register_path_fp64_bit_exact(ctx, n, L, s):
+    # padded sizes 2^18 .. 2^22 take the register-blocked two-pass kernels
+    rng = np.random.default_rng(n)
+    m = rng.standard_normal((n, L))
+    got = rn.sketch_rows(dev(m), rn.SketchSpec.srht(s, 5 + s), ctx=ctx).cpu().numpy()
+    assert np.array_equal(got, orc.srht_rows(m, s, 5 + s))
+
+
+def test_srht_register_path_fp32(ctx):
+    rng = np.random.default_rng(21)
+    m = rng.standard_t(3, size=((1 << 20), 40)).astype(np.float32)
+    got = rn.sketch_rows(dev(m), rn.SketchSpec.srht(4096, 17), ctx=ctx).cpu().numpy()
+    assert relf(got, orc.srht_rows(m.astype(np.float64), 4096, 17)) <= 1e-4
+
+
 def test_srht_rows_fp32(ctx):
     rng = np.random.default_rng(12)
     m = rng.standard_t(3, size=(1 << 14, 96)).astype(np.float32)
