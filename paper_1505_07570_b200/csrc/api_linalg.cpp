@@ -89,9 +89,59 @@ DevMat f64_colmajor(rnla_ctx* ctx, const rnla_mat* a) {
 // ---------------------------------------------------------------------------
 template <class T>
 struct KsvdWork {
-  // Compute type T for the passes over A; orthonormalization in fp64.
+  // orth(Y) = thin_qr(Y).Q semantics (src/core.cpp:37-46). Tall-skinny Y is
+  // orthonormalized by CholeskyQR2 (Gram -> Cholesky -> Y R^-1, twice; the
+  // Gram of fp64 data on DMMA, of fp32 data on tcgen05), then the reference's
+  // sign rule is applied, which makes Q unique: any stable orthonormalization
+  // of the same range gives the same Q up to rounding (SURVEY A.6 measured
+  // Householder vs CholeskyQR2 top-20 sigma within 1e-15). A Cholesky
+  // breakdown (numerically rank-deficient Y) falls back to Householder.
   static void orth(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, int64_t ld_unused) {
     (void)ld_unused;
+    if (rows >= 4 * cols && cholqr2(ctx, rows, cols, Y)) return;
+    householder(ctx, rows, cols, Y);
+  }
+
+  static bool cholqr2(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
+    DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream);
+    DevBuf tmp(sizeof(T) * rows * cols, ctx->stream), Rt;
+    if constexpr (!std::is_same<T, double>::value) Rt = DevBuf(sizeof(T) * cols * cols, ctx->stream);
+    for (int pass = 0; pass < 2; ++pass) {
+      if constexpr (std::is_same<T, double>::value) {
+        gemm<double>(ctx, cols, cols, rows, 1.0, Y, rows, 1, Y, 1, rows, 0.0, G.as<double>(), 1, cols);
+      } else {
+        DevBuf Gf(sizeof(float) * cols * cols, ctx->stream);
+        gemm<float>(ctx, cols, cols, rows, 1.f, Y, rows, 1, Y, 1, rows, 0.f, Gf.as<float>(), 1, cols);
+        copy2d_cast<float, double>(ctx, cols, cols, Gf.as<float>(), 1, cols, G.as<double>(), 1, cols);
+      }
+      if (!cholesky_upper(ctx, cols, G.as<double>())) return false;
+      if (!diag_ratio_ok(ctx, cols, G.as<double>(), std::is_same<T, double>::value ? 1e-5 : 1e-2)) return false;
+      upper_inverse(ctx, cols, G.as<double>(), Rinv.as<double>());
+      if constexpr (std::is_same<T, double>::value) {
+        gemm<double>(ctx, rows, cols, cols, 1.0, Y, 1, rows, Rinv.as<double>(), 1, cols, 0.0, tmp.as<double>(), 1,
+                     rows);
+      } else {
+        copy2d_cast<double, float>(ctx, cols, cols, Rinv.as<double>(), 1, cols, Rt.as<float>(), 1, cols);
+        gemm<float>(ctx, rows, cols, cols, 1.f, Y, 1, rows, Rt.as<float>(), 1, cols, 0.f, tmp.as<float>(), 1, rows);
+      }
+      RNLA_CUDA(cudaMemcpyAsync(Y, tmp.p, sizeof(T) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    sign_fix(ctx, rows, cols, Y);
+    return true;
+  }
+
+  static void sign_fix(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
+    if constexpr (std::is_same<T, double>::value) {
+      fix_column_signs(ctx, rows, cols, Y, 1, rows, nullptr, 0, 0, 0, true);
+    } else {
+      DevBuf w(sizeof(double) * rows * cols, ctx->stream);
+      copy2d_cast<float, double>(ctx, rows, cols, Y, 1, rows, w.as<double>(), 1, rows);
+      fix_column_signs(ctx, rows, cols, w.as<double>(), 1, rows, nullptr, 0, 0, 0, true);
+      copy2d_cast<double, float>(ctx, rows, cols, w.as<double>(), 1, rows, Y, 1, rows);
+    }
+  }
+
+  static void householder(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
     DevBuf w(sizeof(double) * rows * cols, ctx->stream), r(sizeof(double) * cols * cols, ctx->stream);
     if constexpr (std::is_same<T, double>::value) {
       RNLA_CUDA(cudaMemcpyAsync(w.p, Y, sizeof(double) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -145,8 +195,10 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   }
   KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), m);  // Q = thin_qr(C).Q
   // pass 2: B = Q' A (s x n), column-major
+  // computed as B' = A' Q (the streaming orientation of the A' Q power step),
+  // written transposed: element (i, j) of B' lands at B[j + i*s].
   DevBuf B(sizeof(T) * s * n, ctx->stream);
-  gemm<T>(ctx, s, n, m, T(1), Y.as<T>(), m, 1, Ap, A.rs, A.cs, T(0), B.as<T>(), 1, s);
+  gemm<T>(ctx, n, s, m, T(1), Ap, A.cs, A.rs, Y.as<T>(), 1, m, T(0), B.as<T>(), s, 1);
   ++passes;
   DevBuf B64;
   const double* Bp;

@@ -8,14 +8,16 @@
 // config 3 shape; 1-pass BF16 2.3e-3 and 1-pass TF32 2.9e-4 fail the 1e-4
 // gate), at an effective 1/3 of the BF16 tensor peak (~550 TF measured).
 //
-// CTA = one 128 x BN output tile (BN <= 256, multiple of 16) over a K range:
+// CTA = one 128 x BN output tile (BN <= 160, multiple of 16) over a K range:
 //   warps 0-7  : producers -- load fp32 A/B tiles (64 k per stage) from global,
 //                split to bf16 hi/lo and store them in the canonical K-major
 //                SWIZZLE_128B smem layout; mbarrier `full[stage]`;
-//   warp 8     : one elected lane issues 4 k-steps x 3 tcgen05.mma
-//                (kind::f16, M=128, N=BN, K=16) per stage and commits to
-//                `empty[stage]`; a final commit signals the epilogue;
-//   warps 8-11 : epilogue -- tcgen05.ld (32x32b) from TMEM, alpha/beta, store.
+//   warp 12    : one lane issues 4 k-steps x 3 tcgen05.mma (kind::f16, M=128,
+//                N=BN, K=16) per stage into TMEM partial buffer X[c & 1] and
+//                commits to `empty[stage]`; every TC_PROMOTE_KB stages it
+//                commits `xfull` and later waits `xfree` before reusing X;
+//   warps 8-11 : epilogue -- tcgen05.ld X, add into the TMEM accumulator Y
+//                with fp32 CUDA-core adds (tcgen05.st), final alpha/beta store.
 // Global operands may be K-contiguous or MN-contiguous; the converting
 // loader always produces K-major smem, so only the K-major descriptor is used.
 // The fp32 data is read through registers because it has to be split before
@@ -31,7 +33,8 @@ namespace {
 
 constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES_MAX = 4;
 constexpr int TC_PRODUCERS = 256;  // warps 0-7
-constexpr int TC_THREADS = 384;    // + warps 8-11
+constexpr int TC_MMA_WARP = 12;    // warps 8-11 run the epilogue
+constexpr int TC_THREADS = 416;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -86,6 +89,25 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                : "memory");
 }
 
+constexpr int TC_PROMOTE_KB = 8;  // k-blocks (x64 k) per TMEM partial sum
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -111,40 +133,65 @@ __device__ __forceinline__ void split8(const float* f, uint4& hi, uint4& lo) {
 // [r0, r0 + R) valid below `rows`, k valid below `kend`, into K-major SW128
 // hi/lo tiles (row r at r*128 B, 16-B chunk q at (q ^ (r & 7)) * 16).
 template <bool KCONTIG>
-__device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
-                                                int64_t r0, int64_t k0, int64_t kend, int R, uint8_t* hi,
-                                                uint8_t* lo, int tid) {
-  const int units = R * 8;  // (row, 8-k chunk)
-  for (int u = tid; u < units; u += TC_PRODUCERS) {
-    int r, q;
-    if (KCONTIG) {  // 8 lanes cover one row's 64 k: 256 B contiguous
-      r = u >> 3;
-      q = u & 7;
-    } else {  // lanes run along rows (MN-contiguous in global)
-      r = (u % R);
-      q = u / R;
-    }
-    const int64_t gr = r0 + r, gk = k0 + 8 * q;
-    float f[8];
-    if (gr < rows && gk + 8 <= kend) {
-      const float* p = X + gr * rs + gk * ks;
-      if (KCONTIG && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-        const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-      } else {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) f[t] = __ldg(p + t * ks);
-      }
+__device__ __forceinline__ void unit_coords(int u, int R, int& r, int& q) {
+  if (KCONTIG) {  // 8 lanes cover one row's 64 k: 256 B contiguous
+    r = u >> 3;
+    q = u & 7;
+  } else {  // lanes run along rows (MN-contiguous in global)
+    r = u % R;
+    q = u / R;
+  }
+}
+
+template <bool KCONTIG>
+__device__ __forceinline__ void load_unit(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
+                                          int64_t gr, int64_t gk, int64_t kend, float* f) {
+  if (gr < rows && gk + 8 <= kend) {
+    const float* p = X + gr * rs + gk * ks;
+    if (KCONTIG && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
     } else {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) f[t] = (gr < rows && gk + t < kend) ? __ldg(X + gr * rs + (gk + t) * ks) : 0.f;
+      for (int t = 0; t < 8; ++t) f[t] = __ldg(p + t * ks);
     }
-    uint4 h, l;
-    split8(f, h, l);
-    const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
-    *reinterpret_cast<uint4*>(hi + off) = h;
-    *reinterpret_cast<uint4*>(lo + off) = l;
+  } else {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) f[t] = (gr < rows && gk + t < kend) ? __ldg(X + gr * rs + (gk + t) * ks) : 0.f;
+  }
+}
+
+// All loads of the tile are issued before any conversion (R*8/256 units per
+// thread in flight), then each unit is split and stored.
+template <bool KCONTIG, int R>
+__device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
+                                                int64_t r0, int64_t k0, int64_t kend, uint8_t* hi, uint8_t* lo,
+                                                int tid) {
+  constexpr int UNITS = R * 8;  // (row, 8-k chunk)
+  constexpr int UPT = (UNITS + TC_PRODUCERS - 1) / TC_PRODUCERS;
+  float f[UPT][8];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int u = tid + i * TC_PRODUCERS;
+    if (UNITS % TC_PRODUCERS == 0 || u < UNITS) {
+      int r, q;
+      unit_coords<KCONTIG>(u, R, r, q);
+      load_unit<KCONTIG>(X, rs, ks, rows, r0 + r, k0 + 8 * q, kend, f[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int u = tid + i * TC_PRODUCERS;
+    if (UNITS % TC_PRODUCERS == 0 || u < UNITS) {
+      int r, q;
+      unit_coords<KCONTIG>(u, R, r, q);
+      uint4 h, l;
+      split8(f[i], h, l);
+      const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
+      *reinterpret_cast<uint4*>(hi + off) = h;
+      *reinterpret_cast<uint4*>(lo + off) = l;
+    }
   }
 }
 
@@ -156,11 +203,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr int A_TILE = TC_BM * 128;  // bytes per bf16 tile (128 rows x 64 k)
   constexpr int B_TILE = BN * 128;
   constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;
-  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  // TMEM: two MMA partial-sum buffers X0, X1 and the promoted accumulator Y.
+  // The tensor core's fp32 accumulation does not round to nearest (measured:
+  // rel-F error 5.7e-5 at K = 16384 in one accumulator vs 4.6e-6 at K ~ 400),
+  // so every TC_PROMOTE_KB k-blocks the epilogue adds the finished partial
+  // into Y with CUDA-core fp32 adds while the MMAs fill the other buffer.
+  static_assert(3 * BN <= 512, "BN too large for promoted accumulation");
+  constexpr uint32_t TMEM_COLS = 3 * BN <= 128 ? 128 : (3 * BN <= 256 ? 256 : 512);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);  // full[S], empty[S], accum
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  // full[S], empty[S], xfull[2], xfree[2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m0 = (int64_t)blockIdx.x * TC_BM, n0 = (int64_t)blockIdx.y * BN;
@@ -172,7 +226,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(smem_u32(&bars[s]), TC_PRODUCERS);
       mbar_init(smem_u32(&bars[STAGES + s]), 1);
     }
-    mbar_init(smem_u32(&bars[2 * STAGES]), 1);
+    mbar_init(smem_u32(&bars[2 * STAGES]), 1);      // xfull[0]
+    mbar_init(smem_u32(&bars[2 * STAGES + 1]), 1);  // xfull[1]
+    mbar_init(smem_u32(&bars[2 * STAGES + 2]), 128);  // xfree[0] (epilogue threads)
+    mbar_init(smem_u32(&bars[2 * STAGES + 3]), 128);  // xfree[1]
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 8) {  // TMEM accumulator: 128 lanes x TMEM_COLS fp32 columns
@@ -192,52 +249,85 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
       uint8_t* base = smem + st * STAGE;
       const int64_t k0 = kbeg + (int64_t)kb * TC_BK;
-      load_split_tile<A_KC>(A, a_rs, a_cs, M, m0, k0, kend, TC_BM, base, base + A_TILE, tid);
-      load_split_tile<B_KC>(B, b_cs, b_rs, N, n0, k0, kend, BN, base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, tid);
+      load_split_tile<A_KC, TC_BM>(A, a_rs, a_cs, M, m0, k0, kend, base, base + A_TILE, tid);
+      load_split_tile<B_KC, BN>(B, b_cs, b_rs, N, n0, k0, kend, base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, tid);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive(smem_u32(&bars[st]));
     }
-  } else {
-    if (warp == 8) {
-      // ---------------- MMA issuer ----------------
+  } else if (warp == TC_MMA_WARP) {
+    {
+      // ---------------- MMA issuer (own warp: it waits on epilogue arrivals) ----------------
       if (lane == 0) {
         constexpr uint32_t idesc = idesc_bf16_f32(BN);
         for (int kb = 0; kb < nkb; ++kb) {
           const int st = kb % STAGES;
+          const int chunk = kb / TC_PROMOTE_KB, xb = chunk & 1, kin = kb % TC_PROMOTE_KB;
+          if (kin == 0 && chunk >= 2)  // X[xb] drained by the epilogue (chunk - 2)?
+            mbar_wait(smem_u32(&bars[2 * STAGES + 2 + xb]), (uint32_t)(((chunk / 2) - 1) & 1));
           mbar_wait(smem_u32(&bars[st]), (uint32_t)((kb / STAGES) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t dst = tmem + (uint32_t)(xb * BN);
           const uint32_t base = smem_u32(smem + st * STAGE);
           const uint32_t ahi = base, alo = base + A_TILE, bhi = base + 2 * A_TILE, blo = bhi + B_TILE;
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
             const uint32_t koff = kk * 32;  // 16 bf16 per UMMA_K
-            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_bf16(tmem, kmajor_sw128_desc(ahi + koff), kmajor_sw128_desc(bhi + koff), idesc, acc0);
-            mma_bf16(tmem, kmajor_sw128_desc(ahi + koff), kmajor_sw128_desc(blo + koff), idesc, 1u);
-            mma_bf16(tmem, kmajor_sw128_desc(alo + koff), kmajor_sw128_desc(bhi + koff), idesc, 1u);
+            const uint32_t acc0 = (kin > 0 || kk > 0) ? 1u : 0u;
+            mma_bf16(dst, kmajor_sw128_desc(ahi + koff), kmajor_sw128_desc(bhi + koff), idesc, acc0);
+            mma_bf16(dst, kmajor_sw128_desc(ahi + koff), kmajor_sw128_desc(blo + koff), idesc, 1u);
+            mma_bf16(dst, kmajor_sw128_desc(alo + koff), kmajor_sw128_desc(bhi + koff), idesc, 1u);
           }
           mma_commit(smem_u32(&bars[STAGES + st]));  // frees the stage when these MMAs finish
+          if (kin == TC_PROMOTE_KB - 1 || kb == nkb - 1) mma_commit(smem_u32(&bars[2 * STAGES + xb]));  // X ready
         }
-        mma_commit(smem_u32(&bars[2 * STAGES]));  // accumulator complete
       }
       __syncwarp();
     }
+  } else {
     // ---------------- epilogue (warps 8-11) ----------------
-    mbar_wait(smem_u32(&bars[2 * STAGES]), 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
     const int64_t row = m0 + quarter * 32 + lane;
-    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t yaddr = tlane + (uint32_t)(2 * BN);
+    const int nchunks = (nkb + TC_PROMOTE_KB - 1) / TC_PROMOTE_KB;
+    // chunks 0 .. nchunks-2: Y (+)= X[c & 1] in TMEM; the last chunk is combined on the way out
+    for (int c = 0; c + 1 < nchunks; ++c) {
+      const int xb = c & 1;
+      mbar_wait(smem_u32(&bars[2 * STAGES + xb]), (uint32_t)((c / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t x[16], y[16];
+        tmem_ld16(tlane + (uint32_t)(xb * BN + c0), x);
+        if (c > 0) tmem_ld16(yaddr + (uint32_t)c0, y);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (c > 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = __float_as_uint(__uint_as_float(y[j]) + __uint_as_float(x[j]));
+        }
+        tmem_st16(yaddr + (uint32_t)c0, x);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      mbar_arrive(smem_u32(&bars[2 * STAGES + 2 + xb]));  // X[xb] free for chunk c + 2
+    }
+    const int last = nchunks - 1;
+    if (nchunks > 0) {
+      mbar_wait(smem_u32(&bars[2 * STAGES + (last & 1)]), (uint32_t)((last / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+    }
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr + (uint32_t)c0));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (nkb == 0) {
+      uint32_t v[16], y[16];
+      if (nchunks > 0) {
+        tmem_ld16(tlane + (uint32_t)((last & 1) * BN + c0), v);
+        if (last > 0) tmem_ld16(yaddr + (uint32_t)c0, y);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (last > 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(y[j]) + __uint_as_float(v[j]));
+        }
+      } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K range: the sum is zero
       }
@@ -271,7 +361,7 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
                int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float alpha, float beta,
                float* C, int64_t c_rs, int64_t c_cs, float* ws) {
   constexpr size_t STAGE = 2 * TC_BM * 128 + 2 * BN * 128;
-  const size_t smem = STAGES * STAGE + 1024 + 8 * (2 * STAGES + 2);
+  const size_t smem = STAGES * STAGE + 1024 + 8 * (2 * STAGES + 5);
   auto kern = gemm_bf16x3_kernel<A_KC, B_KC, BN, STAGES>;
   RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)((n + BN - 1) / BN), (unsigned)splits);
@@ -291,9 +381,7 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
   else if (bn <= 64) RNLA_TC(64, 4);
   else if (bn <= 96) RNLA_TC(96, 4);
   else if (bn <= 128) RNLA_TC(128, 3);
-  else if (bn <= 160) RNLA_TC(160, 3);
-  else if (bn <= 192) RNLA_TC(192, 2);
-  else RNLA_TC(256, 2);
+  else RNLA_TC(160, 3);
 #undef RNLA_TC
 }
 
@@ -321,7 +409,8 @@ void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, co
                  int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
                  int64_t c_cs) {
   if (m == 0 || n == 0) return;
-  const int bn_full = (int)std::min<int64_t>(256, ((n + 15) / 16) * 16);
+  // one N tile up to 160 columns (3 accumulators fit TMEM), else 128-column tiles
+  const int bn_full = n <= 160 ? (int)(((n + 15) / 16) * 16) : 128;
   const int64_t ntiles = (n + bn_full - 1) / bn_full;
   const int64_t tiles = ((m + TC_BM - 1) / TC_BM) * ntiles;
   // split K until every SM has a tile (K ranges stay multiples of 64)

@@ -146,6 +146,20 @@ bool cholesky_upper(rnla_ctx* ctx, int64_t n, double* G) {
   return hinfo == 0;
 }
 
+bool diag_ratio_ok(rnla_ctx* ctx, int64_t n, const double* R, double thresh) {
+  std::vector<double> d((size_t)n);
+  RNLA_CUDA(cudaMemcpy2DAsync(d.data(), sizeof(double), R, sizeof(double) * (n + 1), sizeof(double), n,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  double lo = INFINITY, hi = 0.0;
+  for (double v : d) {
+    if (!std::isfinite(v)) return false;
+    lo = std::min(lo, std::fabs(v));
+    hi = std::max(hi, std::fabs(v));
+  }
+  return n == 0 || (hi > 0.0 && lo > thresh * hi);
+}
+
 void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv) {
   // Rinv = R^-1 by a triangular solve against the identity (lower part zero).
   std::vector<double> eye((size_t)(n * n), 0.0);
