@@ -33,6 +33,7 @@ namespace {
 
 constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES_MAX = 4;
 constexpr int TC_PRODUCERS = 256;  // warps 0-7
+constexpr int TC_GROUP = 128;      // producer group (4 warps) per k-block
 constexpr int TC_MMA_WARP = 12;    // warps 8-11 run the epilogue
 constexpr int TC_THREADS = 416;
 
@@ -164,17 +165,17 @@ __device__ __forceinline__ void load_unit(const float* __restrict__ X, int64_t r
 
 // All loads of the tile are issued before any conversion (R*8/256 units per
 // thread in flight), then each unit is split and stored.
-template <bool KCONTIG, int R>
+template <bool KCONTIG, int R, int NT>
 __device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
                                                 int64_t r0, int64_t k0, int64_t kend, uint8_t* hi, uint8_t* lo,
                                                 int tid) {
   constexpr int UNITS = R * 8;  // (row, 8-k chunk)
-  constexpr int UPT = (UNITS + TC_PRODUCERS - 1) / TC_PRODUCERS;
+  constexpr int UPT = (UNITS + NT - 1) / NT;
   float f[UPT][8];
 #pragma unroll
   for (int i = 0; i < UPT; ++i) {
-    const int u = tid + i * TC_PRODUCERS;
-    if (UNITS % TC_PRODUCERS == 0 || u < UNITS) {
+    const int u = tid + i * NT;
+    if (UNITS % NT == 0 || u < UNITS) {
       int r, q;
       unit_coords<KCONTIG>(u, R, r, q);
       load_unit<KCONTIG>(X, rs, ks, rows, r0 + r, k0 + 8 * q, kend, f[i]);
@@ -182,8 +183,8 @@ __device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int
   }
 #pragma unroll
   for (int i = 0; i < UPT; ++i) {
-    const int u = tid + i * TC_PRODUCERS;
-    if (UNITS % TC_PRODUCERS == 0 || u < UNITS) {
+    const int u = tid + i * NT;
+    if (UNITS % NT == 0 || u < UNITS) {
       int r, q;
       unit_coords<KCONTIG>(u, R, r, q);
       uint4 h, l;
@@ -195,10 +196,49 @@ __device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int
   }
 }
 
-template <bool A_KC, bool B_KC, int BN, int STAGES>
+// B operand prepared once per GEMM: every (n-block, k-block) tile split to
+// bf16 hi/lo and stored in global memory as the exact K-major SW128 smem
+// image [hi BN x 128 B][lo BN x 128 B], so the main loop moves it with one
+// cp.async.bulk per stage (no conversion, no registers). B (Omega, Q, Z) is
+// small and re-read by every M tile, so this also halves its L2 traffic vs fp32.
+__global__ void split_b_image(int64_t K, int64_t N, const float* __restrict__ B, int64_t b_rs, int64_t b_cs, int BN,
+                              int64_t nkb, int64_t nblk, uint8_t* __restrict__ img) {
+  const int64_t total = nblk * nkb * BN * 8;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(u & 7);
+    const int64_t rest0 = u >> 3;
+    const int j = (int)(rest0 % BN);
+    const int64_t rest = rest0 / BN;
+    const int64_t kb = rest % nkb, nb = rest / nkb;
+    const int64_t gj = nb * BN + j, gk = kb * TC_BK + 8 * q;
+    float f[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) f[t] = (gj < N && gk + t < K) ? B[(gk + t) * b_rs + gj * b_cs] : 0.f;
+    uint4 h, l;
+    split8(f, h, l);
+    uint8_t* tile = img + (nb * nkb + kb) * (int64_t)(2 * BN * 128);
+    const uint32_t off = (uint32_t)j * 128u + (uint32_t)((q ^ (j & 7)) << 4);
+    *reinterpret_cast<uint4*>(tile + off) = h;
+    *reinterpret_cast<uint4*>(tile + BN * 128 + off) = l;
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <bool A_KC, int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_bf16x3_kernel(int64_t M, int64_t N, int64_t K, int64_t kchunk, const float* __restrict__ A, int64_t a_rs,
-                       int64_t a_cs, const float* __restrict__ B, int64_t b_rs, int64_t b_cs, float alpha,
+                       int64_t a_cs, const uint8_t* __restrict__ bimg, int64_t nkb_total, float alpha,
                        float beta, float* C, int64_t c_rs, int64_t c_cs, float* ws) {
   constexpr int A_TILE = TC_BM * 128;  // bytes per bf16 tile (128 rows x 64 k)
   constexpr int B_TILE = BN * 128;
@@ -223,7 +263,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&bars[s]), TC_PRODUCERS);
+      mbar_init(smem_u32(&bars[s]), TC_GROUP + 1);  // a producer group + the bulk-copy expect_tx arrive
       mbar_init(smem_u32(&bars[STAGES + s]), 1);
     }
     mbar_init(smem_u32(&bars[2 * STAGES]), 1);      // xfull[0]
@@ -243,14 +283,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 8) {
-    // ---------------- producers ----------------
-    for (int kb = 0; kb < nkb; ++kb) {
+    // ---------------- producers: two groups of 4 warps take alternate k-blocks,
+    // so two k-blocks of A loads are in flight per SM ----------------
+    const int grp = warp >> 2, gtid = tid & (TC_GROUP - 1);
+    const int64_t kb0 = kbeg / TC_BK;
+    const uint8_t* bsrc = bimg + ((int64_t)blockIdx.y * nkb_total + kb0) * (int64_t)(2 * B_TILE);
+    for (int kb = grp; kb < nkb; kb += 2) {
       const int st = kb % STAGES;
       if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
       uint8_t* base = smem + st * STAGE;
+      if (gtid == 0) {
+        mbar_arrive_expect_tx(smem_u32(&bars[st]), 2 * B_TILE);
+        bulk_copy_g2s(smem_u32(base + 2 * A_TILE), bsrc + (int64_t)kb * (2 * B_TILE), 2 * B_TILE,
+                      smem_u32(&bars[st]));
+      }
       const int64_t k0 = kbeg + (int64_t)kb * TC_BK;
-      load_split_tile<A_KC, TC_BM>(A, a_rs, a_cs, M, m0, k0, kend, base, base + A_TILE, tid);
-      load_split_tile<B_KC, BN>(B, b_cs, b_rs, N, n0, k0, kend, base + 2 * A_TILE, base + 2 * A_TILE + B_TILE, tid);
+      load_split_tile<A_KC, TC_BM, TC_GROUP>(A, a_rs, a_cs, M, m0, k0, kend, base, base + A_TILE, gtid);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive(smem_u32(&bars[st]));
     }
@@ -356,27 +404,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-template <bool A_KC, bool B_KC, int BN, int STAGES>
+template <bool A_KC, int BN, int STAGES>
 void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float alpha, float beta,
                float* C, int64_t c_rs, int64_t c_cs, float* ws) {
   constexpr size_t STAGE = 2 * TC_BM * 128 + 2 * BN * 128;
+  const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
+  DevBuf img(2 * (size_t)BN * 128 * (size_t)(nkb * nblk), ctx->stream);
+  split_b_image<<<grid_for(ctx, nblk * nkb * BN * 8, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb, nblk,
+                                                                                   img.as<uint8_t>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
   const size_t smem = STAGES * STAGE + 1024 + 8 * (2 * STAGES + 5);
-  auto kern = gemm_bf16x3_kernel<A_KC, B_KC, BN, STAGES>;
+  auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES>;
   RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)((n + BN - 1) / BN), (unsigned)splits);
-  kern<<<grid, TC_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs,
-                                                 c_cs, ws);
+  dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)nblk, (unsigned)splits);
+  kern<<<grid, TC_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, A, a_rs, a_cs, img.as<uint8_t>(), nkb, alpha, beta,
+                                                 C, c_rs, c_cs, ws);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
 
-template <bool A_KC, bool B_KC>
+template <bool A_KC>
 void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                  int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float alpha, float beta,
                  float* C, int64_t c_rs, int64_t c_cs, float* ws) {
 #define RNLA_TC(BNV, ST) \
-  launch_tc<A_KC, B_KC, BNV, ST>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws)
+  launch_tc<A_KC, BNV, ST>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws)
   if (bn <= 32) RNLA_TC(32, 4);
   else if (bn <= 64) RNLA_TC(64, 4);
   else if (bn <= 96) RNLA_TC(96, 4);
@@ -426,11 +480,12 @@ void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, co
     wsb = DevBuf(sizeof(float) * (size_t)(splits * m * n), ctx->stream);
     ws = wsb.as<float>();
   }
-  const bool a_kc = (a_cs == 1), b_kc = (b_rs == 1);
-  if (a_kc && b_kc) dispatch_bn<true, true>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
-  else if (a_kc) dispatch_bn<true, false>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
-  else if (b_kc) dispatch_bn<false, true>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
-  else dispatch_bn<false, false>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws);
+  if (a_cs == 1)
+    dispatch_bn<true>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs,
+                      c_cs, ws);
+  else
+    dispatch_bn<false>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, c_rs,
+                       c_cs, ws);
   if (splits > 1) {
     splitk_reduce_f32<<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, n, (int)splits, ws, alpha, beta, C, c_rs,
                                                                            c_cs);
