@@ -69,6 +69,45 @@ SvdDev condensed_svd_dev(rnla_ctx* ctx, int64_t m, int64_t n, const double* A, i
   return f;
 }
 
+// Top-k of condensed_svd for a short-wide B (s x n, s <= n, column-major fp64),
+// as truncated_svd(B, k) uses it in prototype_ksvd (src/randsvd.cpp:100-101):
+// eig(B B') = (Ubar, sigma^2), V = B' Ubar / sigma, then the reference's sign
+// rule on Ubar (paired with V). The Gram squares the condition number, so it
+// is used only when sigma_k >= 1e-3 sigma_1 (relative error of sigma_i is
+// ~eps (sigma_1/sigma_i)^2 <= 1e-10 there); otherwise QR + SVD.
+SvdDev topk_svd_wide(rnla_ctx* ctx, int64_t s, int64_t n, const double* B, int64_t k) {
+  if (s > 512 || k < 1 || std::getenv("RNLA_SVD_NO_GRAM")) return condensed_svd_dev(ctx, s, n, B, 1, s);
+  DevBuf G(sizeof(double) * s * s, ctx->stream), lam(sizeof(double) * s, ctx->stream);
+  gemm<double>(ctx, s, s, n, 1.0, B, 1, s, B, s, 1, 0.0, G.as<double>(), 1, s);
+  eig_sym(ctx, s, G.as<double>(), lam.as<double>());
+  std::vector<double> h((size_t)s);
+  RNLA_CUDA(cudaMemcpyAsync(h.data(), lam.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double l1 = h[(size_t)s - 1], lk = h[(size_t)(s - k)];
+  if (!(l1 > 0.0) || !(lk > 1e-6 * l1)) return condensed_svd_dev(ctx, s, n, B, 1, s);
+  SvdDev f;
+  f.m = s;
+  f.n = n;
+  f.rank = k;
+  f.s.resize((size_t)k);
+  std::vector<double> inv((size_t)k);
+  for (int64_t i = 0; i < k; ++i) {
+    f.s[(size_t)i] = std::sqrt(h[(size_t)(s - 1 - i)]);
+    inv[(size_t)i] = 1.0 / f.s[(size_t)i];
+  }
+  f.U = DevBuf(sizeof(double) * s * k, ctx->stream);
+  f.V = DevBuf(sizeof(double) * n * k, ctx->stream);
+  // Ubar = eigenvectors in descending order
+  copy2d<double>(ctx, s, k, G.as<double>() + (s - 1) * s, 1, -s, f.U.as<double>(), 1, s);
+  DevBuf dinv(sizeof(double) * k, ctx->stream), Us(sizeof(double) * s * k, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(dinv.p, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
+  scale_cols_dev(ctx, s, k, f.U.as<double>(), dinv.as<double>(), Us.as<double>());
+  gemm<double>(ctx, n, k, s, 1.0, B, s, 1, Us.as<double>(), 1, s, 0.0, f.V.as<double>(), 1, n);  // V = B' Ubar / sigma
+  fix_column_signs(ctx, s, k, f.U.as<double>(), 1, s, f.V.as<double>(), 1, n, n, /*pair_cols=*/true);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return f;
+}
+
 // Write a column-major fp64 device block (rows x cols, ld) into an output operand.
 void store_block(rnla_ctx* ctx, const double* src, int64_t rows, int64_t cols, int64_t ld, OutMat& o) {
   if (o.dev.dtype == RNLA_F64)
@@ -134,10 +173,7 @@ struct KsvdWork {
     if constexpr (std::is_same<T, double>::value) {
       fix_column_signs(ctx, rows, cols, Y, 1, rows, nullptr, 0, 0, 0, true);
     } else {
-      DevBuf w(sizeof(double) * rows * cols, ctx->stream);
-      copy2d_cast<float, double>(ctx, rows, cols, Y, 1, rows, w.as<double>(), 1, rows);
-      fix_column_signs(ctx, rows, cols, w.as<double>(), 1, rows, nullptr, 0, 0, 0, true);
-      copy2d_cast<double, float>(ctx, rows, cols, w.as<double>(), 1, rows, Y, 1, rows);
+      fix_column_signs_f32(ctx, rows, cols, Y, 1, rows);
     }
   }
 
@@ -210,7 +246,7 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
     Bp = B64.as<double>();
   }
   const int64_t kk = std::min(k, std::min(s, n));
-  SvdDev small = condensed_svd_dev(ctx, s, n, Bp, 1, s);
+  SvdDev small = topk_svd_wide(ctx, s, n, Bp, kk);
   const int64_t rk = std::min(kk, small.rank);
   // U = Q Ubar (m x rk)
   DevBuf U64(sizeof(double) * m * std::max<int64_t>(rk, 1), ctx->stream);

@@ -31,8 +31,9 @@ void check_info(rnla_ctx* ctx, const DevBuf& info, const char* what) {
 
 // One CTA per column: the first entry with |m| > tol decides the sign
 // (src/core.cpp:15-33); flips the column of M and column/row j of P.
-__global__ void fix_signs_kernel(int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
-                                 int64_t p_rs, int64_t p_cs, int64_t p_len, int pair_cols, double tol) {
+template <class T>
+__global__ void fix_signs_kernel(int64_t rows, int64_t cols, T* M, int64_t m_rs, int64_t m_cs, T* P, int64_t p_rs,
+                                 int64_t p_cs, int64_t p_len, int pair_cols, double tol) {
   const int64_t j = blockIdx.x;
   if (j >= cols) return;
   __shared__ int64_t first;
@@ -40,17 +41,17 @@ __global__ void fix_signs_kernel(int64_t rows, int64_t cols, double* M, int64_t 
   __syncthreads();
   int64_t mine = INT64_MAX;
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x)
-    if (fabs(M[i * m_rs + j * m_cs]) > tol) { mine = i; break; }
+    if (fabs((double)M[i * m_rs + j * m_cs]) > tol) { mine = i; break; }
   if (mine != INT64_MAX) atomicMin((unsigned long long*)&first, (unsigned long long)mine);
   __syncthreads();
   if (first == INT64_MAX) return;
-  const double lead = M[first * m_rs + j * m_cs];
+  const T lead = M[first * m_rs + j * m_cs];
   __syncthreads();
-  if (!(lead < 0.0)) return;
+  if (!(lead < T(0))) return;
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) M[i * m_rs + j * m_cs] = -M[i * m_rs + j * m_cs];
   if (P)
     for (int64_t i = threadIdx.x; i < p_len; i += blockDim.x) {
-      double* q = pair_cols ? &P[i * p_rs + j * p_cs] : &P[j * p_rs + i * p_cs];
+      T* q = pair_cols ? &P[i * p_rs + j * p_cs] : &P[j * p_rs + i * p_cs];
       *q = -*q;
     }
 }
@@ -69,8 +70,16 @@ __global__ void upper_copy_kernel(int64_t n, const double* __restrict__ A, int64
 void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
                       int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols) {
   if (cols == 0) return;
-  fix_signs_kernel<<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, P, p_rs, p_cs, p_len,
-                                                            pair_cols ? 1 : 0, 1e-12);
+  fix_signs_kernel<double><<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, P, p_rs, p_cs, p_len,
+                                                                    pair_cols ? 1 : 0, 1e-12);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+void fix_column_signs_f32(rnla_ctx* ctx, int64_t rows, int64_t cols, float* M, int64_t m_rs, int64_t m_cs) {
+  if (cols == 0) return;
+  fix_signs_kernel<float><<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, nullptr, 0, 0, 0, 1,
+                                                                   1e-12);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }

@@ -9,6 +9,8 @@ namespace rnla {
 void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
                       int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols);
 
+void fix_column_signs_f32(rnla_ctx* ctx, int64_t rows, int64_t cols, float* M, int64_t m_rs, int64_t m_cs);
+
 // Householder thin QR of column-major A (m x n, ld m), in place: A <- Q;
 // R (n x n, upper, exact zeros below) written with strides (r_rs, r_cs).
 void qr_householder(rnla_ctx* ctx, int64_t m, int64_t n, double* A, double* R, int64_t r_rs, int64_t r_cs);
