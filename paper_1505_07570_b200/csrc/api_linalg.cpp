@@ -145,6 +145,7 @@ struct KsvdWork {
     DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream);
     DevBuf tmp(sizeof(T) * rows * cols, ctx->stream), Rt;
     if constexpr (!std::is_same<T, double>::value) Rt = DevBuf(sizeof(T) * cols * cols, ctx->stream);
+    bool signed_ok = false;
     for (int pass = 0; pass < 2; ++pass) {
       if constexpr (std::is_same<T, double>::value) {
         gemm<double>(ctx, cols, cols, rows, 1.0, Y, rows, 1, Y, 1, rows, 0.0, G.as<double>(), 1, cols);
@@ -156,6 +157,8 @@ struct KsvdWork {
       if (!cholesky_upper(ctx, cols, G.as<double>())) return false;
       if (!diag_ratio_ok(ctx, cols, G.as<double>(), std::is_same<T, double>::value ? 1e-5 : 1e-2)) return false;
       upper_inverse(ctx, cols, G.as<double>(), Rinv.as<double>());
+      // sign rule folded into the last R^-1: no extra pass over Q
+      if (pass == 1) signed_ok = presign_upper_inverse<T>(ctx, cols, Y, rows, Rinv.as<double>());
       if constexpr (std::is_same<T, double>::value) {
         gemm<double>(ctx, rows, cols, cols, 1.0, Y, 1, rows, Rinv.as<double>(), 1, cols, 0.0, tmp.as<double>(), 1,
                      rows);
@@ -165,7 +168,7 @@ struct KsvdWork {
       }
       RNLA_CUDA(cudaMemcpyAsync(Y, tmp.p, sizeof(T) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    sign_fix(ctx, rows, cols, Y);
+    if (!signed_ok) sign_fix(ctx, rows, cols, Y);
     return true;
   }
 
@@ -512,7 +515,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
       gemm<double>(ctx, d, d, n, 1.0, M.as<double>(), M.cs, M.rs, M.as<double>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
                    d);
     else
-      gemm_f32_in_f64(ctx, d, d, n, 1.0, M.as<float>(), M.cs, M.rs, M.as<float>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
+      gemm_f32_f64acc(ctx, d, d, n, 1.0, M.as<float>(), M.cs, M.rs, M.as<float>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
                       d);
     if (!cholesky_upper(ctx, d, G.as<double>()))
       throw NumericError("leverage_sample_rows: M'M is not positive definite (rank-deficient M)");

@@ -164,6 +164,11 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
       gemm<double>(ctx, s, s, rows, 1.0, Cb.as<double>(), rows, 1, Cb.as<double>(), 1, rows, 1.0, G.as<double>(), 1,
                    s);
     else
+      // exact fp32 products + fp64 accumulation (DMMA): at the reference's
+      // eigenvalue floor (eps * lam_max * n, src/spsd.cpp:202-205) W^+ keeps
+      // eigenvalues down to ~1e-11 lam_max, which amplifies Gram errors beyond
+      // what tensor-core fp32 accumulation allows (measured 5.7e-3 / 2.1 top-64
+      // error with BF16x3 / BF16x6 + double-float chunks vs 3.6e-7 here).
       gemm_f32_in_f64(ctx, s, s, rows, 1.0, Cb.as<float>(), rows, 1, Cb.as<float>(), 1, rows, 1.0, G.as<double>(), 1,
                       s);
   }

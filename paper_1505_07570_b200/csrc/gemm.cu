@@ -13,6 +13,7 @@
 // deterministic (the reference's determinism tests compare bitwise,
 // tests/test_sketch.cpp:170-182).
 #include "rnla_internal.h"
+#include "util.cuh"
 
 namespace rnla {
 
@@ -85,7 +86,10 @@ __global__ void __launch_bounds__(THREADS) gemm_f64_dmma(int64_t m, int64_t n, i
                                                          double alpha, const TI* __restrict__ A, int64_t a_rs,
                                                          int64_t a_cs, const TI* __restrict__ B, int64_t b_rs,
                                                          int64_t b_cs, double beta, double* C, int64_t c_rs,
-                                                         int64_t c_cs, double* ws) {
+                                                         int64_t c_cs, double* ws, int sym_upper) {
+  // sym_upper: C is symmetric (A = B'); tiles strictly below the diagonal are
+  // skipped and mirrored afterwards (half the Gram flops).
+  if (sym_upper && blockIdx.y > blockIdx.x) return;
   __shared__ __align__(16) double As[2][BM][BK + PAD];
   __shared__ __align__(16) double Bs[2][BN][BK + PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -224,6 +228,15 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_simt(int64_t m, int64_t n, i
     }
 }
 
+// C(i, j) = C(j, i) for the tiles a symmetric launch skipped (tile(i) > tile(j)).
+__global__ void mirror_lower_tiles(int64_t n, double* C, int64_t c_rs, int64_t c_cs) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    if (i / BM > j / BN) C[i * c_rs + j * c_cs] = C[j * c_rs + i * c_cs];
+  }
+}
+
 template <class T>
 __global__ void splitk_reduce(int64_t m, int64_t n, int splits, const T* __restrict__ ws, T alpha, T beta, T* C,
                               int64_t c_rs, int64_t c_cs) {
@@ -271,7 +284,7 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
   dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
   if constexpr (std::is_same<T, double>::value) {
     gemm_f64_dmma<double><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C,
-                                                    c_rs, c_cs, wsp);
+                                                    c_rs, c_cs, wsp, 0);
   } else {
     gemm_f32_simt<<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C,
                                                     c_rs, c_cs, wsp);
@@ -304,14 +317,21 @@ void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alph
     ws = DevBuf(sizeof(double) * (size_t)(splits * m * n), ctx->stream);
     wsp = ws.as<double>();
   }
+  // Gram products (B = A') are symmetric: compute the upper tiles only.
+  const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs) ? 1 : 0;
   dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
   gemm_f64_dmma<float><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta,
-                                                          C, c_rs, c_cs, wsp);
+                                                          C, c_rs, c_cs, wsp, sym);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
   if (splits > 1) {
     const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, (int64_t)ctx->num_sms * 8);
     splitk_reduce<double><<<blocks, 256, 0, ctx->stream>>>(m, n, (int)splits, wsp, alpha, beta, C, c_rs, c_cs);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+  if (sym) {
+    mirror_lower_tiles<<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, C, c_rs, c_cs);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
   }

@@ -32,8 +32,18 @@ void check_info(rnla_ctx* ctx, const DevBuf& info, const char* what) {
 // One CTA per column: the first entry with |m| > tol decides the sign
 // (src/core.cpp:15-33); flips the column of M and column/row j of P.
 template <class T>
-__global__ void fix_signs_kernel(int64_t rows, int64_t cols, T* M, int64_t m_rs, int64_t m_cs, T* P, int64_t p_rs,
-                                 int64_t p_cs, int64_t p_len, int pair_cols, double tol) {
+__global__ void flip_cols_kernel(int64_t rows, int64_t cols, T* M, int64_t m_rs, int64_t m_cs,
+                                 const int* __restrict__ flip) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (m_rs == 1) ? e % rows : e / cols, j = (m_rs == 1) ? e / rows : e % cols;
+    if (flip[j]) M[i * m_rs + j * m_cs] = -M[i * m_rs + j * m_cs];
+  }
+}
+
+template <class T>
+__global__ void fix_signs_kernel(int64_t rows, int64_t cols, const T* M, int64_t m_rs, int64_t m_cs, T* P,
+                                 int64_t p_rs, int64_t p_cs, int64_t p_len, int pair_cols, double tol, int* flip) {
   const int64_t j = blockIdx.x;
   if (j >= cols) return;
   __shared__ int64_t first;
@@ -48,7 +58,7 @@ __global__ void fix_signs_kernel(int64_t rows, int64_t cols, T* M, int64_t m_rs,
   const T lead = M[first * m_rs + j * m_cs];
   __syncthreads();
   if (!(lead < T(0))) return;
-  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) M[i * m_rs + j * m_cs] = -M[i * m_rs + j * m_cs];
+  if (threadIdx.x == 0) flip[j] = 1;  // the column of M is negated by flip_cols_kernel
   if (P)
     for (int64_t i = threadIdx.x; i < p_len; i += blockDim.x) {
       T* q = pair_cols ? &P[i * p_rs + j * p_cs] : &P[j * p_rs + i * p_cs];
@@ -70,18 +80,62 @@ __global__ void upper_copy_kernel(int64_t n, const double* __restrict__ A, int64
 void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int64_t m_rs, int64_t m_cs, double* P,
                       int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols) {
   if (cols == 0) return;
+  DevBuf flip(sizeof(int) * cols, ctx->stream);
+  RNLA_CUDA(cudaMemsetAsync(flip.p, 0, sizeof(int) * cols, ctx->stream));
   fix_signs_kernel<double><<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, P, p_rs, p_cs, p_len,
-                                                                    pair_cols ? 1 : 0, 1e-12);
+                                                                    pair_cols ? 1 : 0, 1e-12, flip.as<int>());
+  RNLA_CUDA(cudaGetLastError());
+  flip_cols_kernel<double><<<grid_for(ctx, rows * cols, 256), 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs,
+                                                                                      flip.as<int>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx, 2);
+}
+
+namespace {
+// q0_j = sum_p Y(0, p) Rinv(p, j) in fp64; negate column j of Rinv when
+// q0_j < 0 so that Q = Y Rinv comes out with the reference's sign rule
+// (first entry with |q| > 1e-12 non-negative, src/core.cpp:15-33). Entries
+// too close to zero to decide reliably raise *ambiguous.
+template <class T>
+__global__ void presign_kernel(int64_t cols, const T* __restrict__ Y, int64_t y_cs, double* Rinv, int* ambiguous) {
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    double q0 = 0.0;
+    for (int64_t p = 0; p <= j; ++p) q0 += (double)Y[p * y_cs] * Rinv[p + j * cols];
+    if (fabs(q0) < 1e-6) {
+      atomicOr(ambiguous, 1);
+    } else if (q0 < 0.0) {
+      for (int64_t p = 0; p <= j; ++p) Rinv[p + j * cols] = -Rinv[p + j * cols];
+    }
+  }
+}
+}  // namespace
+
+template <class T>
+bool presign_upper_inverse(rnla_ctx* ctx, int64_t cols, const T* Y, int64_t y_cs, double* Rinv) {
+  DevBuf flag(sizeof(int), ctx->stream);
+  RNLA_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
+  presign_kernel<T><<<1, 256, 0, ctx->stream>>>(cols, Y, y_cs, Rinv, flag.as<int>());
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
+  int h = 0;
+  RNLA_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h == 0;
 }
+template bool presign_upper_inverse<double>(rnla_ctx*, int64_t, const double*, int64_t, double*);
+template bool presign_upper_inverse<float>(rnla_ctx*, int64_t, const float*, int64_t, double*);
 
 void fix_column_signs_f32(rnla_ctx* ctx, int64_t rows, int64_t cols, float* M, int64_t m_rs, int64_t m_cs) {
   if (cols == 0) return;
+  DevBuf flip(sizeof(int) * cols, ctx->stream);
+  RNLA_CUDA(cudaMemsetAsync(flip.p, 0, sizeof(int) * cols, ctx->stream));
   fix_signs_kernel<float><<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, nullptr, 0, 0, 0, 1,
-                                                                   1e-12);
+                                                                   1e-12, flip.as<int>());
   RNLA_CUDA(cudaGetLastError());
-  note_launch(ctx);
+  flip_cols_kernel<float><<<grid_for(ctx, rows * cols, 256), 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs,
+                                                                                     flip.as<int>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx, 2);
 }
 
 void qr_householder(rnla_ctx* ctx, int64_t m, int64_t n, double* A, double* R, int64_t r_rs, int64_t r_cs) {

@@ -10,6 +10,11 @@ void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int6
                       int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols);
 
 void fix_column_signs_f32(rnla_ctx* ctx, int64_t rows, int64_t cols, float* M, int64_t m_rs, int64_t m_cs);
+// Flip columns of the upper-triangular Rinv so that Y * Rinv satisfies the sign
+// rule on its first row (Y row 0 at Y[p * y_cs]); false when a sign is not
+// decidable from row 0 (then fix the product with fix_column_signs).
+template <class T>
+bool presign_upper_inverse(rnla_ctx* ctx, int64_t cols, const T* Y, int64_t y_cs, double* Rinv);
 
 // Householder thin QR of column-major A (m x n, ld m), in place: A <- Q;
 // R (n x n, upper, exact zeros below) written with strides (r_rs, r_cs).

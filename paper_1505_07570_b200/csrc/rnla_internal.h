@@ -145,6 +145,25 @@ void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, co
                  int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
                  int64_t c_cs);
 
+// Same on tcgen05 with double-float (~fp64) accumulation across 256-row chunks, fp64 output.
+void gemm_f32_tc_f64acc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
+                        int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C,
+                        int64_t c_rs, int64_t c_cs);
+
+// Gram-type fp32 products with fp64-grade accumulation: tcgen05 double-float
+// when enabled, else the DMMA widening kernel below.
+void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
+                     int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
+                     int64_t c_cs);
+inline void gemm_f32_f64acc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                            int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta,
+                            double* C, int64_t c_rs, int64_t c_cs) {
+  if (tc_gemm_enabled())
+    gemm_f32_tc_f64acc(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs);
+  else
+    gemm_f32_in_f64(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs);
+}
+
 // fp32 operands, exact widening to fp64, DMMA fp64 accumulation (Gram-type products).
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                      int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
