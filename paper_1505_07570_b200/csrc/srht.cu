@@ -132,11 +132,15 @@ __global__ void __launch_bounds__(fwht_threads<T, LOGR, W>()) fwht_reg_kernel(co
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   auto sidx = [](int i, int c) { return i * W + c + (i / E) * PADB; };
-  const int tile = blockIdx.y;
+  // Low pass: grid (tile, row block) so the CTAs of neighbouring column tiles
+  // run together and consume both halves of each 128-B line; high pass: grid
+  // (il, tile) so neighbouring il (adjacent scratch rows) run together.
+  const int bx = HI ? blockIdx.x : blockIdx.y;
+  const int tile = HI ? blockIdx.y : blockIdx.x;
   int g0 = 0, g1 = 0;
   if (HI) {
-    g0 = grp_off[blockIdx.x];
-    g1 = grp_off[blockIdx.x + 1];
+    g0 = grp_off[bx];
+    g1 = grp_off[bx + 1];
     if (g0 == g1) return;  // no sampled output has these low bits (uniform per CTA)
   }
   const int64_t col_base = c0 + (int64_t)tile * W;
@@ -148,10 +152,10 @@ __global__ void __launch_bounds__(fwht_threads<T, LOGR, W>()) fwht_reg_kernel(co
     for (int e = 0; e < E; ++e) {
       const int i = rb * E + e;
       if (HI) {
-        const int64_t j = ((int64_t)i << qlo) + blockIdx.x;
+        const int64_t j = ((int64_t)i << qlo) + bx;
         v[e] = tsrc[j * W + c];
       } else {
-        const int64_t j = (int64_t)blockIdx.x * R + i, col = col_base + c;
+        const int64_t j = (int64_t)bx * R + i, col = col_base + c;
         v[e] = (j < n && col < L) ? __ldcs(src + j * ld + col) * (T)signs[j] : T(0);
       }
     }
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(fwht_threads<T, LOGR, W>()) fwht_reg_kernel(co
 #pragma unroll
       for (int m = 0; m < G; ++m) sm[sidx(lo + E * m, c)] = u[m];
     } else {
-      T* dst = scratch + ((int64_t)tile * big_n + (int64_t)blockIdx.x * R) * W;
+      T* dst = scratch + ((int64_t)tile * big_n + (int64_t)bx * R) * W;
 #pragma unroll
       for (int m = 0; m < G; ++m) dst[(int64_t)(lo + E * m) * W + c] = u[m];
     }
@@ -231,7 +235,10 @@ void srht_fast_w(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, i
                  int64_t out_cs) {
   const int64_t big_n = plan.big_n;
   const int64_t tile_bytes = big_n * W * (int64_t)sizeof(T);
-  int64_t tiles_per_strip = std::max<int64_t>(1, ((int64_t)64 << 20) / tile_bytes);
+  // a strip = the column tiles that together cover whole 128-B lines
+  // (launched adjacently), sized to ~128 MB of scratch so it mostly stays in L2
+  const int64_t line_tiles = std::max<int64_t>(1, 128 / (W * (int64_t)sizeof(T)));
+  int64_t tiles_per_strip = std::max<int64_t>(line_tiles, ((int64_t)128 << 20) / tile_bytes / line_tiles * line_tiles);
   const int64_t total_tiles = (L + W - 1) / W;
   tiles_per_strip = std::min(tiles_per_strip, total_tiles);
   DevBuf scratch(sizeof(T) * (size_t)(big_n * W * tiles_per_strip), ctx->stream);
@@ -239,7 +246,7 @@ void srht_fast_w(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, i
   for (int64_t t0 = 0; t0 < total_tiles; t0 += tiles_per_strip) {
     const int64_t nt = std::min(tiles_per_strip, total_tiles - t0);
     const int64_t c0 = t0 * W;
-    const dim3 g1((unsigned)(big_n >> plan.qlo), (unsigned)nt), g2((unsigned)((int64_t)1 << plan.qlo), (unsigned)nt);
+    const dim3 g1((unsigned)nt, (unsigned)(big_n >> plan.qlo)), g2((unsigned)((int64_t)1 << plan.qlo), (unsigned)nt);
 #define RNLA_PASS(LOGR, HI, GRID)                                                                                 \
   launch_fwht_reg<T, LOGR, W, HI>(ctx, GRID, HI ? scratch.as<T>() : in, ld, plan.n, L, plan.signs.as<int8_t>(), \
                                   plan.qlo, c0, scratch.as<T>(), big_n, plan, scale, out, out_rs, out_cs)
@@ -260,7 +267,7 @@ bool srht_fast(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int
                int64_t out_cs) {
   auto ok = [](int q) { return q >= 9 && q <= 11; };
   if (!ok(plan.qlo) || !ok(plan.qhi)) return false;
-  constexpr int W = 128 / sizeof(T);  // 128-B row chunks: no DRAM over-fetch on the strided rows
+  constexpr int W = 64 / sizeof(T);  // 64-B row chunks; paired tiles cover each 128-B line
   if (plan.qlo == 11 || plan.qhi == 11) srht_fast_w<T, W / 2>(ctx, plan, in, ld, L, out, out_rs, out_cs);
   else srht_fast_w<T, W>(ctx, plan, in, ld, L, out, out_rs, out_cs);
   return true;
@@ -306,6 +313,9 @@ template <class T>
 void srht_segments(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int64_t L, T* out, int64_t out_rs,
                    int64_t out_cs) {
   if (L == 0) return;
+  if constexpr (std::is_same<T, float>::value) {
+    if (!std::getenv("RNLA_SRHT_GENERIC") && srht_tma_f32(ctx, plan, in, ld, L, out, out_rs, out_cs)) return;
+  }
   if (!std::getenv("RNLA_SRHT_GENERIC") && srht_fast<T>(ctx, plan, in, ld, L, out, out_rs, out_cs)) return;
   constexpr int W = sizeof(T) == 8 ? 8 : 16;
   const int64_t big_n = plan.big_n;

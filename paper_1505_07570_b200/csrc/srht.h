@@ -14,6 +14,10 @@ struct SrhtPlan {
   SrhtPlan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed);
 };
 
+// TMA-fed fp32 path (srht_tma.cu); false when the shape/alignment does not apply.
+bool srht_tma_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
+                  int64_t out_rs, int64_t out_cs);
+
 // out_t[c] (t < s, c < L) at out[t*out_rs + c*out_cs]; segment j at in + j*ld.
 template <class T>
 void srht_segments(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int64_t L, T* out, int64_t out_rs,
