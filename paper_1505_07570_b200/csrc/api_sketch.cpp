@@ -192,7 +192,8 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
   const int64_t Lo = L + (extra ? 1 : 0);
   const int kind = spec->kind;
   const bool sharded = ctx->world > 1;
-  if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN && sharded) {
+  static const bool force_pipeline = std::getenv("RNLA_PIPELINE") != nullptr;  // tuning knob
+  if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN && (sharded || force_pipeline)) {
     combined_gaussian_pipelined<T>(ctx, M, ld, extra, xs, n, L, spec, row_offset, out, o_rs, o_cs);
     return;
   }
