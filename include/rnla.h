@@ -196,6 +196,13 @@ rnla_status rnla_pseudo_inverse(rnla_ctx* ctx, const rnla_mat* a, double tol, rn
 rnla_status rnla_prototype_ksvd(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, uint64_t seed,
                                 const rnla_sketch_spec* spec, int32_t power_iters, rnla_mat* u, double* sv,
                                 rnla_mat* v, int64_t* rank, int32_t* passes, double* error_fro);
+/* faster_ksvd, randsvd.hpp:38-41 (src/randsvd.cpp:112-160): column count
+ * sketch C = A S (s), joint row sketch of [A, C] (count p_cs -> Gaussian p),
+ * QR of D, rank-k SVD of Q_D' L, back-substitution and a final small SVD.
+ * Exactly two passes over A. Requires k < s < p < p_cs. u m x k, sv[k], v n x k. */
+rnla_status rnla_faster_ksvd(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, int64_t p_cs, int64_t p,
+                             uint64_t seed, rnla_mat* u, double* sv, rnla_mat* v, int64_t* rank, int32_t* passes,
+                             double* error_fro);
 
 /* ---- regression (include/randnla/regression.hpp) ------------------------ */
 /* lsr_sketched, regression.hpp:31-32 (src/regression.cpp:68-92). x[d];

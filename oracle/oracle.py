@@ -274,6 +274,24 @@ def prototype_ksvd(a: np.ndarray, k: int, s: int, seed: int, q: int = 0):
     return qy @ ub, sv, v, 2 + 2 * q
 
 
+def faster_ksvd(a: np.ndarray, k: int, s: int, p_cs: int, p: int, seed: int):
+    """src/randsvd.cpp:112-160: two passes; column count sketch C, then one joint
+    combined (count p_cs -> Gaussian p) row sketch of [A, C]."""
+    a = np.asarray(a, dtype=np.float64)
+    if not (1 <= k < s < p < p_cs):
+        raise ValueError("faster_ksvd: need k < s < p < p_cs")
+    n = a.shape[1]
+    c = count_sketch(a, s, derive_seed(seed, 1))
+    mid = count_sketch_rows(np.hstack([a, c]), p_cs, derive_seed(seed, 2))
+    mid = gaussian_sketch(mid.T, p, derive_seed(seed, 3)).T  # p x (n + s)
+    l, d = mid[:, :n], mid[:, n:]
+    qd, rd = thin_qr(d)
+    u, sv, v = truncated_svd(qd.T @ l, k)
+    back = c @ (pseudo_inverse(rd) @ (u * sv))
+    uf, sf, vf = condensed_svd(back)
+    return uf, sf, v @ vf, 2
+
+
 def numerical_rank(m: np.ndarray, thresh: float = 1e-10) -> int:
     sv = np.linalg.svd(m, compute_uv=False)
     return int(np.sum(sv > thresh * sv[0])) if sv.size and sv[0] > 0 else 0

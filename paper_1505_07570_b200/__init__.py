@@ -31,7 +31,7 @@ __all__ = [
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
     "count_sketch", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
     "leverage_sample_columns", "leverage_sample_rows", "thin_qr", "condensed_svd", "truncated_svd",
-    "pseudo_inverse", "prototype_ksvd", "lsr_sketched", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig",
+    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig",
     "shard_rows",
 ]
 
@@ -531,6 +531,27 @@ def prototype_ksvd(a, k: int, s: int, seed: int, spec: Optional[SketchSpec] = No
         _ctx(ctx).handle, C.byref(am), k, s, C.c_uint64(seed), C.byref(cs) if cs is not None else None,
         int(power_iters), C.byref(um), sv.ctypes.data_as(_abi._F64P), C.byref(vm), C.byref(rank), C.byref(passes),
         C.byref(err) if opts.evaluate_error else None))
+    rk = rank.value
+    return KsvdResult(SvdFactors(u[:, :rk], sv[:rk].copy(), v[:, :rk]), int(passes.value),
+                      float(err.value) if opts.evaluate_error else None)
+
+
+def faster_ksvd(a, k: int, s: int, p_cs: int, p: int, seed: int, opts: KsvdOptions = KsvdOptions(),
+                ctx: Optional[Context] = None) -> KsvdResult:
+    """Two-pass k-SVD: column count sketch C, joint combined row sketch of [A, C]
+    (include/randnla/randsvd.hpp:38-41, src/randsvd.cpp:112-160)."""
+    a2 = _as2d(a)
+    m, n = a2.shape
+    if not (1 <= k < s < p < p_cs):
+        raise ValueError("faster_ksvd: need k < s < p < p_cs")
+    u = _empty_like(a2, m, k, "F")
+    v = _empty_like(a2, n, k, "F")
+    sv = np.empty(k, dtype=np.float64)
+    rank, passes, err = C.c_int64(), C.c_int32(), C.c_double()
+    am, um, vm = _mat(a2), _mat(u), _mat(v)
+    _check(_abi.lib().rnla_faster_ksvd(
+        _ctx(ctx).handle, C.byref(am), k, s, p_cs, p, C.c_uint64(seed), C.byref(um), sv.ctypes.data_as(_abi._F64P),
+        C.byref(vm), C.byref(rank), C.byref(passes), C.byref(err) if opts.evaluate_error else None))
     rk = rank.value
     return KsvdResult(SvdFactors(u[:, :rk], sv[:rk].copy(), v[:, :rk]), int(passes.value),
                       float(err.value) if opts.evaluate_error else None)

@@ -25,4 +25,10 @@ void scale_rows_dev(rnla_ctx* ctx, int64_t r, int64_t n, const double* V, const 
 void scale_cols_dev(rnla_ctx* ctx, int64_t n, int64_t r, const double* V, const double* d, double* out);
 double sum_squares_dev(rnla_ctx* ctx, const double* p, int64_t count);
 
+// Row sketch of a row-major tall M (n rows of length L, row stride ld) into
+// out (element (t, c) at out[t*o_rs + c*o_cs]); api_sketch.cpp.
+template <class T>
+void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int64_t xs, int64_t n, int64_t L,
+                     const rnla_sketch_spec* spec, int64_t row_offset, T* out, int64_t o_rs, int64_t o_cs);
+
 }  // namespace rnla

@@ -291,11 +291,120 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   vo.finish(ctx);
 }
 
+// ---------------------------------------------------------------------------
+// faster_ksvd (src/randsvd.cpp:112-160), fp64 working precision
+// ---------------------------------------------------------------------------
+const DenseOperator& gaussian_operator(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int dtype);
+
+// ||A - U diag(s) V'||_F, row blocks of A (column-major fp64 A, U m x r, V n x r).
+static double residual_fro_f64(rnla_ctx* ctx, const double* A, int64_t m, int64_t n, const double* U,
+                               const std::vector<double>& s, const double* V) {
+  const int64_t r = (int64_t)s.size();
+  DevBuf sd(sizeof(double) * std::max<int64_t>(r, 1), ctx->stream), SVt(sizeof(double) * std::max<int64_t>(r * n, 1),
+                                                                        ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(sd.p, s.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
+  scale_rows_dev(ctx, r, n, V, sd.as<double>(), SVt.as<double>());
+  DevBuf R(sizeof(double) * m * n, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(R.p, A, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  gemm<double>(ctx, m, n, r, -1.0, U, 1, m, SVt.as<double>(), 1, r, 1.0, R.as<double>(), 1, m);
+  const double t = sum_squares_dev(ctx, R.as<double>(), m * n);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return std::sqrt(t);
+}
+
+void faster_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, int64_t p_cs, int64_t p, uint64_t seed,
+                      const rnla_mat* u_out, double* sv_out, const rnla_mat* v_out, int64_t* rank_out,
+                      int32_t* passes_out, double* error_fro) {
+  const int64_t m = a->rows, n = a->cols;
+  OutMat uo(ctx, u_out, m, k, "faster_ksvd: U", false), vo(ctx, v_out, n, k, "faster_ksvd: V", false);
+  DevMat A = f64_colmajor(ctx, a);
+  const double* Ap = A.as<double>();
+  // pass 1: C = A S (count sketch of the columns, seed derive_seed(seed, 1)) -> m x s column-major
+  DevBuf C(sizeof(double) * m * s, ctx->stream);
+  count_sketch_segments<double>(ctx, Ap, A.cs, nullptr, 1, n, m, s, derive_seed(seed, 1), 0, C.as<double>(), m,
+                                false);
+  // pass 2: joint row sketch of [A, C] (count p_cs -> Gaussian p), rows keyed by their index
+  const int64_t w = n + s;
+  DevBuf AC(sizeof(double) * m * w, ctx->stream);
+  copy2d<double>(ctx, m, n, Ap, 1, A.cs, AC.as<double>(), w, 1);
+  copy2d<double>(ctx, m, s, C.as<double>(), 1, m, AC.as<double>() + n, w, 1);
+  DevBuf sk(sizeof(double) * p * w, ctx->stream);
+  {
+    rnla_sketch_spec sp{};
+    sp.kind = RNLA_SKETCH_COMBINED;
+    sp.s = p_cs;
+    sp.seed = derive_seed(seed, 2);
+    sp.stage2_kind = RNLA_SKETCH_GAUSSIAN;
+    sp.stage2_s = p;
+    sp.stage2_seed = derive_seed(seed, 3);
+    sketch_rows_dev<double>(ctx, AC.as<double>(), w, nullptr, 1, m, w, &sp, 0, sk.as<double>(), w, 1);
+  }
+  // L = sk[:, :n] (p x n), D = sk[:, n:] (p x s); thin_qr(D)
+  DevBuf D(sizeof(double) * p * s, ctx->stream), Rd(sizeof(double) * s * s, ctx->stream);
+  copy2d<double>(ctx, p, s, sk.as<double>() + n, w, 1, D.as<double>(), 1, p);
+  thin_qr_dev(ctx, p, s, D.as<double>(), Rd.as<double>());
+  // small = truncated_svd(Q_D' L, k)
+  DevBuf QtL(sizeof(double) * s * n, ctx->stream);
+  gemm<double>(ctx, s, n, p, 1.0, D.as<double>(), p, 1, sk.as<double>(), w, 1, 0.0, QtL.as<double>(), 1, s);
+  SvdDev small = condensed_svd_dev(ctx, s, n, QtL.as<double>(), 1, s);
+  const int64_t k1 = std::min(k, small.rank);
+  // back = C pinv(R_D) (Ubar Sigma): m x k1
+  DevBuf pinv(sizeof(double) * s * s, ctx->stream);
+  {
+    DevBuf Ur(sizeof(double) * s * s, ctx->stream), Vr(sizeof(double) * s * s, ctx->stream),
+        Sr(sizeof(double) * s, ctx->stream), inv(sizeof(double) * s, ctx->stream), Vs(sizeof(double) * s * s,
+                                                                                         ctx->stream);
+    svd_thin(ctx, s, s, Rd.as<double>(), 1, s, Ur.as<double>(), Sr.as<double>(), Vr.as<double>());
+    std::vector<double> hs((size_t)s), hinv((size_t)s, 0.0);
+    RNLA_CUDA(cudaMemcpyAsync(hs.data(), Sr.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < s; ++i)
+      if (hs[0] > 0.0 && hs[(size_t)i] > 1e-12 * hs[0]) hinv[(size_t)i] = 1.0 / hs[(size_t)i];
+    RNLA_CUDA(cudaMemcpyAsync(inv.p, hinv.data(), sizeof(double) * s, cudaMemcpyHostToDevice, ctx->stream));
+    scale_cols_dev(ctx, s, s, Vr.as<double>(), inv.as<double>(), Vs.as<double>());
+    gemm<double>(ctx, s, s, s, 1.0, Vs.as<double>(), 1, s, Ur.as<double>(), s, 1, 0.0, pinv.as<double>(), 1, s);
+  }
+  DevBuf sd(sizeof(double) * std::max<int64_t>(k1, 1), ctx->stream), US(sizeof(double) * s * std::max<int64_t>(k1, 1),
+                                                                         ctx->stream),
+      T(sizeof(double) * s * std::max<int64_t>(k1, 1), ctx->stream),
+      back(sizeof(double) * m * std::max<int64_t>(k1, 1), ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(sd.p, small.s.data(), sizeof(double) * k1, cudaMemcpyHostToDevice, ctx->stream));
+  scale_cols_dev(ctx, s, k1, small.U.as<double>(), sd.as<double>(), US.as<double>());
+  gemm<double>(ctx, s, k1, s, 1.0, pinv.as<double>(), 1, s, US.as<double>(), 1, s, 0.0, T.as<double>(), 1, s);
+  gemm<double>(ctx, m, k1, s, 1.0, C.as<double>(), 1, m, T.as<double>(), 1, s, 0.0, back.as<double>(), 1, m);
+  SvdDev fin = condensed_svd_dev(ctx, m, k1, back.as<double>(), 1, m);
+  const int64_t r = fin.rank;
+  DevBuf Vout(sizeof(double) * n * std::max<int64_t>(r, 1), ctx->stream);
+  gemm<double>(ctx, n, r, k1, 1.0, small.V.as<double>(), 1, n, fin.V.as<double>(), 1, k1, 0.0, Vout.as<double>(), 1,
+               n);
+  store_block(ctx, fin.U.as<double>(), m, r, m, uo);
+  store_block(ctx, Vout.as<double>(), n, r, n, vo);
+  for (int64_t i = 0; i < r; ++i) sv_out[i] = fin.s[(size_t)i];
+  *rank_out = r;
+  *passes_out = 2;
+  if (error_fro) *error_fro = residual_fro_f64(ctx, Ap, m, n, fin.U.as<double>(), fin.s, Vout.as<double>());
+  uo.finish(ctx);
+  vo.finish(ctx);
+}
+
 }  // namespace rnla
 
 using namespace rnla;
 
 extern "C" {
+
+rnla_status rnla_faster_ksvd(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, int64_t p_cs, int64_t p,
+                             uint64_t seed, rnla_mat* u, double* sv, rnla_mat* v, int64_t* rank, int32_t* passes,
+                             double* error_fro) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "faster_ksvd: a");
+    require(k >= 1 && k < s && s < p && p < p_cs, "faster_ksvd: need k < s < p < p_cs");
+    require(ctx->world == 1, "faster_ksvd: row-sharded contexts are not supported");
+    require(sv && rank && passes, "faster_ksvd: null output");
+    faster_ksvd_impl(ctx, a, k, s, p_cs, p, seed, u, sv, v, rank, passes, error_fro);
+  });
+}
 
 rnla_status rnla_thin_qr(rnla_ctx* ctx, const rnla_mat* a, rnla_mat* q, rnla_mat* r) {
   return guard([&] {

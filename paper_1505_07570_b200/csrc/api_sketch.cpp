@@ -351,6 +351,9 @@ void apply_columns(rnla_ctx* ctx, const rnla_mat* a, const rnla_sketch_spec* spe
   o.finish(ctx);
 }
 
+template void sketch_rows_dev<double>(rnla_ctx*, const double*, int64_t, const double*, int64_t, int64_t, int64_t,
+                                      const rnla_sketch_spec*, int64_t, double*, int64_t, int64_t);
+
 }  // namespace rnla
 
 using namespace rnla;

@@ -126,3 +126,50 @@ def test_prototype_count_spec(ctx):
 def test_prototype_argument_checks(ctx):
     with pytest.raises(ValueError, match="k <= s <= min"):
         rn.prototype_ksvd(np.ones((10, 8)), 5, 9, 1, ctx=ctx)
+
+
+def test_faster_ksvd_recovers_low_rank(ctx):
+    # tests/test_randsvd.cpp:61-72
+    a = orc.gaussian_matrix(120, 4, 6) @ orc.gaussian_matrix(4, 100, 60)
+    r = rn.faster_ksvd(a, 4, 16, 256, 64, 9, opts=rn.KsvdOptions(True), ctx=ctx)
+    assert r.error_fro <= 1e-6 * np.linalg.norm(a)
+    assert r.passes_over_a == 2
+    U = r.factors.U
+    assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-8
+
+
+def test_faster_ksvd_argument_checks(ctx):
+    # tests/test_randsvd.cpp:74-79
+    a = orc.gaussian_matrix(30, 30, 10)
+    for args in [(5, 5, 40, 20), (5, 10, 20, 20), (5, 10, 15, 20)]:
+        with pytest.raises(ValueError, match="k < s < p < p_cs"):
+            rn.faster_ksvd(a, *args, 1, ctx=ctx)
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_faster_ksvd_matches_oracle(ctx, on_device):
+    rng = np.random.default_rng(5)
+    m, n, k, s, p_cs, p = 3000, 400, 10, 24, 512, 96
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = np.exp(-np.arange(1, n + 1) / 8.0)
+    a = (u * sig) @ v.T + 1e-6 * rng.standard_normal((m, n))
+    r = rn.faster_ksvd(dev(a) if on_device else a, k, s, p_cs, p, 31, opts=rn.KsvdOptions(True), ctx=ctx)
+    uo, so, vo, passes = orc.faster_ksvd(a, k, s, p_cs, p, 31)
+    assert r.passes_over_a == passes == 2
+    sv = r.factors.singular_values
+    assert sv.size == so.size
+    assert np.max(np.abs(sv - so) / so) <= 1e-8
+    U = r.factors.U.cpu().numpy() if on_device else r.factors.U
+    V = r.factors.V.cpu().numpy() if on_device else r.factors.V
+    assert np.max(np.abs(U[:, :3] - uo[:, :3])) <= 1e-6
+    assert np.max(np.abs(V[:, :3] - vo[:, :3])) <= 1e-6
+    ref_err = np.linalg.norm(a - (uo * so) @ vo.T)
+    assert abs(r.error_fro - ref_err) <= 1e-8 * np.linalg.norm(a)
+
+
+def test_faster_ksvd_fp32_input(ctx):
+    a = (orc.gaussian_matrix(500, 6, 2) @ orc.gaussian_matrix(6, 300, 3)).astype(np.float32)
+    r = rn.faster_ksvd(dev(a), 6, 12, 200, 48, 4, opts=rn.KsvdOptions(True), ctx=ctx)
+    assert r.factors.U.dtype == torch.float32
+    assert r.error_fro <= 1e-5 * np.linalg.norm(a.astype(np.float64))

@@ -112,6 +112,20 @@ def test_gaussian_sketch_fp32(ctx):
     assert relf(got, orc.gaussian_sketch(a.astype(np.float64), 150, 9)) <= 1e-4
 
 
+@pytest.mark.parametrize("m,n,s,order", [(256, 16384, 150, "C"), (256, 16384, 150, "F"), (8192, 2048, 30, "C"),
+                                         (3000, 4096, 160, "F"), (130, 700, 17, "C")])
+def test_tcgen05_bf16x3_gemm_precision(ctx, m, n, s, order):
+    # fp32 Gaussian sketch = A * Omega on tcgen05 (BF16x3 split, TMEM partial sums
+    # promoted every 512 k): K-contiguous (C) and MN-contiguous (F) operands,
+    # split-K and ragged tiles; error stays ~5e-6 independent of K.
+    rng = np.random.default_rng(m + n)
+    a = np.asarray(rng.standard_normal((m, n)), dtype=np.float32, order=order)
+    ta = dev(a) if order == "C" else dev(np.ascontiguousarray(a.T)).t()
+    got = rn.gaussian_sketch(ta, s, 31 + s, ctx=ctx).cpu().numpy()
+    err = relf(got, orc.gaussian_sketch(a.astype(np.float64), s, 31 + s))
+    assert err <= 2e-5, err
+
+
 def test_gaussian_norm_in_expectation(ctx):
     # tests/test_sketch.cpp:37-45
     a = orc.gaussian_matrix(10, 50, 1)

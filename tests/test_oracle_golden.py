@@ -228,3 +228,14 @@ def test_count_sketch_edge_sizes(n, s):
     for j in range(n):
         ref[b[j]] += g[j] * m[j]
     assert np.array_equal(out, ref)
+
+
+def test_oracle_faster_ksvd_recovers_low_rank():
+    # tests/test_randsvd.cpp:61-79 restated on the oracle
+    a = orc.gaussian_matrix(120, 4, 6) @ orc.gaussian_matrix(4, 100, 60)
+    u, s, v, passes = orc.faster_ksvd(a, 4, 16, 256, 64, 9)
+    assert passes == 2
+    assert np.linalg.norm(a - (u * s) @ v.T) <= 1e-6 * np.linalg.norm(a)
+    assert np.linalg.norm(u.T @ u - np.eye(u.shape[1])) <= 1e-8
+    with pytest.raises(ValueError):
+        orc.faster_ksvd(a, 5, 10, 15, 20, 1)

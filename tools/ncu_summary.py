@@ -1,0 +1,24 @@
+"""Summarise an ncu --set full report: key throughput / stall metrics per kernel launch (JSON to stdout)."""
+import csv, io, json, subprocess, sys
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h, u = rows[0], rows[1]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes.sum.per_second",
+        "lts__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_op_hmma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "launch__grid_size",
+        "launch__block_size", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+out = []
+for r in rows[2:]:
+    d = {}
+    for w in want:
+        for i, k in enumerate(h):
+            if k == w:
+                d[w] = r[i] + (" " + u[i] if u[i] else "")
+    out.append(d)
+print(json.dumps(out, indent=1))
