@@ -100,6 +100,16 @@ rnla_status rnla_ctx_create(int device, rnla_ctx** out);
  * rank 0 and broadcast by the caller. */
 rnla_status rnla_ctx_create_dist(int device, int world, int rank, const void* nccl_unique_id, rnla_ctx** out);
 rnla_status rnla_nccl_unique_id(void* out128);
+/* In-process shard group: `world` contexts driven by `world` host threads of
+ * one process (any devices, including several ranks on one GPU). Collectives
+ * are staged through pinned host memory and summed in rank order, so results
+ * are bitwise identical on every rank and independent of the device count;
+ * no kernel ever waits on another rank's kernel. Same shard semantics as
+ * rnla_ctx_create_dist. The group must outlive its contexts. */
+typedef struct rnla_group rnla_group;
+rnla_status rnla_group_create(int world, rnla_group** out);
+void rnla_group_destroy(rnla_group* group);
+rnla_status rnla_ctx_create_grouped(int device, rnla_group* group, int rank, rnla_ctx** out);
 void rnla_ctx_destroy(rnla_ctx* ctx);
 rnla_status rnla_ctx_synchronize(rnla_ctx* ctx);
 /* The context's CUDA stream (a cudaStream_t), for callers that time with events. */

@@ -25,7 +25,7 @@ import numpy as np
 from . import _abi
 
 __all__ = [
-    "Context", "default_context", "SketchKind", "SketchSpec", "ColumnSelection", "SvdFactors", "QrFactors",
+    "Context", "ShardGroup", "default_context", "SketchKind", "SketchSpec", "ColumnSelection", "SvdFactors", "QrFactors",
     "KsvdResult", "KsvdOptions", "LsrSolution", "KernelSpec", "KernelView", "NystromFactor", "NumericError",
     "CudaError", "splitmix64", "derive_seed", "count_sketch_hashes", "gaussian_matrix",
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
@@ -58,13 +58,38 @@ def _check(status: int) -> None:
 # --------------------------------------------------------------------------
 # context
 # --------------------------------------------------------------------------
+class ShardGroup:
+    """In-process shard group (rnla_group): `world` contexts driven by `world`
+    host threads; collectives are staged through host memory and summed in rank
+    order. Create one Context per rank with ``Context(device, group=g, rank=r)``."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(_abi.lib().rnla_group_create(int(world), C.byref(h)))
+        self._h = h
+        self.world = int(world)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().rnla_group_destroy(self._h)
+            self._h = None
+
+
 class Context:
     """One CUDA device: stream, workspace and cached operators (rnla_ctx)."""
 
-    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None):
+    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 group: Optional[ShardGroup] = None):
         lib = _abi.lib()
         h = C.c_void_p()
-        if world > 1:
+        if group is not None:
+            _check(lib.rnla_ctx_create_grouped(device, group.handle, rank, C.byref(h)))
+            world = group.world
+        elif world > 1:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _check(lib.rnla_ctx_create_dist(device, world, rank, buf, C.byref(h)))
         else:

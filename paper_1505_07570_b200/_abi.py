@@ -56,6 +56,9 @@ SIGNATURES = {
     "rnla_last_error": (C.c_char_p, []),
     "rnla_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "rnla_ctx_create_dist": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(_P)]),
+    "rnla_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "rnla_group_destroy": (None, [_P]),
+    "rnla_ctx_create_grouped": (C.c_int, [C.c_int, _P, C.c_int, C.POINTER(_P)]),
     "rnla_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "rnla_ctx_destroy": (None, [_P]),
     "rnla_ctx_synchronize": (C.c_int, [_P]),

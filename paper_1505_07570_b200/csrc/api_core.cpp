@@ -6,6 +6,7 @@
 
 #include <new>
 
+#include "dist.h"
 #include "marshal.h"
 
 namespace rnla {
@@ -227,6 +228,29 @@ rnla_status rnla_ctx_create(int device, rnla_ctx** out) {
     require(out != nullptr, "rnla_ctx_create: null out");
     auto c = std::make_unique<rnla_ctx>();
     ctx_init(c.get(), device);
+    *out = c.release();
+  });
+}
+
+rnla_status rnla_group_create(int world, rnla_group** out) {
+  return guard([&] {
+    require(out != nullptr && world >= 1, "rnla_group_create: bad argument");
+    *out = group_create(world);
+  });
+}
+
+void rnla_group_destroy(rnla_group* group) { group_destroy(group); }
+
+rnla_status rnla_ctx_create_grouped(int device, rnla_group* group, int rank, rnla_ctx** out) {
+  return guard([&] {
+    require(out != nullptr && group != nullptr, "rnla_ctx_create_grouped: null argument");
+    const int world = group_world(group);
+    require(rank >= 0 && rank < world, "rnla_ctx_create_grouped: bad rank");
+    auto c = std::make_unique<rnla_ctx>();
+    ctx_init(c.get(), device);
+    c->world = world;
+    c->rank = rank;
+    c->group = group;
     *out = c.release();
   });
 }

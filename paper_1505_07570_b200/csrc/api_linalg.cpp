@@ -10,6 +10,7 @@
 #include <numeric>
 
 #include "algos.h"
+#include "dist.h"
 #include "linalg.cuh"
 #include "marshal.h"
 #include "rbf.cuh"
@@ -135,13 +136,47 @@ struct KsvdWork {
   // of the same range gives the same Q up to rounding (SURVEY A.6 measured
   // Householder vs CholeskyQR2 top-20 sigma within 1e-15). A Cholesky
   // breakdown (numerically rank-deficient Y) falls back to Householder.
-  static void orth(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, int64_t ld_unused) {
-    (void)ld_unused;
-    if (rows >= 4 * cols && cholqr2(ctx, rows, cols, Y)) return;
+  //
+  // Row-sharded Y (`sharded`: this rank's consecutive row block, SURVEY
+  // §8(e)): the Gram is allreduced (every rank then factors the identical
+  // matrix and takes the same branch), the breakdown fallback is TSQR
+  // (local Householder, allgather of the R factors, QR of the stack), and the
+  // sign rule is decided on the global row order.
+  static void orth(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, bool sharded) {
+    if (sharded) {
+      if (cholqr2(ctx, rows, cols, Y, true)) return;
+      tsqr(ctx, rows, cols, Y);
+      return;
+    }
+    if (rows >= 4 * cols && cholqr2(ctx, rows, cols, Y, false)) return;
     householder(ctx, rows, cols, Y);
   }
 
-  static bool cholqr2(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
+  static void tsqr(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
+    const int W = ctx->world;
+    DevBuf w(sizeof(double) * rows * cols, ctx->stream), r(sizeof(double) * cols * cols, ctx->stream),
+        all(sizeof(double) * W * cols * cols, ctx->stream), stack(sizeof(double) * W * cols * cols, ctx->stream),
+        rr(sizeof(double) * cols * cols, ctx->stream), qw(sizeof(double) * rows * cols, ctx->stream);
+    if constexpr (std::is_same<T, double>::value)
+      RNLA_CUDA(cudaMemcpyAsync(w.p, Y, sizeof(double) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      copy2d_cast<float, double>(ctx, rows, cols, Y, 1, rows, w.as<double>(), 1, rows);
+    thin_qr_dev(ctx, rows, cols, w.as<double>(), r.as<double>());
+    allgather_blocks(ctx, r.p, all.p, (size_t)(cols * cols), RNLA_F64);
+    for (int q = 0; q < W; ++q)  // stacked (W cols) x cols, rank blocks in order
+      copy2d<double>(ctx, cols, cols, all.as<double>() + (int64_t)q * cols * cols, 1, cols,
+                     stack.as<double>() + (int64_t)q * cols, 1, (int64_t)W * cols);
+    thin_qr_dev(ctx, (int64_t)W * cols, cols, stack.as<double>(), rr.as<double>());
+    gemm<double>(ctx, rows, cols, cols, 1.0, w.as<double>(), 1, rows, stack.as<double>() + (int64_t)ctx->rank * cols, 1,
+                 (int64_t)W * cols, 0.0, qw.as<double>(), 1, rows);
+    if constexpr (std::is_same<T, double>::value)
+      RNLA_CUDA(cudaMemcpyAsync(Y, qw.p, sizeof(double) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      copy2d_cast<double, float>(ctx, rows, cols, qw.as<double>(), 1, rows, Y, 1, rows);
+    fix_column_signs_sharded<T>(ctx, rows, cols, Y, 1, rows, nullptr, 0, 0, 0, false);
+  }
+
+  static bool cholqr2(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, bool sharded) {
     DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream);
     DevBuf tmp(sizeof(T) * rows * cols, ctx->stream), Rt;
     if constexpr (!std::is_same<T, double>::value) Rt = DevBuf(sizeof(T) * cols * cols, ctx->stream);
@@ -154,11 +189,12 @@ struct KsvdWork {
         gemm<float>(ctx, cols, cols, rows, 1.f, Y, rows, 1, Y, 1, rows, 0.f, Gf.as<float>(), 1, cols);
         copy2d_cast<float, double>(ctx, cols, cols, Gf.as<float>(), 1, cols, G.as<double>(), 1, cols);
       }
+      if (sharded) allreduce_sum(ctx, G.p, (size_t)(cols * cols), RNLA_F64);
       if (!cholesky_upper(ctx, cols, G.as<double>())) return false;
       if (!diag_ratio_ok(ctx, cols, G.as<double>(), std::is_same<T, double>::value ? 1e-5 : 1e-2)) return false;
       upper_inverse(ctx, cols, G.as<double>(), Rinv.as<double>());
       // sign rule folded into the last R^-1: no extra pass over Q
-      if (pass == 1) signed_ok = presign_upper_inverse<T>(ctx, cols, Y, rows, Rinv.as<double>());
+      if (pass == 1 && !sharded) signed_ok = presign_upper_inverse<T>(ctx, cols, Y, rows, Rinv.as<double>());
       if constexpr (std::is_same<T, double>::value) {
         gemm<double>(ctx, rows, cols, cols, 1.0, Y, 1, rows, Rinv.as<double>(), 1, cols, 0.0, tmp.as<double>(), 1,
                      rows);
@@ -168,7 +204,10 @@ struct KsvdWork {
       }
       RNLA_CUDA(cudaMemcpyAsync(Y, tmp.p, sizeof(T) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    if (!signed_ok) sign_fix(ctx, rows, cols, Y);
+    if (sharded)
+      fix_column_signs_sharded<T>(ctx, rows, cols, Y, 1, rows, nullptr, 0, 0, 0, false);
+    else if (!signed_ok)
+      sign_fix(ctx, rows, cols, Y);
     return true;
   }
 
@@ -206,6 +245,12 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   if (spec) local = *spec;
   else { local.kind = RNLA_SKETCH_GAUSSIAN; local.seed = seed; }
   local.s = s;
+  // Row-sharded A: U comes back as this rank's rows,
+  // sigma and V replicated.
+  const bool sharded = ctx->world > 1;
+  require(!sharded || local.kind == RNLA_SKETCH_GAUSSIAN,
+          "prototype_ksvd: row-sharded contexts support the Gaussian test matrix");
+  require(!sharded || m >= s, "prototype_ksvd: every row shard needs at least s rows");
   int passes = 0;
   // pass 1: Y = A S (m x s, column-major)
   DevBuf Y(sizeof(T) * m * s, ctx->stream);
@@ -221,23 +266,26 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
     if (st != RNLA_OK) throw InvalidArgument(rnla_last_error());
     require(cols == s, "prototype_ksvd: sketch returned a different width");
   }
+  const int dt = std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32;
   DevBuf Z(sizeof(T) * n * s, ctx->stream);
   for (int32_t it = 0; it < q; ++it) {
-    KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), m);
-    // Z = orth(A' Q): n x s
+    KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), sharded);
+    // Z = orth(A' Q): n x s (a sum over row shards)
     gemm<T>(ctx, n, s, m, T(1), Ap, A.cs, A.rs, Y.as<T>(), 1, m, T(0), Z.as<T>(), 1, n);
+    if (sharded) allreduce_sum(ctx, Z.p, (size_t)(n * s), dt);
     ++passes;
-    KsvdWork<T>::orth(ctx, n, s, Z.as<T>(), n);
+    KsvdWork<T>::orth(ctx, n, s, Z.as<T>(), false);
     // Y = A Z
     gemm<T>(ctx, m, s, n, T(1), Ap, A.rs, A.cs, Z.as<T>(), 1, n, T(0), Y.as<T>(), 1, m);
     ++passes;
   }
-  KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), m);  // Q = thin_qr(C).Q
+  KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), sharded);  // Q = thin_qr(C).Q
   // pass 2: B = Q' A (s x n), column-major
   // computed as B' = A' Q (the streaming orientation of the A' Q power step),
   // written transposed: element (i, j) of B' lands at B[j + i*s].
   DevBuf B(sizeof(T) * s * n, ctx->stream);
   gemm<T>(ctx, n, s, m, T(1), Ap, A.cs, A.rs, Y.as<T>(), 1, m, T(0), B.as<T>(), s, 1);
+  if (sharded) allreduce_sum(ctx, B.p, (size_t)(n * s), dt);
   ++passes;
   DevBuf B64;
   const double* Bp;
@@ -285,6 +333,7 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
                    1, rows);
       total += sum_squares_dev(ctx, R.as<double>(), rows * n);
     }
+    if (sharded) total = allreduce_scalar(ctx, total);
     *error_fro = std::sqrt(total);
   }
   uo.finish(ctx);

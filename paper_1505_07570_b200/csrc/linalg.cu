@@ -9,6 +9,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include "dist.h"
 #include "linalg.cuh"
 #include "util.cuh"
 
@@ -124,6 +125,80 @@ bool presign_upper_inverse(rnla_ctx* ctx, int64_t cols, const T* Y, int64_t y_cs
 }
 template bool presign_upper_inverse<double>(rnla_ctx*, int64_t, const double*, int64_t, double*);
 template bool presign_upper_inverse<float>(rnla_ctx*, int64_t, const float*, int64_t, double*);
+
+namespace {
+// sign[j] = sign of the first entry of column j with |m| > tol (0: none).
+template <class T>
+__global__ void lead_sign_kernel(int64_t rows, int64_t cols, const T* M, int64_t m_rs, int64_t m_cs, double tol,
+                                 double* sign) {
+  const int64_t j = blockIdx.x;
+  if (j >= cols) return;
+  __shared__ unsigned long long first;
+  if (threadIdx.x == 0) first = ~0ull;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x)
+    if (fabs((double)M[i * m_rs + j * m_cs]) > tol) {
+      atomicMin(&first, (unsigned long long)i);
+      break;
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) sign[j] = first == ~0ull ? 0.0 : (M[(int64_t)first * m_rs + j * m_cs] < T(0) ? -1.0 : 1.0);
+}
+
+__global__ void flip_paired_kernel(int64_t cols, const int* __restrict__ flip, double* P, int64_t p_rs, int64_t p_cs,
+                                   int64_t p_len, int pair_cols) {
+  const int64_t total = cols * p_len;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / p_len, i = e % p_len;
+    if (!flip[j]) continue;
+    double* q = pair_cols ? &P[i * p_rs + j * p_cs] : &P[j * p_rs + i * p_cs];
+    *q = -*q;
+  }
+}
+}  // namespace
+
+template <class T>
+void fix_column_signs_sharded(rnla_ctx* ctx, int64_t rows, int64_t cols, T* M, int64_t m_rs, int64_t m_cs, double* P,
+                              int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols) {
+  if (cols == 0) return;
+  const int W = std::max(1, ctx->world);
+  DevBuf sign(sizeof(double) * cols, ctx->stream), all(sizeof(double) * cols * W, ctx->stream);
+  lead_sign_kernel<T><<<(unsigned)cols, 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs, 1e-12, sign.as<double>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  allgather_blocks(ctx, sign.p, all.p, (size_t)cols, RNLA_F64);
+  std::vector<double> h((size_t)(cols * W));
+  RNLA_CUDA(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * cols * W, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<int> flip((size_t)cols, 0);
+  for (int64_t j = 0; j < cols; ++j)
+    for (int r = 0; r < W; ++r) {  // ranks hold consecutive row blocks: the first decisive rank wins
+      const double sgn = h[(size_t)(r * cols + j)];
+      if (sgn != 0.0) {
+        flip[(size_t)j] = sgn < 0.0;
+        break;
+      }
+    }
+  DevBuf fl(sizeof(int) * cols, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(fl.p, flip.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, ctx->stream));
+  if (rows > 0) {
+    flip_cols_kernel<T><<<grid_for(ctx, rows * cols, 256), 256, 0, ctx->stream>>>(rows, cols, M, m_rs, m_cs,
+                                                                                  fl.as<int>());
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+  if (P && p_len > 0) {
+    flip_paired_kernel<<<grid_for(ctx, cols * p_len, 256), 256, 0, ctx->stream>>>(cols, fl.as<int>(), P, p_rs, p_cs,
+                                                                                   p_len, pair_cols ? 1 : 0);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // `flip` host vector lifetime
+}
+template void fix_column_signs_sharded<double>(rnla_ctx*, int64_t, int64_t, double*, int64_t, int64_t, double*, int64_t,
+                                               int64_t, int64_t, bool);
+template void fix_column_signs_sharded<float>(rnla_ctx*, int64_t, int64_t, float*, int64_t, int64_t, double*, int64_t,
+                                              int64_t, int64_t, bool);
 
 void fix_column_signs_f32(rnla_ctx* ctx, int64_t rows, int64_t cols, float* M, int64_t m_rs, int64_t m_cs) {
   if (cols == 0) return;

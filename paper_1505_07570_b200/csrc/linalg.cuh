@@ -10,6 +10,12 @@ void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int6
                       int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols);
 
 void fix_column_signs_f32(rnla_ctx* ctx, int64_t rows, int64_t cols, float* M, int64_t m_rs, int64_t m_cs);
+// The same rule for a row-sharded M (this rank's consecutive row block): the
+// first entry over the global row order decides (one allgather of per-rank
+// lead signs); P (replicated) is flipped like fix_column_signs does.
+template <class T>
+void fix_column_signs_sharded(rnla_ctx* ctx, int64_t rows, int64_t cols, T* M, int64_t m_rs, int64_t m_cs, double* P,
+                              int64_t p_rs, int64_t p_cs, int64_t p_len, bool pair_cols);
 // Flip columns of the upper-triangular Rinv so that Y * Rinv satisfies the sign
 // rule on its first row (Y row 0 at Y[p * y_cs]); false when a sign is not
 // decidable from row 0 (then fix the product with fix_column_signs).

@@ -94,6 +94,7 @@ struct rnla_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaStream_t aux_stream = nullptr;  // concurrent compute (e.g. Gaussian stage under the count sketch)
   void* nccl = nullptr;      // ncclComm_t
+  rnla_group* group = nullptr;  // in-process host-staged group (dist.cpp), else NCCL
   void* cusolver = nullptr;  // cusolverDnHandle_t
   void* cublas = nullptr;    // cublasHandle_t
   int num_sms = 148;

@@ -1,0 +1,164 @@
+"""Row-sharded paths on one GPU: an in-process shard group
+(rnla_group) drives `world` contexts from `world` host threads. Collectives
+are staged through host memory, so no kernel waits on another rank's kernel;
+the sharded decomposition (hash by global row index, owner-reduced Gaussian
+chunks, allreduced Grams / A'Q / B', TSQR fallback, global sign rule) is the
+same code the NCCL contexts run. Each sharded result is checked against the
+single-context result and the oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1505_07570_b200 as rn
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def run_group(world, fn, timeout=300):
+    """fn(ctx, rank) in `world` threads; returns the per-rank results."""
+    group = rn.ShardGroup(world)
+    out, errs = [None] * world, []
+
+    def body(r):
+        ctx = None
+        try:
+            torch.cuda.set_device(0)
+            ctx = rn.Context(0, group=group, rank=r)
+            out[r] = fn(ctx, r)
+            ctx.synchronize()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            errs.append(e)
+        finally:
+            if ctx is not None:
+                ctx.close()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+    group.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def shards(n, world):
+    return [rn.shard_rows(n, world, r) for r in range(world)]
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_combined_sketch_rows(ctx, world):
+    rng = np.random.default_rng(world)
+    n, d = 20000, 33
+    a = rng.standard_normal((n, d))
+    b = rng.standard_normal(n)
+    spec = rn.SketchSpec.combined(512, rn.SketchSpec.gaussian(128, 7), 11)
+    ref = rn.sketch_rows(dev(a), spec, extra=dev(b), ctx=ctx).cpu().numpy()
+    sh = shards(n, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        return rn.sketch_rows(dev(a[lo:hi]), spec, extra=dev(b[lo:hi]), row_offset=lo, ctx=c).cpu().numpy()
+
+    res = run_group(world, fn)
+    for r in range(world):
+        assert np.array_equal(res[r], res[0])  # replicated result, identical bits
+    assert np.linalg.norm(res[0] - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_lsr_sketched(ctx, world):
+    rng = np.random.default_rng(10 + world)
+    n, d = 30000, 20
+    a = rng.standard_normal((n, d))
+    b = a @ rng.standard_normal(d) + 0.01 * rng.standard_normal(n)
+    spec = rn.SketchSpec.combined(1024, rn.SketchSpec.gaussian(256, 3), 5)
+    ref = rn.lsr_sketched(dev(a), dev(b), spec, ctx=ctx)
+    sh = shards(n, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        return rn.lsr_sketched(dev(a[lo:hi]), dev(b[lo:hi]), spec, ctx=c)
+
+    res = run_group(world, fn)
+    for s in res:
+        assert np.max(np.abs(s.x - ref.x)) <= 1e-10 * np.max(np.abs(ref.x))
+        assert abs(s.objective - ref.objective) <= 1e-10 * ref.objective
+
+
+def decaying(m, n, seed, decay=20.0, noise=1e-3):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((m, min(m, n))))
+    v, _ = np.linalg.qr(rng.standard_normal((n, min(m, n))))
+    sig = np.exp(-np.arange(1, min(m, n) + 1) / decay)
+    return (u * sig) @ v.T + noise * rng.standard_normal((m, n))
+
+
+@pytest.mark.parametrize("world,q", [(2, 0), (2, 2), (3, 1)])
+def test_sharded_prototype_ksvd_fp64(ctx, world, q):
+    m, n, k, s = 3000, 400, 10, 20
+    a = decaying(m, n, 7)
+    ref = rn.prototype_ksvd(dev(a), k, s, 77, power_iters=q, opts=rn.KsvdOptions(True), ctx=ctx)
+    uo, so, vo, _ = orc.prototype_ksvd(a, k, s, 77, q=q)
+    sh = shards(m, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        res = rn.prototype_ksvd(dev(a[lo:hi]), k, s, 77, power_iters=q, opts=rn.KsvdOptions(True), ctx=c)
+        return res.factors.U.cpu().numpy(), res.factors.singular_values, res.factors.V.cpu().numpy(), \
+            res.passes_over_a, res.error_fro
+
+    res = run_group(world, fn)
+    U = np.vstack([x[0] for x in res])
+    for x in res:
+        assert x[3] == 2 + 2 * q
+        assert np.array_equal(x[1], res[0][1]) and np.array_equal(x[2], res[0][2])
+        assert abs(x[4] - ref.error_fro) <= 1e-9 * ref.error_fro
+    sv = res[0][1]
+    assert np.max(np.abs(sv - so) / so) <= 1e-8
+    assert np.max(np.abs(sv - ref.factors.singular_values) / so) <= 1e-10
+    # signs follow the global first-row rule: the stacked U matches the unsharded U
+    Ur = ref.factors.U.cpu().numpy()
+    assert np.max(np.abs(U[:, :5] - Ur[:, :5])) <= 1e-8
+    assert np.max(np.abs(U[:, :5] - uo[:, :5])) <= 1e-6
+
+
+def test_sharded_prototype_ksvd_fp32(ctx):
+    m, n, k, s, world = 8192, 1024, 20, 40, 2
+    a = decaying(m, n, 9, decay=40.0, noise=1e-4).astype(np.float32)
+    _, so, _, _ = orc.prototype_ksvd(a.astype(np.float64), k, s, 5, q=2)
+    sh = shards(m, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        return rn.prototype_ksvd(dev(a[lo:hi]), k, s, 5, power_iters=2, ctx=c).factors.singular_values
+
+    res = run_group(world, fn)
+    assert np.max(np.abs(res[0] - so) / so) <= 1e-3
+
+
+def test_sharded_prototype_tsqr_fallback(ctx):
+    # exactly rank 5 < s: CholeskyQR breaks down, the sharded path falls back to TSQR
+    m, n, k, s, world = 2000, 300, 5, 16, 2
+    a = orc.gaussian_matrix(m, 5, 3) @ orc.gaussian_matrix(5, n, 4)
+    ref = rn.prototype_ksvd(a, k, s, 9, opts=rn.KsvdOptions(True), ctx=ctx)
+    sh = shards(m, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        res = rn.prototype_ksvd(dev(a[lo:hi]), k, s, 9, opts=rn.KsvdOptions(True), ctx=c)
+        return res.factors.U.cpu().numpy(), res.factors.singular_values, res.error_fro
+
+    res = run_group(world, fn)
+    U = np.vstack([x[0] for x in res])
+    assert np.max(np.abs(res[0][1] - ref.factors.singular_values) / ref.factors.singular_values) <= 1e-10
+    assert res[0][2] <= 1e-8 * np.linalg.norm(a)
+    assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-10
