@@ -15,40 +15,52 @@ namespace rnla {
 
 namespace {
 
-// Selected landmarks (src/spsd.cpp:189-191) and the kernel columns C = K[:, S]
-// for X (n x d): fp64 output when T = double, else fp32.
+// Selected landmarks (src/spsd.cpp:189-191) for the kernel columns C = K[:, S]
+// of X (this rank's n_local x d rows of the global n points; fp64 output
+// when T = double, else fp32). The landmark points are gathered by their
+// owners and replicated (an allreduce of the zero-padded s x d block).
 struct Landmarks {
-  std::vector<int64_t> sel;
-  DevBuf dsel, sq;  // device copy of sel, squared norms of all n points
+  std::vector<int64_t> sel;  // global indices, ascending
+  DevBuf dsel;               // local row of each landmark, -1 if another rank owns it
+  DevBuf sq;                 // squared norms of this rank's rows
+  DevMat Xs;                 // landmark points (s x d), replicated
+  DevBuf sqS;                // their squared norms (same FMA chain: bitwise equal to sq[sel])
+  int64_t r_off = 0;
 };
 
 template <class T>
-Landmarks landmarks(rnla_ctx* ctx, const DevMat& X, int64_t s, uint64_t seed) {
+Landmarks landmarks(rnla_ctx* ctx, const DevMat& X, int64_t s, uint64_t seed, int64_t n_global, int64_t r_off) {
   Landmarks L;
   const int64_t n = X.rows, d = X.cols;
-  L.sel = sample_without_replacement_host(derive_seed(seed, 1), n, s);
+  L.sel = sample_without_replacement_host(derive_seed(seed, 1), n_global, s);
+  L.r_off = r_off;
+  std::vector<int64_t> loc(L.sel);
+  for (auto& v : loc) v = (v >= r_off && v < r_off + n) ? v - r_off : -1;
   L.dsel = DevBuf(sizeof(int64_t) * s, ctx->stream);
-  RNLA_CUDA(cudaMemcpyAsync(L.dsel.p, L.sel.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
-  L.sq = DevBuf(sizeof(T) * n, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(L.dsel.p, loc.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+  L.sq = DevBuf(sizeof(T) * std::max<int64_t>(n, 1), ctx->stream);
   sq_norms<T>(ctx, n, d, X.as<T>(), X.rs, X.cs, nullptr, L.sq.as<T>());
+  L.Xs = alloc_dense(ctx, s, d, true, X.dtype);
+  gather_rows<T>(ctx, s, d, X.as<T>(), X.rs, X.cs, L.dsel.as<int64_t>(), L.Xs.as<T>(), L.Xs.rs, L.Xs.cs);
+  if (ctx->world > 1) allreduce_sum(ctx, L.Xs.p, (size_t)(s * d), X.dtype);
+  L.sqS = DevBuf(sizeof(T) * s, ctx->stream);
+  sq_norms<T>(ctx, s, d, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, nullptr, L.sqS.as<T>());
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // `loc` leaves scope
   return L;
 }
 
+// Rows [r0, r0 + rows) of this rank's block of C = K[:, S].
 template <class T>
 void kernel_columns(rnla_ctx* ctx, const DevMat& X, const Landmarks& L, int64_t r0, int64_t rows, double sigma,
-                    T* C, int64_t c_rs, int64_t c_cs, DevBuf& sqsel) {
+                    T* C, int64_t c_rs, int64_t c_cs) {
   const int64_t s = (int64_t)L.sel.size(), d = X.cols;
-  if (!sqsel.p) {
-    sqsel = DevBuf(sizeof(T) * s, ctx->stream);
-    gather_columns<T>(ctx, 1, s, L.sq.as<T>(), 1, 1, L.dsel.as<int64_t>(), nullptr, sqsel.as<T>(), 1, 1);
-  }
-  // diag_of[t] = sel[t] - r0 marks the landmark's own row inside this block.
+  // diag_of[t] = the landmark's own row inside this block (forced to exactly 1).
   DevBuf diag(sizeof(int64_t) * s, ctx->stream);
   std::vector<int64_t> h(L.sel);
-  for (auto& v : h) v -= r0;
+  for (auto& v : h) v -= L.r_off + r0;
   RNLA_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
-  rbf_block<T>(ctx, rows, s, d, X.as<T>() + r0 * X.rs, X.rs, X.cs, X.as<T>(), X.rs, X.cs, L.dsel.as<int64_t>(),
-               L.sq.as<T>() + r0, sqsel.as<T>(), sigma, diag.as<int64_t>(), C, c_rs, c_cs);
+  rbf_block<T>(ctx, rows, s, d, X.as<T>() + r0 * X.rs, X.rs, X.cs, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, nullptr,
+               L.sq.as<T>() + r0, L.sqS.as<T>(), sigma, diag.as<int64_t>(), C, c_rs, c_cs);
   RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // `h` leaves scope
 }
 
@@ -102,10 +114,11 @@ void nystrom_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uin
   const int64_t n = X.rows;
   const int64_t kk = target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
   require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
-  Landmarks L = landmarks<T>(ctx, X, s, seed);
+  require(ctx->world == 1, "nystrom: row-sharded contexts use nystrom_eig");
+  Landmarks L = landmarks<T>(ctx, X, s, seed, n, 0);
   // C = K[:, S] (n x s, col-major, compute dtype), W = rows S of C
-  DevBuf C(sizeof(T) * n * s, ctx->stream), sqsel;
-  kernel_columns<T>(ctx, X, L, 0, n, sigma, C.as<T>(), 1, n, sqsel);
+  DevBuf C(sizeof(T) * n * s, ctx->stream);
+  kernel_columns<T>(ctx, X, L, 0, n, sigma, C.as<T>(), 1, n);
   DevBuf W(sizeof(double) * s * s, ctx->stream);
   DevBuf W64;
   if constexpr (std::is_same<T, double>::value) {
@@ -150,16 +163,14 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   const int64_t r_off = global_row_offset(ctx, n_local, &n);
   const int64_t kk = target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
   require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
-  require(ctx->world == 1, "nystrom_eig: row-sharded contexts are not supported yet");
-  (void)r_off;
-  Landmarks L = landmarks<T>(ctx, X, s, seed);
-  const int64_t blk = std::min<int64_t>(n_local, 16384);
-  DevBuf Cb(sizeof(T) * blk * s, ctx->stream), sqsel;
+  Landmarks L = landmarks<T>(ctx, X, s, seed, n, r_off);
+  const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(n_local, 16384));
+  DevBuf Cb(sizeof(T) * blk * s, ctx->stream);
   DevBuf G(sizeof(double) * s * s, ctx->stream), W(sizeof(double) * s * s, ctx->stream);
   RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * s * s, ctx->stream));
   for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
     const int64_t rows = std::min(blk, n_local - r0);
-    kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows, sqsel);
+    kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows);
     if constexpr (std::is_same<T, double>::value)
       gemm<double>(ctx, s, s, rows, 1.0, Cb.as<double>(), rows, 1, Cb.as<double>(), 1, rows, 1.0, G.as<double>(), 1,
                    s);
@@ -172,18 +183,15 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
       gemm_f32_in_f64(ctx, s, s, rows, 1.0, Cb.as<float>(), rows, 1, Cb.as<float>(), 1, rows, 1.0, G.as<double>(), 1,
                       s);
   }
+  if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(s * s), RNLA_F64);  // C'C over row shards
   // W = K[S, S]: its rows are the landmark rows of C (recomputed directly).
   {
-    DevBuf Wt(sizeof(T) * s * s, ctx->stream), sqs2;
-    DevMat Xs = alloc_dense(ctx, s, X.cols, true, X.dtype);
-    gather_rows<T>(ctx, s, X.cols, X.as<T>(), X.rs, X.cs, L.dsel.as<int64_t>(), Xs.as<T>(), Xs.rs, Xs.cs);
-    DevBuf sqS(sizeof(T) * s, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
-    gather_columns<T>(ctx, 1, s, L.sq.as<T>(), 1, 1, L.dsel.as<int64_t>(), nullptr, sqS.as<T>(), 1, 1);
+    DevBuf Wt(sizeof(T) * s * s, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
     std::vector<int64_t> id((size_t)s);
     for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
     RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
-    rbf_block<T>(ctx, s, s, X.cols, Xs.as<T>(), Xs.rs, Xs.cs, Xs.as<T>(), Xs.rs, Xs.cs, nullptr, sqS.as<T>(),
-                 sqS.as<T>(), sigma, ident.as<int64_t>(), Wt.as<T>(), 1, s);
+    rbf_block<T>(ctx, s, s, X.cols, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, nullptr,
+                 L.sqS.as<T>(), L.sqS.as<T>(), sigma, ident.as<int64_t>(), Wt.as<T>(), 1, s);
     if constexpr (std::is_same<T, double>::value)
       RNLA_CUDA(cudaMemcpyAsync(W.p, Wt.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
     else
@@ -224,7 +232,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
     }
     for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
       const int64_t rows = std::min(blk, n_local - r0);
-      kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows, sqsel);
+      kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows);
       if constexpr (std::is_same<T, double>::value) {
         gemm<double>(ctx, rows, k, s, 1.0, Cb.as<double>(), 1, rows, P.as<double>(), 1, s, 0.0,
                      U64.as<double>() + r0, 1, n_local);
@@ -235,7 +243,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
         copy2d_cast<float, double>(ctx, rows, k, Ub.as<float>(), 1, rows, U64.as<double>() + r0, 1, n_local);
       }
     }
-    fix_column_signs(ctx, n_local, k, U64.as<double>(), 1, n_local, nullptr, 0, 0, 0, true);
+    fix_column_signs_sharded<double>(ctx, n_local, k, U64.as<double>(), 1, n_local, nullptr, 0, 0, 0, true);
     store_block(ctx, U64.as<double>(), n_local, k, n_local, uo);
     uo.finish(ctx);
   }

@@ -191,7 +191,8 @@ __global__ void gather_rows_kernel(int64_t cnt, int64_t cols, const T* __restric
   const int64_t total = cnt * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / cols, c = e % cols;
-    out[i * o_rs + c * o_cs] = A[idx[i] * a_rs + c * a_cs];
+    const int64_t r = idx[i];
+    out[i * o_rs + c * o_cs] = r >= 0 ? A[r * a_rs + c * a_cs] : T(0);
   }
 }
 __global__ void symmetrize_kernel(int64_t n, const double* __restrict__ W, double* __restrict__ out) {

@@ -27,7 +27,7 @@ void row_sqnorms(rnla_ctx* ctx, int64_t n, int64_t d, const T* M, int64_t rs, in
 }  // namespace rnla
 
 namespace rnla {
-// out(i, c) = A(idx[i], c) for i < cnt, c < cols.
+// out(i, c) = A(idx[i], c) for i < cnt, c < cols (0 where idx[i] < 0).
 template <class T>
 void gather_rows(rnla_ctx* ctx, int64_t cnt, int64_t cols, const T* A, int64_t a_rs, int64_t a_cs, const int64_t* idx,
                  T* out, int64_t o_rs, int64_t o_cs);

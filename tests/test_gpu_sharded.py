@@ -162,3 +162,44 @@ def test_sharded_prototype_tsqr_fallback(ctx):
     assert np.max(np.abs(res[0][1] - ref.factors.singular_values) / ref.factors.singular_values) <= 1e-10
     assert res[0][2] <= 1e-8 * np.linalg.norm(a)
     assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_nystrom_eig_fp64(ctx, world):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((3000, 8)) * 2
+    u_ref, lam_ref, sel_ref, kept_ref = rn.nystrom_eig(rn.KernelView(x, rn.KernelSpec(3.0)), 200, 9, 150, 12, ctx=ctx)
+    L, sel_o, _ = orc.nystrom(x, 3.0, 200, 9, 150)
+    _, lo = orc.approx_eig(L, 12)
+    sh = shards(x.shape[0], world)
+
+    def fn(c, r):
+        lo_, hi = sh[r]
+        return rn.nystrom_eig(rn.KernelView(dev(x[lo_:hi]), rn.KernelSpec(3.0)), 200, 9, 150, 12, ctx=c)
+
+    res = run_group(world, fn)
+    U = np.vstack([r_[0].cpu().numpy() for r_ in res])
+    for u_, lam, sel, kept in res:
+        assert np.array_equal(sel, sel_ref) and np.array_equal(sel, sel_o) and kept == kept_ref
+        assert np.array_equal(lam, res[0][1])
+    lam = res[0][1]
+    assert np.max(np.abs(lam - lam_ref) / lam_ref) <= 1e-10
+    assert np.max(np.abs(lam - lo) / lo) <= 1e-8
+    assert np.max(np.abs(U[:, :6] - u_ref[:, :6])) <= 1e-8
+
+
+def test_sharded_nystrom_eig_fp32(ctx):
+    rng = np.random.default_rng(5)
+    means = rng.standard_normal((4, 16)) * 3
+    x = (means[rng.integers(0, 4, 8192)] + rng.standard_normal((8192, 16))).astype(np.float32)
+    L, _, _ = orc.nystrom(x.astype(np.float64), 6.0, 256, 3, 128)
+    _, lo = orc.approx_eig(L, 16)
+    sh = shards(x.shape[0], 2)
+
+    def fn(c, r):
+        lo_, hi = sh[r]
+        return rn.nystrom_eig(rn.KernelView(dev(x[lo_:hi]), rn.KernelSpec(6.0)), 256, 3, 128, 16,
+                              want_vectors=False, ctx=c)[1]
+
+    res = run_group(2, fn)
+    assert np.max(np.abs(res[0] - lo) / lo) <= 1e-3
