@@ -665,16 +665,23 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
     check_mat(m, "leverage_sample_rows: m");
     require(scores != nullptr, "leverage_sample_rows: null scores");
     require(indices == nullptr || (p >= 1 && count_out), "sample_with_replacement: count < 1");
+    // Row-sharded M: scores are this rank's rows, the
+    // indices are global, drawn from the allgathered score vector (replicated).
     const int64_t n = m->rows, d = m->cols;
-    require(n >= d && d >= 1, "thin_qr: rows < cols");
+    int64_t n_total = n;
+    const int64_t r_off = global_row_offset(ctx, n, &n_total);
+    require(n_total >= d && d >= 1, "thin_qr: rows < cols");
     DevMat M = to_device(ctx, m);
     DevBuf G(sizeof(double) * d * d, ctx->stream), Rinv(sizeof(double) * d * d, ctx->stream);
-    if (M.dtype == RNLA_F64)
+    if (n == 0)
+      RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * d * d, ctx->stream));
+    else if (M.dtype == RNLA_F64)
       gemm<double>(ctx, d, d, n, 1.0, M.as<double>(), M.cs, M.rs, M.as<double>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
                    d);
     else
       gemm_f32_f64acc(ctx, d, d, n, 1.0, M.as<float>(), M.cs, M.rs, M.as<float>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
                       d);
+    if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(d * d), RNLA_F64);
     if (!cholesky_upper(ctx, d, G.as<double>()))
       throw NumericError("leverage_sample_rows: M'M is not positive definite (rank-deficient M)");
     upper_inverse(ctx, d, G.as<double>(), Rinv.as<double>());
@@ -698,10 +705,24 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
         row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
       }
     }
-    RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (n > 0) RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
     if (indices) {
-      std::vector<int64_t> draws = sample_with_replacement_host(seed, scores, n, p);
+      std::vector<double> all_scores;
+      const double* w = scores;
+      if (ctx->world > 1) {
+        DevBuf g(sizeof(double) * n_total, ctx->stream);
+        RNLA_CUDA(cudaMemsetAsync(g.p, 0, sizeof(double) * n_total, ctx->stream));
+        if (n > 0)
+          RNLA_CUDA(cudaMemcpyAsync(g.as<double>() + r_off, sc.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        allreduce_sum(ctx, g.p, (size_t)n_total, RNLA_F64);
+        all_scores.resize((size_t)n_total);
+        RNLA_CUDA(cudaMemcpyAsync(all_scores.data(), g.p, sizeof(double) * n_total, cudaMemcpyDeviceToHost, ctx->stream));
+        RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+        w = all_scores.data();
+      }
+      std::vector<int64_t> draws = sample_with_replacement_host(seed, w, n_total, p);
       std::sort(draws.begin(), draws.end());
       draws.erase(std::unique(draws.begin(), draws.end()), draws.end());
       std::copy(draws.begin(), draws.end(), indices);

@@ -217,8 +217,16 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
     dense_stage<T>(ctx, spec->stage2_kind, mp, Lo, s, Lo, spec->stage2_s, spec->stage2_seed, out, o_rs, o_cs);
     return;
   }
+  if (kind == RNLA_SKETCH_SRHT && sharded) {
+    require(extra == nullptr, "sketch_rows: an appended column is supported for count and combined sketches");
+    int64_t n_total = n;
+    const int64_t off = global_row_offset(ctx, n, &n_total);
+    require(off == row_offset, "sketch_rows: row_offset differs from the shard layout (rnla_shard_rows order)");
+    srht_rows_sharded<T>(ctx, M, ld, n, L, off, n_total, spec->s, spec->seed, out, o_rs, o_cs);
+    return;
+  }
   require(!sharded && row_offset == 0,
-          "sketch_rows: row sharding is supported for count and combined (count-first) sketches");
+          "sketch_rows: row sharding is supported for count, combined (count-first) and SRHT sketches");
   require(extra == nullptr, "sketch_rows: an appended column is supported for count and combined sketches");
   if (kind == RNLA_SKETCH_GAUSSIAN || kind == RNLA_SKETCH_SRHT) {
     dense_stage<T>(ctx, kind, M, ld, n, L, spec->s, spec->seed, out, o_rs, o_cs);

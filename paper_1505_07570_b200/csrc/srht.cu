@@ -16,8 +16,10 @@
 // Stages run in the reference order with the same x+y / x-y operations, so
 // the fp64 result is bit-identical to the reference's loop. Strips are
 // processed in groups small enough for T to stay resident in the 126 MB L2.
+#include "dist.h"
 #include "rnla_internal.h"
 #include "srht.h"
+#include "util.cuh"
 
 namespace rnla {
 
@@ -278,31 +280,51 @@ bool srht_fast(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int
 SrhtPlan::SrhtPlan(rnla_ctx* ctx, int64_t n_, int64_t s_, uint64_t seed_) : n(n_), s(s_), seed(seed_) {
   big_n = next_pow2(n);
   require(s >= 1 && s <= big_n, "srht_sketch: s > padded dimension");
+  std::vector<int8_t> sg((size_t)std::max<int64_t>(n, 1));
+  std::vector<int64_t> idx((size_t)s);
+  srht_operator_host(seed, n, s, sg.data(), idx.data());
+  host_idx = idx;
+  build(ctx, sg.data(), idx.data());
+}
+
+SrhtPlan::SrhtPlan(rnla_ctx* ctx, const int8_t* block_signs, int64_t present, int64_t block, const int64_t* idx,
+                   int64_t s_, int64_t block_off_)
+    : n(present), s(s_), big_n(block), block_off(block_off_) {
+  std::vector<int64_t> loc((size_t)s);
+  std::vector<double> sgn((size_t)s);
+  for (int64_t t = 0; t < s; ++t) {
+    loc[(size_t)t] = idx[t] & (block - 1);
+    sgn[(size_t)t] = (__builtin_popcountll((unsigned long long)(block_off & idx[t])) & 1) ? -1.0 : 1.0;
+  }
+  host_idx = loc;
+  out_sign = DevBuf(sizeof(double) * s, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(out_sign.p, sgn.data(), sizeof(double) * s, cudaMemcpyHostToDevice, ctx->stream));
+  build(ctx, block_signs, loc.data());
+}
+
+void SrhtPlan::build(rnla_ctx* ctx, const int8_t* sg, const int64_t* idx) {
   q = 0;
   while (((int64_t)1 << q) < big_n) ++q;
   require(q <= 22, "srht_sketch: padded dimension above 2^22 is not supported");
   qlo = (q + 1) / 2;
   qhi = q - qlo;
-  std::vector<int8_t> sg((size_t)std::max<int64_t>(n, 1));
-  std::vector<int64_t> idx((size_t)s);
-  srht_operator_host(seed, n, s, sg.data(), idx.data());
-  host_idx = idx;
   const int64_t R = (int64_t)1 << qlo;
   std::vector<int32_t> off((size_t)R + 1, 0), gt((size_t)s), gh((size_t)s);
-  for (int64_t t = 0; t < s; ++t) off[(size_t)(idx[(size_t)t] & (R - 1)) + 1]++;
+  for (int64_t t = 0; t < s; ++t) off[(size_t)(idx[t] & (R - 1)) + 1]++;
   for (int64_t i = 0; i < R; ++i) off[(size_t)i + 1] += off[(size_t)i];
   std::vector<int32_t> cur(off.begin(), off.end() - 1);
   for (int64_t t = 0; t < s; ++t) {
-    const int64_t lo = idx[(size_t)t] & (R - 1);
+    const int64_t lo = idx[t] & (R - 1);
     const int32_t g = cur[(size_t)lo]++;
     gt[(size_t)g] = (int32_t)t;
-    gh[(size_t)g] = (int32_t)(idx[(size_t)t] >> qlo);
+    gh[(size_t)g] = (int32_t)(idx[t] >> qlo);
   }
-  signs = DevBuf(sg.size(), ctx->stream);
+  const size_t ns = (size_t)std::max<int64_t>(n, 1);
+  signs = DevBuf(ns, ctx->stream);
   grp_off = DevBuf(sizeof(int32_t) * off.size(), ctx->stream);
   grp_t = DevBuf(sizeof(int32_t) * gt.size(), ctx->stream);
   grp_hi = DevBuf(sizeof(int32_t) * gh.size(), ctx->stream);
-  RNLA_CUDA(cudaMemcpyAsync(signs.p, sg.data(), sg.size(), cudaMemcpyHostToDevice, ctx->stream));
+  if (n > 0) RNLA_CUDA(cudaMemcpyAsync(signs.p, sg, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
   RNLA_CUDA(cudaMemcpyAsync(grp_off.p, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice, ctx->stream));
   RNLA_CUDA(cudaMemcpyAsync(grp_t.p, gt.data(), sizeof(int32_t) * gt.size(), cudaMemcpyHostToDevice, ctx->stream));
   RNLA_CUDA(cudaMemcpyAsync(grp_hi.p, gh.data(), sizeof(int32_t) * gh.size(), cudaMemcpyHostToDevice, ctx->stream));
@@ -350,5 +372,56 @@ template void srht_segments<double>(rnla_ctx*, const SrhtPlan&, const double*, i
                                     int64_t);
 template void srht_segments<float>(rnla_ctx*, const SrhtPlan&, const float*, int64_t, int64_t, float*, int64_t,
                                    int64_t);
+
+namespace {
+template <class T>
+__global__ void signed_accumulate_kernel(int64_t s, int64_t L, const T* __restrict__ tmp,
+                                         const double* __restrict__ sign, T* __restrict__ acc) {
+  const int64_t total = s * L;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    acc[e] += (T)sign[e / L] * tmp[e];
+}
+}  // namespace
+
+// Row-sharded SRHT. With j = o + jl for a block of
+// 2^b rows at an offset o that is a multiple of 2^b, and any t:
+//   (-1)^popcount(j & t) = (-1)^popcount(o & t) * (-1)^popcount(jl & (t mod 2^b)),
+// so this rank's rows, cut into aligned power-of-two blocks, each contribute
+// sign_t * [H_{2^b} (signs . x)]_{t mod 2^b} to every sampled output t. The
+// partial outputs are summed over ranks by one allreduce (s x L).
+template <class T>
+void srht_rows_sharded(rnla_ctx* ctx, const T* in, int64_t ld, int64_t n_local, int64_t L, int64_t row_off,
+                       int64_t n_total, int64_t s, uint64_t seed, T* out, int64_t out_rs, int64_t out_cs) {
+  const int64_t big_n = next_pow2(n_total);
+  require(s >= 1 && s <= big_n, "srht_sketch: s > padded dimension");
+  std::vector<int8_t> sg((size_t)std::max<int64_t>(n_total, 1));
+  std::vector<int64_t> idx((size_t)s);
+  srht_operator_host(seed, n_total, s, sg.data(), idx.data());
+  DevBuf acc(sizeof(T) * s * std::max<int64_t>(L, 1), ctx->stream), tmp(sizeof(T) * s * std::max<int64_t>(L, 1),
+                                                                          ctx->stream);
+  RNLA_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(T) * s * L, ctx->stream));
+  const int64_t end = row_off + n_local;
+  const int64_t limit = end == n_total ? big_n : end;  // the last rank owns the zero padding
+  for (int64_t cur = row_off; cur < end;) {
+    int64_t b = cur == 0 ? big_n : (cur & -cur);
+    while (cur + b > limit) b >>= 1;
+    const int64_t present = std::min(b, end - cur);
+    SrhtPlan plan(ctx, sg.data() + cur, present, b, idx.data(), s, cur);
+    srht_segments<T>(ctx, plan, in + (cur - row_off) * ld, ld, L, tmp.as<T>(), L, 1);
+    signed_accumulate_kernel<T><<<grid_for(ctx, s * L, 256), 256, 0, ctx->stream>>>(s, L, tmp.as<T>(),
+                                                                                     plan.out_sign.as<double>(),
+                                                                                     acc.as<T>());
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+    cur += b;
+  }
+  allreduce_sum(ctx, acc.p, (size_t)(s * L), std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32);
+  copy2d<T>(ctx, s, L, acc.as<T>(), L, 1, out, out_rs, out_cs);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+template void srht_rows_sharded<double>(rnla_ctx*, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                        uint64_t, double*, int64_t, int64_t);
+template void srht_rows_sharded<float>(rnla_ctx*, const float*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                       uint64_t, float*, int64_t, int64_t);
 
 }  // namespace rnla

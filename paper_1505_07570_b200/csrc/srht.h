@@ -11,7 +11,16 @@ struct SrhtPlan {
   std::vector<int64_t> host_idx;   // sorted sampled indices (src/sketch.cpp:65)
   DevBuf signs;                    // int8[n]
   DevBuf grp_off, grp_t, grp_hi;   // samples grouped by idx & (2^qlo - 1)
+  int64_t block_off = 0;           // block plans: global index of the block's first row
+  DevBuf out_sign;                 // block plans: (-1)^popcount(block_off & idx_t), fp64[s]
   SrhtPlan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed);
+  // Plan of one aligned block (2^b rows at block_off, `present` of them real)
+  // of a global operator whose sampled indices are idx[0..s).
+  SrhtPlan(rnla_ctx* ctx, const int8_t* block_signs, int64_t present, int64_t block, const int64_t* idx, int64_t s,
+           int64_t block_off);
+
+ private:
+  void build(rnla_ctx* ctx, const int8_t* signs, const int64_t* idx);
 };
 
 // TMA-fed fp32 path (srht_tma.cu); false when the shape/alignment does not apply.
@@ -22,5 +31,11 @@ bool srht_tma_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t 
 template <class T>
 void srht_segments(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, int64_t L, T* out, int64_t out_rs,
                    int64_t out_cs);
+
+// Row-sharded S^T M: this rank's n_local rows start at global row row_off of
+// n_total; the replicated s x L result is written to out.
+template <class T>
+void srht_rows_sharded(rnla_ctx* ctx, const T* in, int64_t ld, int64_t n_local, int64_t L, int64_t row_off,
+                       int64_t n_total, int64_t s, uint64_t seed, T* out, int64_t out_rs, int64_t out_cs);
 
 }  // namespace rnla

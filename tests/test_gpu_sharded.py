@@ -203,3 +203,51 @@ def test_sharded_nystrom_eig_fp32(ctx):
 
     res = run_group(2, fn)
     assert np.max(np.abs(res[0] - lo) / lo) <= 1e-3
+
+
+@pytest.mark.parametrize("world,n,dtype", [(2, 40000, np.float64), (3, 40000, np.float64), (4, 1 << 16, np.float64),
+                                           (2, 1 << 18, np.float32), (3, 300001, np.float32)])
+def test_sharded_srht_rows(ctx, world, n, dtype):
+    rng = np.random.default_rng(n % 1000 + world)
+    d, s = 24, 512
+    m = rng.standard_normal((n, d)).astype(dtype)
+    spec = rn.SketchSpec.srht(s, 33)
+    ref = rn.sketch_rows(dev(m), spec, ctx=ctx).cpu().numpy()
+    sh = shards(n, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        return rn.sketch_rows(dev(m[lo:hi]), spec, row_offset=lo, ctx=c).cpu().numpy()
+
+    res = run_group(world, fn)
+    for x in res:
+        assert np.array_equal(x, res[0])
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    assert np.linalg.norm(res[0] - ref) <= tol * np.linalg.norm(ref)
+    if n <= 40000:
+        o = orc.srht_rows(m.astype(np.float64), s, 33)
+        assert np.linalg.norm(res[0] - o) <= 1e-12 * np.linalg.norm(o)
+
+
+@pytest.mark.parametrize("world,dtype", [(2, np.float64), (3, np.float32)])
+def test_sharded_leverage_sample_rows(ctx, world, dtype):
+    rng = np.random.default_rng(21)
+    n, d, p = 50000, 24, 3000
+    m = rng.standard_t(3, size=(n, d)).astype(dtype)
+    sc_ref, idx_ref = rn.leverage_sample_rows(dev(m), p, 17, ctx=ctx)
+    sh = shards(n, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        return rn.leverage_sample_rows(dev(m[lo:hi]), p, 17, ctx=c)
+
+    res = run_group(world, fn)
+    scores = np.concatenate([x[0] for x in res])
+    for x in res:
+        assert np.array_equal(x[1], res[0][1])  # replicated global indices
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    assert np.max(np.abs(scores - sc_ref) / sc_ref) <= tol
+    # the draw is the reference sampler over the gathered scores, bit-exact
+    draws = np.unique(orc.sample_with_replacement(scores, p, 17))
+    assert np.array_equal(res[0][1], draws)
+    assert abs(scores.sum() - d) <= 1e-6 * d
