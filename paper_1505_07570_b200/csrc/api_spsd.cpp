@@ -208,18 +208,34 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   gemm<double>(ctx, s, kp, s, 1.0, G.as<double>(), 1, s, Tm.as<double>(), 1, s, 0.0, GT.as<double>(), 1, s);
   gemm<double>(ctx, kp, kp, s, 1.0, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, 0.0, M.as<double>(), 1, kp);
   symmetrize(ctx, kp, M.as<double>(), Ms.as<double>());
-  eig_sym(ctx, kp, Ms.as<double>(), ev.as<double>());
-  std::vector<double> h((size_t)kp);
-  RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * kp, cudaMemcpyDeviceToHost, ctx->stream));
-  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int64_t t = 0; t < k; ++t) lam_out[t] = h[(size_t)(kp - 1 - t)];
+  // Only the top k eigenpairs are needed: syevdx on an index range when k is
+  // well below kp (most of the back-transformation is skipped), else syevd.
+  std::vector<double> top((size_t)k);
+  const double* vtop = nullptr;  // eigenvector of the largest eigenvalue; the next ones at stride -kp
+  if (2 * k <= kp && !std::getenv("RNLA_EIG_FULL")) {
+    const int64_t found = eig_sym_top(ctx, kp, Ms.as<double>(), k, ev.as<double>());
+    if (found != k) throw NumericError("approx_eig: partial eigensolver returned fewer pairs");
+    std::vector<double> h((size_t)k);
+    RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < k; ++t) top[(size_t)t] = h[(size_t)(k - 1 - t)];
+    vtop = Ms.as<double>() + (k - 1) * kp;
+  } else {
+    eig_sym(ctx, kp, Ms.as<double>(), ev.as<double>());
+    std::vector<double> h((size_t)kp);
+    RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * kp, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < k; ++t) top[(size_t)t] = h[(size_t)(kp - 1 - t)];
+    vtop = Ms.as<double>() + (kp - 1) * kp;
+  }
+  for (int64_t t = 0; t < k; ++t) lam_out[t] = top[(size_t)t];
   if (u_out) {
     // P = T V_k diag(1/sigma) (s x k), U = C P, sign-fixed like condensed_svd's U.
     DevBuf Vk(sizeof(double) * kp * k, ctx->stream), P(sizeof(double) * s * k, ctx->stream),
         isg(sizeof(double) * k, ctx->stream), Vs(sizeof(double) * kp * k, ctx->stream);
-    copy2d<double>(ctx, kp, k, Ms.as<double>() + (kp - 1) * kp, 1, -kp, Vk.as<double>(), 1, kp);
+    copy2d<double>(ctx, kp, k, vtop, 1, -kp, Vk.as<double>(), 1, kp);
     std::vector<double> inv((size_t)k);
-    for (int64_t t = 0; t < k; ++t) inv[(size_t)t] = 1.0 / std::sqrt(h[(size_t)(kp - 1 - t)]);
+    for (int64_t t = 0; t < k; ++t) inv[(size_t)t] = 1.0 / std::sqrt(top[(size_t)t]);
     RNLA_CUDA(cudaMemcpyAsync(isg.p, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
     scale_cols_dev(ctx, kp, k, Vk.as<double>(), isg.as<double>(), Vs.as<double>());
     gemm<double>(ctx, s, k, kp, 1.0, Tm.as<double>(), 1, s, Vs.as<double>(), 1, kp, 0.0, P.as<double>(), 1, s);

@@ -326,4 +326,22 @@ void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W) {
   check_info(ctx, info, "eig");
 }
 
+int64_t eig_sym_top(rnla_ctx* ctx, int64_t n, double* A, int64_t k, double* W) {
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0, found = 0;
+  DevBuf info(sizeof(int), ctx->stream);
+  const int il = (int)(n - k + 1), iu = (int)n;
+  cusolver_check(cusolverDnDsyevdx_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                              CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, 0.0, 0.0, il, iu, &found, W,
+                                              &lwork),
+                 "syevdx_bufferSize");
+  DevBuf work(sizeof(double) * lwork, ctx->stream);
+  cusolver_check(cusolverDnDsyevdx(h, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER, (int)n,
+                                   A, (int)n, 0.0, 0.0, il, iu, &found, W, work.as<double>(), lwork, info.as<int>()),
+                 "syevdx");
+  note_launch(ctx);
+  check_info(ctx, info, "eig");
+  return found;
+}
+
 }  // namespace rnla

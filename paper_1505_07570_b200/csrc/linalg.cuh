@@ -39,5 +39,8 @@ void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv);
 
 // Symmetric eigen-decomposition of column-major A (n x n): A <- eigenvectors, W ascending.
 void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W);
+// The k largest eigenpairs only (syevdx, index range): W[0..k) ascending, their
+// eigenvectors in the first k columns of A. Returns the number found.
+int64_t eig_sym_top(rnla_ctx* ctx, int64_t n, double* A, int64_t k, double* W);
 
 }  // namespace rnla

@@ -240,7 +240,8 @@ void srht_fast_w(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld, i
   // a strip = the column tiles that together cover whole 128-B lines
   // (launched adjacently), sized to ~128 MB of scratch so it mostly stays in L2
   const int64_t line_tiles = std::max<int64_t>(1, 128 / (W * (int64_t)sizeof(T)));
-  int64_t tiles_per_strip = std::max<int64_t>(line_tiles, ((int64_t)128 << 20) / tile_bytes / line_tiles * line_tiles);
+  int64_t tiles_per_strip =
+      std::max<int64_t>(line_tiles, (srht_strip_mb() << 20) / tile_bytes / line_tiles * line_tiles);
   const int64_t total_tiles = (L + W - 1) / W;
   tiles_per_strip = std::min(tiles_per_strip, total_tiles);
   DevBuf scratch(sizeof(T) * (size_t)(big_n * W * tiles_per_strip), ctx->stream);

@@ -23,6 +23,12 @@ struct SrhtPlan {
   void build(rnla_ctx* ctx, const int8_t* signs, const int64_t* idx);
 };
 
+// Scratch budget per launch pair of the two-pass transform (RNLA_SRHT_STRIP_MB, default 1024).
+inline int64_t srht_strip_mb() {
+  static const int64_t mb = std::getenv("RNLA_SRHT_STRIP_MB") ? std::max<long long>(1, std::atoll(std::getenv("RNLA_SRHT_STRIP_MB"))) : 1024;
+  return mb;
+}
+
 // TMA-fed fp32 path (srht_tma.cu); false when the shape/alignment does not apply.
 bool srht_tma_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
                   int64_t out_rs, int64_t out_cs);

@@ -43,24 +43,39 @@ __device__ __forceinline__ void mbar_wait0(uint32_t bar) {
       "@!p bra W_%=;\n\t}\n" ::"r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+// L2 policies: the input and the last read of the scratch are streamed
+// (evict_first); the scratch written by the low pass is kept (evict_last) so
+// the high pass finds it in L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
+                                            uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+      "[%4], %5;\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint32_t bar) {
+                                            uint32_t bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
-          "r"(dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
-               "r"(c1), "r"(src)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
+                   map),
+               "r"(c0), "r"(c1), "r"(src), "l"(pol)
                : "memory");
 }
 
@@ -92,12 +107,13 @@ __global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_
   __syncthreads();
   if (tid == 0) {
     mbar_expect(su32(&bar), R * TW * 4);
+    const uint64_t pol = policy_evict_first();
     for (int b = 0; b < R / 256; ++b) {
       const uint32_t dst = su32(sm + b * 256 * TW);
       if (HI)  // scratch viewed as [jh][il][TW] per strip: rows jh = b*256.. of this il
-        tma_load_3d(dst, &src_map, 0, bx, tile * (int)(big_n >> qlo) + b * 256, su32(&bar));
+        tma_load_3d(dst, &src_map, 0, bx, tile * (int)(big_n >> qlo) + b * 256, su32(&bar), pol);
       else  // input A (row-major n x L): columns c0 + tile*16.., rows bx*R + b*256..
-        tma_load_2d(dst, &src_map, (int)(c0 + tile * TW), bx * R + b * 256, su32(&bar));
+        tma_load_2d(dst, &src_map, (int)(c0 + tile * TW), bx * R + b * 256, su32(&bar), pol);
     }
   }
   mbar_wait0(su32(&bar));
@@ -160,8 +176,9 @@ __global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     if (tid == 0) {
+      const uint64_t pol = policy_evict_last();
       for (int b = 0; b < R / 256; ++b)
-        tma_store_2d(&dst_map, 0, (int)(tile * big_n + rbase + b * 256), su32(sm + b * 256 * TW));
+        tma_store_2d(&dst_map, 0, (int)(tile * big_n + rbase + b * 256), su32(sm + b * 256 * TW), pol);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
@@ -225,8 +242,12 @@ bool srht_tma_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t 
   if ((reinterpret_cast<uintptr_t>(in) & 15) || ((ld * 4) % 16) || plan.n > (int64_t)INT32_MAX) return false;
   const int64_t big_n = plan.big_n;
   const int64_t total_tiles = (L + TW - 1) / TW;
-  // strip of tile pairs (whole 128-B lines), scratch ~128 MB
-  int64_t tps = std::max<int64_t>(2, (((int64_t)128 << 20) / (big_n * TW * 4)) / 2 * 2);
+  // strip of column tiles per launch pair. Measured on cfg2 (2^20 x 1024):
+  // 64 MB (L2-sized) 3.82 ms, 128 MB 3.07, 256 MB 2.80, 1 GB 2.58, 4 GB 2.56 --
+  // wide launches (no wave tails) beat L2 residency of the scratch.
+  const int64_t strip_mb = srht_strip_mb();
+  int64_t tps = std::max<int64_t>(1, (strip_mb << 20) / (big_n * TW * 4));
+  if (tps > 1) tps = tps / 2 * 2;  // whole 128-B lines per strip
   tps = std::min(tps, total_tiles);
   DevBuf scratch(sizeof(float) * (size_t)(big_n * TW * tps), ctx->stream);
   // input map: dims {L, n} (cols inner), row stride ld*4 bytes, box {16, 256}
