@@ -220,6 +220,15 @@ rnla_status rnla_faster_ksvd(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_
  * ran. a is n x d, b is n x 1. */
 rnla_status rnla_lsr_sketched(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b, const rnla_sketch_spec* spec,
                               double* x, double* objective, int32_t* flagged);
+/* lsr_preconditioned, regression.hpp:44-56 with PreconditionedOptions
+ * {sketch_size (0: min(d^2, 20d) capped at n), use_cg, sketch_kind (COUNT,
+ * GAUSSIAN or SRHT)} (src/regression.cpp:94-198). x[d], *iterations; the
+ * objective |Ax - b|^2 and kappa(A R_Y^-1) are skipped when their pointers
+ * are NULL. Each iteration is one fused pass over A: A'(b - A T z). d <= 1024.
+ * RNLA_ENUMERIC when the sketched matrix is singular twice. */
+rnla_status rnla_lsr_preconditioned(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b, double eps, uint64_t seed,
+                                    int64_t sketch_size, int32_t use_cg, int32_t sketch_kind, double* x,
+                                    double* objective, int32_t* iterations, double* kappa_estimate);
 
 /* ---- SPSD / kernels (include/randnla/spsd.hpp) -------------------------- */
 /* rbf_kernel, spsd.hpp:19-20 (src/spsd.cpp:33-47). Rows are points. */

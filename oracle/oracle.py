@@ -297,6 +297,75 @@ def numerical_rank(m: np.ndarray, thresh: float = 1e-10) -> int:
     return int(np.sum(sv > thresh * sv[0])) if sv.size and sv[0] > 0 else 0
 
 
+def lsr_preconditioned(a: np.ndarray, b: np.ndarray, eps: float, seed: int, sketch_size: int = 0,
+                       use_cg: bool = False, kind: str = "count"):
+    """src/regression.cpp:94-198 (sketch-and-precondition; CountSketch by default).
+    Returns (x, objective, iterations, kappa_estimate)."""
+    import scipy.linalg as sla
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    n, d = a.shape
+    if n < d:
+        raise ValueError("lsr_preconditioned: n < d")
+    if not (0.0 < eps < 1.0):
+        raise ValueError("lsr_preconditioned: eps out of (0,1)")
+    s = sketch_size or min(d * d, 20 * d)
+    s = min(s, n)
+    if s < d:
+        raise ValueError("lsr_preconditioned: sketch size < d")
+    stacked = np.hstack([a, b[:, None]])
+    draw = seed
+    for attempt in range(2):
+        if kind == "count":
+            sk = count_sketch_rows(stacked, s, draw)
+        elif kind == "gaussian":
+            sk = gaussian_sketch(stacked.T, s, draw).T
+        else:
+            sk = srht_rows(stacked, s, draw)
+        q, r = thin_qr(sk[:, :d])
+        dg = np.abs(np.diag(r))
+        if dg.max() > 0 and dg.min() > 1e-12 * dg.max():
+            break
+        if attempt >= 1:
+            raise RuntimeError("lsr_preconditioned: sketched matrix singular")
+        draw = derive_seed(seed, 0x5E5A)
+    sb = sk[:, d]
+    t = lambda v: sla.solve_triangular(r, v, lower=False)  # noqa: E731
+    tt = lambda v: sla.solve_triangular(r, v, lower=False, trans="T")  # noqa: E731
+    z = q.T @ sb
+    budget = int(math.ceil(10.0 * math.log10(1.0 / eps)))
+    grad_tol = max(1e-15 * np.linalg.norm(tt(a.T @ b)), 1e-300)
+    it = 0
+    if not use_cg:
+        prev = math.inf
+        while it < budget:
+            grad = tt(a.T @ (b - a @ t(z)))
+            z = z + grad
+            gn = np.linalg.norm(grad)
+            if gn <= grad_tol or gn >= 0.9 * prev:
+                it += 1
+                break
+            prev = gn
+            it += 1
+    else:
+        rr = tt(a.T @ (b - a @ t(z)))
+        p = rr.copy()
+        rs = rr @ rr
+        while it < budget and math.sqrt(rs) > grad_tol:
+            ap = tt(a.T @ (a @ t(p)))
+            alpha = rs / (p @ ap)
+            z = z + alpha * p
+            rr = rr - alpha * ap
+            rs_new = rr @ rr
+            p = rr + (rs_new / rs) * p
+            rs = rs_new
+            it += 1
+    x = t(z)
+    res = a @ x - b
+    sv = np.linalg.svd(a @ sla.solve_triangular(r, np.eye(d), lower=False), compute_uv=False)
+    return x, float(res @ res), it, float(sv[0] / sv[-1])
+
+
 def lsr_sketched(a: np.ndarray, b: np.ndarray, sk: np.ndarray):
     """Solve with a given sketch sk = S^T [A, b] (src/regression.cpp:80-91)."""
     d = a.shape[1]

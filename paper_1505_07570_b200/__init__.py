@@ -31,7 +31,7 @@ __all__ = [
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
     "count_sketch", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
     "leverage_sample_columns", "leverage_sample_rows", "thin_qr", "condensed_svd", "truncated_svd",
-    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig",
+    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig",
     "shard_rows",
 ]
 
@@ -607,6 +607,32 @@ def lsr_sketched(a, b, spec: SketchSpec, ctx: Optional[Context] = None) -> LsrSo
     _check(_abi.lib().rnla_lsr_sketched(_ctx(ctx).handle, C.byref(am), C.byref(bm), C.byref(cs),
                                         x.ctypes.data_as(_abi._F64P), C.byref(obj), C.byref(flagged)))
     return LsrSolution(x=x, objective=float(obj.value), flagged=bool(flagged.value))
+
+
+@dataclasses.dataclass(frozen=True)
+class PreconditionedOptions:
+    """include/randnla/regression.hpp:37-41."""
+    sketch_size: int = 0  # 0: min(d^2, 20 d) capped at n
+    use_cg: bool = False  # default: gradient descent with unit step
+    sketch_kind: SketchKind = SketchKind.kCountSketch
+
+
+def lsr_preconditioned(a, b, eps: float, seed: int, opts: PreconditionedOptions = PreconditionedOptions(),
+                       want_kappa: bool = True, ctx: Optional[Context] = None) -> LsrSolution:
+    """Sketch-and-precondition LSR (src/regression.cpp:94-198): T = R_Y^-1 from the QR of
+    Y = S'A, z0 = Q_Y' S'b, then O(log 1/eps) iterations, each one fused pass over A."""
+    a2 = _as2d(a)
+    b2 = _as2d(b)
+    x = np.empty(a2.shape[1], dtype=np.float64)
+    obj, kappa = C.c_double(), C.c_double()
+    it = C.c_int32()
+    am, bm = _mat(a2), _mat(b2)
+    _check(_abi.lib().rnla_lsr_preconditioned(
+        _ctx(ctx).handle, C.byref(am), C.byref(bm), float(eps), C.c_uint64(seed), int(opts.sketch_size),
+        1 if opts.use_cg else 0, int(opts.sketch_kind), x.ctypes.data_as(_abi._F64P), C.byref(obj), C.byref(it),
+        C.byref(kappa) if want_kappa else None))
+    return LsrSolution(x=x, objective=float(obj.value), iterations=int(it.value),
+                       kappa_estimate=float(kappa.value) if want_kappa else None)
 
 
 # --------------------------------------------------------------------------

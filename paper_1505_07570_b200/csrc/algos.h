@@ -25,6 +25,14 @@ void scale_rows_dev(rnla_ctx* ctx, int64_t r, int64_t n, const double* V, const 
 void scale_cols_dev(rnla_ctx* ctx, int64_t n, int64_t r, const double* V, const double* d, double* out);
 double sum_squares_dev(rnla_ctx* ctx, const double* p, int64_t count);
 
+// g = A'(beta*b - A w) and *rr = |beta*b - A w|^2 in one pass over the
+// row-major A (n x d, row stride ld; d <= 1024), fp64 accumulation; g and rr
+// are device pointers (lsr.cu).
+bool normal_gemv_supported(int64_t d);
+template <class T>
+void normal_gemv(rnla_ctx* ctx, int64_t n, int64_t d, const T* A, int64_t ld, const T* b, int64_t b_stride,
+                 double beta, const double* w, double* g, double* rr);
+
 // Row sketch of a row-major tall M (n rows of length L, row stride ld) into
 // out (element (t, c) at out[t*o_rs + c*o_cs]); api_sketch.cpp.
 template <class T>

@@ -173,3 +173,65 @@ def test_faster_ksvd_fp32_input(ctx):
     r = rn.faster_ksvd(dev(a), 6, 12, 200, 48, 4, opts=rn.KsvdOptions(True), ctx=ctx)
     assert r.factors.U.dtype == torch.float32
     assert r.error_fro <= 1e-5 * np.linalg.norm(a.astype(np.float64))
+
+
+def _ill_conditioned(n, d, seed, decades=5.0):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((n, d)))
+    v, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    a = (u * 10.0 ** (-decades * np.arange(d) / (d - 1))) @ v.T
+    return a, rng.standard_normal(n)
+
+
+def test_lsr_preconditioned_reference_cases(ctx):
+    # tests/test_regression.cpp:54-86
+    a, _ = orc.thin_qr(orc.gaussian_matrix(300, 6, 10))
+    b = orc.gaussian_matrix(300, 1, 11)[:, 0]
+    sol = rn.lsr_preconditioned(a, b, 1e-10, 13, rn.PreconditionedOptions(sketch_size=120), ctx=ctx)
+    exact = np.linalg.lstsq(a, b, rcond=None)[0]
+    assert np.linalg.norm(sol.x - exact) <= 1e-8 * (np.linalg.norm(exact) + 1)
+    assert sol.iterations <= 40 and sol.kappa_estimate <= 2.0
+    a, b = _ill_conditioned(800, 10, 20)
+    exact = np.linalg.lstsq(a, b, rcond=None)[0]
+    for cg in (False, True):
+        sol = rn.lsr_preconditioned(a, b, 1e-8, 22, rn.PreconditionedOptions(sketch_size=200, use_cg=cg), ctx=ctx)
+        assert np.linalg.norm(sol.x - exact) <= 1e-7 * np.linalg.norm(exact)
+        assert sol.iterations <= 80
+    with pytest.raises(ValueError, match="eps out of"):
+        rn.lsr_preconditioned(orc.gaussian_matrix(10, 4, 50), orc.gaussian_matrix(10, 1, 54), 2.0, 1, ctx=ctx)
+    with pytest.raises(ValueError, match="n < d"):
+        rn.lsr_preconditioned(orc.gaussian_matrix(3, 5, 50), orc.gaussian_matrix(3, 1, 54), 0.1, 1, ctx=ctx)
+
+
+@pytest.mark.parametrize("kind,cg,dtype", [("count", False, np.float64), ("count", True, np.float64),
+                                           ("gaussian", False, np.float64), ("srht", True, np.float64),
+                                           ("count", False, np.float32)])
+def test_lsr_preconditioned_matches_oracle(ctx, kind, cg, dtype):
+    a, b = _ill_conditioned(20000, 48, 3, decades=4.0)
+    a, b = a.astype(dtype), b.astype(dtype)
+    kinds = {"count": rn.SketchKind.kCountSketch, "gaussian": rn.SketchKind.kGaussian, "srht": rn.SketchKind.kSrht}
+    opts = rn.PreconditionedOptions(sketch_size=0, use_cg=cg, sketch_kind=kinds[kind])
+    sol = rn.lsr_preconditioned(dev(a), dev(b), 1e-10, 99, opts, ctx=ctx)
+    x, obj, it, kappa = orc.lsr_preconditioned(a.astype(np.float64), b.astype(np.float64), 1e-10, 99, kind=kind,
+                                               use_cg=cg)
+    tol = 1e-9 if dtype == np.float64 else 1e-5
+    assert np.linalg.norm(sol.x - x) <= tol * np.linalg.norm(x)
+    assert abs(sol.objective - obj) <= 1e-9 * obj
+    # the gradient-descent stop ("gradient stalled at the rounding floor",
+    # regression.cpp:159-166) is rounding-sensitive: the count may differ by a few
+    assert abs(sol.iterations - it) <= max(2, it // 10)
+    assert abs(sol.kappa_estimate - kappa) <= (1e-6 if dtype == np.float64 else 1e-4) * kappa
+
+
+def test_lsr_preconditioned_large_d_fused_pass(ctx):
+    # d = 512 (the config-1 width): the fused pass holds 16 fp64 per lane
+    rng = np.random.default_rng(8)
+    n, d = 60000, 512
+    a = rng.standard_normal((n, d))
+    b = a @ rng.standard_normal(d) + 0.1 * rng.standard_normal(n)
+    sol = rn.lsr_preconditioned(dev(a), dev(b), 1e-12, 4, want_kappa=False, ctx=ctx)
+    exact = np.linalg.lstsq(a, b, rcond=None)[0]
+    assert np.linalg.norm(sol.x - exact) <= 1e-10 * np.linalg.norm(exact)
+    r = a @ exact - b
+    assert abs(sol.objective - r @ r) <= 1e-10 * (r @ r)
+    assert sol.kappa_estimate is None

@@ -229,6 +229,30 @@ def test_sharded_srht_rows(ctx, world, n, dtype):
         assert np.linalg.norm(res[0] - o) <= 1e-12 * np.linalg.norm(o)
 
 
+@pytest.mark.parametrize("world,cg", [(2, False), (3, True)])
+def test_sharded_lsr_preconditioned(ctx, world, cg):
+    rng = np.random.default_rng(40 + world)
+    n, d = 30000, 40
+    a = rng.standard_normal((n, d)) * np.logspace(0, -3, d)
+    b = a @ rng.standard_normal(d) + 0.01 * rng.standard_normal(n)
+    opts = rn.PreconditionedOptions(use_cg=cg)
+    ref = rn.lsr_preconditioned(dev(a), dev(b), 1e-10, 7, opts, ctx=ctx)
+    sh = shards(n, world)
+
+    def fn(c, r):
+        lo, hi = sh[r]
+        return rn.lsr_preconditioned(dev(a[lo:hi]), dev(b[lo:hi]), 1e-10, 7, opts, ctx=c)
+
+    res = run_group(world, fn)
+    for s in res:
+        assert np.array_equal(s.x, res[0].x) and s.iterations == res[0].iterations
+    s = res[0]
+    assert np.linalg.norm(s.x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
+    assert abs(s.objective - ref.objective) <= 1e-10 * ref.objective
+    assert abs(s.iterations - ref.iterations) <= max(2, ref.iterations // 10)
+    assert abs(s.kappa_estimate - ref.kappa_estimate) <= 1e-8 * ref.kappa_estimate
+
+
 @pytest.mark.parametrize("world,dtype", [(2, np.float64), (3, np.float32)])
 def test_sharded_leverage_sample_rows(ctx, world, dtype):
     rng = np.random.default_rng(21)

@@ -239,3 +239,26 @@ def test_oracle_faster_ksvd_recovers_low_rank():
     assert np.linalg.norm(u.T @ u - np.eye(u.shape[1])) <= 1e-8
     with pytest.raises(ValueError):
         orc.faster_ksvd(a, 5, 10, 15, 20, 1)
+
+
+def test_oracle_lsr_preconditioned_reference_properties():
+    # tests/test_regression.cpp:54-86, restated on the oracle
+    a, _ = orc.thin_qr(orc.gaussian_matrix(300, 6, 10))
+    b = orc.gaussian_matrix(300, 1, 11)[:, 0]
+    x, obj, it, kappa = orc.lsr_preconditioned(a, b, 1e-10, 13, sketch_size=120)
+    exact = np.linalg.lstsq(a, b, rcond=None)[0]
+    assert np.linalg.norm(x - exact) <= 1e-8 * (np.linalg.norm(exact) + 1)
+    assert it <= 40 and kappa <= 2.0
+    rng = np.random.default_rng(20)
+    n, d = 800, 10
+    u, _ = np.linalg.qr(rng.standard_normal((n, d)))
+    v, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    a = (u * 10.0 ** (-5.0 * np.arange(d) / (d - 1))) @ v.T
+    b = rng.standard_normal(n)
+    exact = np.linalg.lstsq(a, b, rcond=None)[0]
+    for cg in (False, True):
+        x, _, it, _ = orc.lsr_preconditioned(a, b, 1e-8, 22, sketch_size=200, use_cg=cg)
+        assert np.linalg.norm(x - exact) <= 1e-7 * np.linalg.norm(exact)
+        assert it <= 80
+    with pytest.raises(ValueError):
+        orc.lsr_preconditioned(a, b, 2.0, 1)
