@@ -269,6 +269,31 @@ inline KsvdResult prototype_ksvd(const DenseMatrix& a, Index k, Index s, std::ui
   return r;
 }
 
+// randsvd.hpp:38-41: two passes, k < s < p < p_cs.
+inline KsvdResult faster_ksvd(const DenseMatrix& a, Index k, Index s, Index p_cs, Index p, std::uint64_t seed,
+                              const KsvdOptions& opts = {}) {
+  DenseMatrix u(a.rows(), k), v(a.cols(), k);
+  std::vector<double> sv(static_cast<size_t>(k));
+  Index rank = 0;
+  int32_t passes = 0;
+  double err = 0.0;
+  rnla_mat am = detail::view(a), um = detail::view(u), vm = detail::view(v);
+  detail::check(rnla_faster_ksvd(detail::ctx(), &am, k, s, p_cs, p, seed, &um, sv.data(), &vm, &rank, &passes,
+                                 opts.evaluate_error ? &err : nullptr));
+  KsvdResult r;
+  r.factors.U = DenseMatrix(a.rows(), rank);
+  r.factors.V = DenseMatrix(a.cols(), rank);
+  r.factors.singular_values = Vector(rank);
+  for (Index j = 0; j < rank; ++j) {
+    r.factors.singular_values(j) = sv[static_cast<size_t>(j)];
+    for (Index i = 0; i < a.rows(); ++i) r.factors.U(i, j) = u(i, j);
+    for (Index i = 0; i < a.cols(); ++i) r.factors.V(i, j) = v(i, j);
+  }
+  r.passes_over_a = passes;
+  if (opts.evaluate_error) r.error_fro = err;
+  return r;
+}
+
 // ---------------- regression.hpp ----------------
 struct LsrSolution {
   Vector x;
@@ -287,6 +312,28 @@ inline LsrSolution lsr_sketched(const DenseMatrix& a, const Vector& b, const Ske
   rnla_sketch_spec cs = spec.to_c();
   detail::check(rnla_lsr_sketched(detail::ctx(), &am, &bm, &cs, sol.x.data(), &sol.objective, &flagged));
   sol.flagged = flagged != 0;
+  return sol;
+}
+
+struct PreconditionedOptions {
+  Index sketch_size = 0;  // 0: min(d^2, 20 d) capped at n
+  bool use_cg = false;    // default: gradient descent with unit step
+  SketchKind sketch_kind = SketchKind::kCountSketch;
+};
+
+// regression.hpp:44-56 (src/regression.cpp:94-198).
+inline LsrSolution lsr_preconditioned(const DenseMatrix& a, const Vector& b, double eps, std::uint64_t seed,
+                                      const PreconditionedOptions& opts = {}) {
+  LsrSolution sol;
+  sol.x = Vector(a.cols());
+  int32_t it = 0;
+  double kappa = 0.0;
+  rnla_mat am = detail::view(a), bm = detail::view(b);
+  detail::check(rnla_lsr_preconditioned(detail::ctx(), &am, &bm, eps, seed, opts.sketch_size, opts.use_cg ? 1 : 0,
+                                        static_cast<int32_t>(opts.sketch_kind), sol.x.data(), &sol.objective, &it,
+                                        &kappa));
+  sol.iterations = it;
+  sol.kappa_estimate = kappa;
   return sol;
 }
 

@@ -128,6 +128,27 @@ int main() {
     const LsrSolution sk = lsr_sketched(a, b, SketchSpec::count_sketch(500, 9));
     CHECK(!sk.flagged);
     CHECK(sk.objective > 0.0);
+    // preconditioned LSR reaches the exact optimum: objective <= sketched objective
+    PreconditionedOptions po;
+    po.sketch_size = 200;
+    const LsrSolution pc = lsr_preconditioned(a, b, 1e-10, 13, po);
+    CHECK(pc.objective <= sk.objective && pc.iterations <= 100);
+    CHECK(pc.kappa_estimate.has_value() && *pc.kappa_estimate <= 2.0);
+    bool threw = false;
+    try {
+      lsr_preconditioned(a, b, 2.0, 1);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // faster k-SVD: rank-4 input recovered in two passes (test_randsvd.cpp:61-72)
+    const DenseMatrix a = matmul(random_matrix(120, 4, 6), random_matrix(4, 100, 60));
+    KsvdOptions opts;
+    opts.evaluate_error = true;
+    const KsvdResult r = faster_ksvd(a, 4, 16, 256, 64, 9, opts);
+    CHECK(*r.error_fro <= 1e-6 * fro(a));
+    CHECK(r.passes_over_a == 2);
   }
   {  // RBF kernel: exact unit diagonal and bitwise symmetry (test_spsd.cpp:20-31)
     const DenseMatrix x = random_matrix(30, 4, 1);
