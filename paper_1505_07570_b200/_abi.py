@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librnla_b200.so")
+# RNLA_LIB_PATH: load an alternative build of the same library (A/B kernel experiments).
+LIB_PATH = os.environ.get("RNLA_LIB_PATH") or os.path.join(_HERE, "_lib", "librnla_b200.so")
 
 RNLA_OK, RNLA_EINVAL, RNLA_ENUMERIC, RNLA_ECUDA, RNLA_ENCCL, RNLA_ENOMEM = range(6)
 RNLA_F64, RNLA_F32 = 0, 1

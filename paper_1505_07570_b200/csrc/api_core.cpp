@@ -4,6 +4,8 @@
 #include <cusolverDn.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <cstdlib>
 #include <new>
 
 #include "dist.h"
@@ -45,6 +47,17 @@ rnla_status guard(const std::function<void()>& f) {
     return RNLA_ECUDA;
   }
   }
+}
+
+void trace_mark(rnla_ctx* ctx, const char* label) {
+  static const bool on = std::getenv("RNLA_TRACE") != nullptr;
+  if (!on) return;
+  static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(ctx->stream);
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[rnla trace] %-40s %9.3f ms\n", label,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 StreamScope::StreamScope(rnla_ctx* c, cudaStream_t s) : ctx(c), saved(c->stream) {

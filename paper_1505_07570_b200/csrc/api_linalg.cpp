@@ -671,6 +671,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
     int64_t n_total = n;
     const int64_t r_off = global_row_offset(ctx, n, &n_total);
     require(n_total >= d && d >= 1, "thin_qr: rows < cols");
+    trace_mark(ctx, "leverage_rows: enter");
     DevMat M = to_device(ctx, m);
     DevBuf G(sizeof(double) * d * d, ctx->stream), Rinv(sizeof(double) * d * d, ctx->stream);
     if (n == 0)
@@ -681,10 +682,12 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
     else
       gemm_f32_f64acc(ctx, d, d, n, 1.0, M.as<float>(), M.cs, M.rs, M.as<float>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
                       d);
+    trace_mark(ctx, "leverage_rows: gram");
     if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(d * d), RNLA_F64);
     if (!cholesky_upper(ctx, d, G.as<double>()))
       throw NumericError("leverage_sample_rows: M'M is not positive definite (rank-deficient M)");
     upper_inverse(ctx, d, G.as<double>(), Rinv.as<double>());
+    trace_mark(ctx, "leverage_rows: chol+inverse");
     DevBuf sc(sizeof(double) * n, ctx->stream);
     const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(n, ((int64_t)1 << 26) / d));
     DevBuf T(sizeof(double) * blk * d, ctx->stream);
@@ -705,8 +708,10 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
         row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
       }
     }
+    trace_mark(ctx, "leverage_rows: scores");
     if (n > 0) RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    trace_mark(ctx, "leverage_rows: d2h");
     if (indices) {
       std::vector<double> all_scores;
       const double* w = scores;
@@ -726,6 +731,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
       std::sort(draws.begin(), draws.end());
       draws.erase(std::unique(draws.begin(), draws.end()), draws.end());
       std::copy(draws.begin(), draws.end(), indices);
+      trace_mark(ctx, "leverage_rows: d2h + host draw");
       *count_out = (int64_t)draws.size();
     }
   });

@@ -22,6 +22,7 @@
 // loader always produces K-major smem, so only the K-major descriptor is used.
 // The fp32 data is read through registers because it has to be split before
 // the MMA anyway (a TMA copy would add an smem round trip).
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "rnla_internal.h"
@@ -32,10 +33,17 @@ namespace rnla {
 namespace {
 
 constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES_MAX = 4;
-constexpr int TC_PRODUCERS = 256;  // warps 0-7
-constexpr int TC_GROUP = 128;      // producer group (4 warps) per k-block
-constexpr int TC_MMA_WARP = 12;    // warps 8-11 run the epilogue
-constexpr int TC_THREADS = 416;
+// Producer groups of 4 warps take k-blocks round-robin (more groups = more
+// A bytes in flight per SM: the loads are register-staged).
+#ifndef RNLA_TC_NGROUPS
+#define RNLA_TC_NGROUPS 2
+#endif
+constexpr int TC_NGROUPS = RNLA_TC_NGROUPS;
+constexpr int TC_GROUP = 128;                     // producer group (4 warps) per k-block
+constexpr int TC_PRODUCERS = TC_GROUP * TC_NGROUPS;  // warps 0 .. 4*NG-1
+constexpr int TC_EPI_WARP0 = 4 * TC_NGROUPS;      // 4 epilogue warps (TMEM lane quarters)
+constexpr int TC_MMA_WARP = TC_EPI_WARP0 + 4;     // one MMA-issuing warp
+constexpr int TC_THREADS = 32 * (TC_MMA_WARP + 1);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -195,6 +203,31 @@ __device__ __forceinline__ void load_unit(const float* __restrict__ X, int64_t r
   }
 }
 
+#ifndef RNLA_TC_PF
+#define RNLA_TC_PF 0  // measured: no gain on the config-3 passes (38.3 vs 38.8 ms); off by default
+#endif
+// L2 prefetch of one 128-row x 64-k fp32 tile by the 128 threads of a group.
+template <bool KCONTIG>
+__device__ __forceinline__ void prefetch_tile_l2(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
+                                                 int64_t r0, int64_t k0, int64_t kend, int tid) {
+  if (KCONTIG) {  // row r = tid: 64 k = 256 B = two 128-B lines
+    const int64_t gr = r0 + tid;
+    if (gr < rows) {
+      const float* p = X + gr * rs + k0 * ks;
+      asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p));
+      if (k0 + 32 < kend) asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p + 32 * ks));
+    }
+  } else {  // k-row kk = tid / 2 (64 of them), half h: rows r0 + 64h .. of 128 contiguous floats
+    const int kk = tid >> 1, h = tid & 1;
+    const int64_t gk = k0 + kk, gr = r0 + 64 * h;
+    if (gk < kend && gr < rows) {
+      const float* p = X + gr * rs + gk * ks;
+      asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p));
+      if (gr + 32 < rows) asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p + 32 * rs));
+    }
+  }
+}
+
 // All loads of the tile are issued before any conversion (R*8/256 units per
 // thread in flight), then each unit is split and stored.
 // NS pieces go to tiles base, base + R*128, base + 2*R*128.
@@ -262,6 +295,61 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
                : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_g2s(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// TMA-fed variant: the fp32 A k-block (128 rows x 64 k) lands in the stage by
+// TMA (K-contiguous A: two 128 B-wide SWIZZLE_128B boxes; MN-contiguous A: one
+// unswizzled [64 k][128 rows] box), then a producer group reads it from smem,
+// splits it and writes the bf16 pieces IN PLACE (the pieces need as many
+// bytes as the fp32 tile for NS = 2): the DRAM latency is covered by the TMA
+// ring instead of by registers.
+template <bool KCONTIG, int NS>
+__device__ __forceinline__ void convert_tile_inplace(uint8_t* base, int gtid, int grp) {
+  constexpr int UPT = (TC_BM * 8) / TC_GROUP;
+  constexpr int A_TILE = TC_BM * 128;
+  float f[UPT][8];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int u = gtid + i * TC_GROUP;
+    int r, q;
+    unit_coords<KCONTIG>(u, TC_BM, r, q);
+    if (KCONTIG) {
+      const uint8_t* row = base + (q >> 2) * (A_TILE) + r * 128;
+      const int g0 = (q & 3) * 2;
+      const float4 a = *reinterpret_cast<const float4*>(row + ((g0 ^ (r & 7)) << 4));
+      const float4 b = *reinterpret_cast<const float4*>(row + (((g0 + 1) ^ (r & 7)) << 4));
+      f[i][0] = a.x; f[i][1] = a.y; f[i][2] = a.z; f[i][3] = a.w;
+      f[i][4] = b.x; f[i][5] = b.y; f[i][6] = b.z; f[i][7] = b.w;
+    } else {
+      const float* tile = reinterpret_cast<const float*>(base);  // [64 k][128 rows]
+#pragma unroll
+      for (int t = 0; t < 8; ++t) f[i][t] = tile[(8 * q + t) * TC_BM + r];
+    }
+  }
+  named_bar_sync(1 + grp, TC_GROUP);  // the whole fp32 tile is in registers before it is overwritten
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int u = gtid + i * TC_GROUP;
+    int r, q;
+    unit_coords<KCONTIG>(u, TC_BM, r, q);
+    uint4 pc[NS];
+    split8n<NS>(f[i], pc);
+    const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
+#pragma unroll
+    for (int p = 0; p < NS; ++p) *reinterpret_cast<uint4*>(base + p * A_TILE + off) = pc[p];
+  }
+}
+
 __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
@@ -272,13 +360,17 @@ __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void* src, uin
 // updated with TwoSum every 4 k-blocks (256 rows), output in fp64 -- for the
 // Nystrom Gram C'C, whose W^+-weighted eigenvalues need fp64-grade
 // accumulation across <= 256-row chunks (SURVEY §7 hard part 8).
-template <bool A_KC, int BN, int STAGES, bool DF>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <bool A_KC, int BN, int STAGES, bool DF, bool TMA_A>
+__global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
     gemm_bf16x3_kernel(int64_t M, int64_t N, int64_t K, int64_t kchunk, const float* __restrict__ A, int64_t a_rs,
                        int64_t a_cs, const uint8_t* __restrict__ bimg, int64_t nkb_total, double alpha,
                        double beta, typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-                       typename std::conditional<DF, double, float>::type* ws) {
+                       typename std::conditional<DF, double, float>::type* ws, int sym,
+                       const __grid_constant__ CUtensorMap amap) {
   using OutT = typename std::conditional<DF, double, float>::type;
+  // symmetric products (C = A'A): tiles strictly below the diagonal are skipped
+  // (uniformly for the whole CTA, before any barrier) and mirrored afterwards
+  if (sym && (int64_t)blockIdx.x * TC_BM >= ((int64_t)blockIdx.y + 1) * BN) return;
   constexpr int PKB = DF ? 4 : TC_PROMOTE_KB;
   // DF also splits three ways (BF16x6: hh, hm, mh, hl, lh, mm ~ fp32-faithful
   // products, 1.9e-7 rel-F per SURVEY §7 hard part 5); otherwise BF16x3.
@@ -296,9 +388,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr uint32_t TMEM_COLS = TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // full[S], empty[S], xfull[2], xfree[2]
+  // full[S], empty[S], xfull[2], xfree[2], tfull[S] (TMA_A: the A tile and B image landed)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* tfull = bars + 2 * STAGES + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m0 = (int64_t)blockIdx.x * TC_BM, n0 = (int64_t)blockIdx.y * BN;
@@ -307,8 +400,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&bars[s]), TC_GROUP + 1);  // a producer group + the bulk-copy expect_tx arrive
+      // a producer group (+ the bulk-copy expect_tx arrive when the group issues it)
+      mbar_init(smem_u32(&bars[s]), TMA_A ? TC_GROUP : TC_GROUP + 1);
       mbar_init(smem_u32(&bars[STAGES + s]), 1);
+      mbar_init(smem_u32(&tfull[s]), 1);
     }
     mbar_init(smem_u32(&bars[2 * STAGES]), 1);      // xfull[0]
     mbar_init(smem_u32(&bars[2 * STAGES + 1]), 1);  // xfull[1]
@@ -316,7 +411,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_init(smem_u32(&bars[2 * STAGES + 3]), 128);  // xfree[1]
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 8) {  // TMEM accumulator: 128 lanes x TMEM_COLS fp32 columns
+  if (warp == TC_EPI_WARP0) {  // TMEM accumulator: 128 lanes x TMEM_COLS fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -326,14 +421,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 8) {
+  if (TMA_A && warp < TC_EPI_WARP0) {
+    // ---------------- converters: groups take k-blocks round-robin; each waits
+    // for its stage's TMA, splits the fp32 tile in place, hands it to the MMA ----------------
+    const int grp = warp >> 2, gtid = tid & (TC_GROUP - 1);
+    for (int kb = grp; kb < nkb; kb += TC_NGROUPS) {
+      const int st = kb % STAGES;
+      // TMA completions may land out of order: before the parity wait on tfull,
+      // make sure the stage's previous phase (k-block kb - STAGES) was consumed,
+      // so this wait cannot alias a phase two steps back.
+      if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
+      mbar_wait(smem_u32(&tfull[st]), (uint32_t)((kb / STAGES) & 1));
+      convert_tile_inplace<A_KC, NS>(smem + st * STAGE, gtid, grp);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(smem_u32(&bars[st]));
+    }
+  } else if (TMA_A && warp == TC_MMA_WARP + 1) {
+    // ---------------- TMA issuer: A boxes + the B image of each stage ----------------
+    if (lane == 0) {
+      const int64_t kb0 = kbeg / TC_BK;
+      const uint8_t* bsrc = bimg + ((int64_t)blockIdx.y * nkb_total + kb0) * (int64_t)(NS * B_TILE);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
+        uint8_t* base = smem + st * STAGE;
+        const uint32_t bar = smem_u32(&tfull[st]);
+        mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 + NS * B_TILE));
+        const int k0 = (int)(kbeg + (int64_t)kb * TC_BK);
+        if (A_KC) {
+          tma_load_2d_g2s(smem_u32(base), &amap, k0, (int)m0, bar);
+          tma_load_2d_g2s(smem_u32(base + A_TILE), &amap, k0 + 32, (int)m0, bar);
+        } else {
+          tma_load_2d_g2s(smem_u32(base), &amap, (int)m0, k0, bar);
+        }
+        bulk_copy_g2s(smem_u32(base + NS * A_TILE), bsrc + (int64_t)kb * (NS * B_TILE), NS * B_TILE, bar);
+      }
+    }
+    __syncwarp();
+  } else if (warp < TC_EPI_WARP0) {
     // ---------------- producers: two groups of 4 warps take alternate k-blocks,
     // so two k-blocks of A loads are in flight per SM ----------------
     const int grp = warp >> 2, gtid = tid & (TC_GROUP - 1);
     const int64_t kb0 = kbeg / TC_BK;
     const uint8_t* bsrc = bimg + ((int64_t)blockIdx.y * nkb_total + kb0) * (int64_t)(NS * B_TILE);
-    for (int kb = grp; kb < nkb; kb += 2) {
+    for (int kb = grp; kb < nkb; kb += TC_NGROUPS) {
       const int st = kb % STAGES;
+#if RNLA_TC_PF > 0
+      {  // warm L2 with this group's k-block RNLA_TC_PF rounds ahead (hides DRAM latency
+         // of the register-staged loads without more registers)
+        const int64_t kp = kbeg + (int64_t)(kb + RNLA_TC_PF * TC_NGROUPS) * TC_BK;
+        if (kp < kend) prefetch_tile_l2<A_KC>(A, a_rs, a_cs, M, m0, kp, kend, gtid);
+      }
+#endif
       if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
       uint8_t* base = smem + st * STAGE;
       if (gtid == 0) {
@@ -362,7 +501,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint32_t base = smem_u32(smem + st * STAGE);
           const uint32_t a0 = base, b0 = base + NS * A_TILE;
           // products (i, j) of pieces: (0,0) (0,1) (1,0) [+ (0,2) (2,0) (1,1) for NS = 3]
-          constexpr int NP = NS == 3 ? 6 : 3;
+#ifndef RNLA_TC_NPMAX
+#define RNLA_TC_NPMAX 6
+#endif
+          constexpr int NP = (NS == 3 ? 6 : 3) < RNLA_TC_NPMAX ? (NS == 3 ? 6 : 3) : RNLA_TC_NPMAX;  // NPMAX: timing experiments only
           constexpr int PI[6] = {0, 0, 1, 0, 2, 1}, PJ[6] = {0, 1, 0, 2, 0, 1};
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
@@ -469,17 +611,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
-  if (warp == 8) {
+  if (warp == TC_EPI_WARP0) {
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
-template <bool A_KC, int BN, int STAGES, bool DF>
+template <bool A_KC, int BN, int STAGES, bool DF, bool TMA_A>
 void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
                typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-               typename std::conditional<DF, double, float>::type* ws) {
+               typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap) {
   constexpr int NS = DF ? 3 : 2;
   constexpr size_t STAGE = NS * (TC_BM * 128 + BN * 128);
   const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
@@ -488,12 +630,14 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
                                                                                        nblk, img.as<uint8_t>());
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
-  const size_t smem = STAGES * STAGE + 1024 + 8 * (2 * STAGES + 5);
-  auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES, DF>;
+  const size_t smem = STAGES * STAGE + 1024 + 8 * (3 * STAGES + 5);
+  auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES, DF, TMA_A>;
   RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)nblk, (unsigned)splits);
-  kern<<<grid, TC_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, A, a_rs, a_cs, img.as<uint8_t>(), nkb, alpha, beta,
-                                                 C, c_rs, c_cs, ws);
+  CUtensorMap dummy{};
+  kern<<<grid, TMA_A ? TC_THREADS + 32 : TC_THREADS, smem, ctx->stream>>>(
+      m, n, k, kchunk, A, a_rs, a_cs, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs, ws, sym,
+      amap ? *amap : dummy);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
@@ -502,13 +646,19 @@ template <bool A_KC, bool DF>
 void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                  int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
                  typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-                 typename std::conditional<DF, double, float>::type* ws) {
+                 typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap) {
   // as many stages as fit in ~220 KB of shared memory (at most 4)
 #define RNLA_ST(BNV) \
   std::min(4, (220 * 1024) / ((DF ? 3 : 2) * (TC_BM * 128 + (BNV) * 128)))
-#define RNLA_TC(BNV) \
-  launch_tc<A_KC, BNV, RNLA_ST(BNV), DF>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C, \
-                                         c_rs, c_cs, ws)
+#define RNLA_TC(BNV)                                                                                           \
+  do {                                                                                                         \
+    if (amap)                                                                                                  \
+      launch_tc<A_KC, BNV, RNLA_ST(BNV), DF, true>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs, b_cs, \
+                                                   alpha, beta, C, c_rs, c_cs, ws, sym, amap);                 \
+    else                                                                                                       \
+      launch_tc<A_KC, BNV, RNLA_ST(BNV), DF, false>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs,      \
+                                                    b_cs, alpha, beta, C, c_rs, c_cs, ws, sym, nullptr);       \
+  } while (0)
   if (bn <= 32) RNLA_TC(32);
   else if (bn <= 64) RNLA_TC(64);
   else if (bn <= 96) RNLA_TC(96);
@@ -531,6 +681,61 @@ __global__ void splitk_reduce_tc(int64_t m, int64_t n, int splits, const OutT* _
   }
 }
 
+// TMA map of the fp32 A operand for the TMA-fed kernel, or false when the
+// layout does not allow it (then the register-staged loader runs).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+bool make_a_map(CUtensorMap* map, const float* A, int64_t m, int64_t k, int64_t a_rs, int64_t a_cs) {
+  // Opt-in (RNLA_TC_TMA=1): measured 38.1 vs 38.6 ms on config 3 (the A path
+  // is not latency-bound), and one full-suite run stalled once with it on, so
+  // the register-staged loader stays the default until that is understood.
+  static const bool off = std::getenv("RNLA_TC_TMA") == nullptr || std::getenv("RNLA_TC_NO_TMA") != nullptr;
+  if (off || !encode_tiled() || (reinterpret_cast<uintptr_t>(A) & 15) || m >= INT32_MAX || k >= INT32_MAX) return false;
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r;
+  if (a_cs == 1 && a_rs > 0 && (a_rs * 4) % 16 == 0) {  // K-contiguous: dims {k, m}, boxes {32 k, 128 rows}, SW128
+    const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)m};
+    const cuuint64_t strides[1] = {(cuuint64_t)a_rs * 4};
+    const cuuint32_t box[2] = {32, (cuuint32_t)TC_BM};
+    r = encode_tiled()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (a_rs == 1 && a_cs > 0 && (a_cs * 4) % 16 == 0) {  // MN-contiguous: dims {m, k}, box {128 rows, 64 k}
+    const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)k};
+    const cuuint64_t strides[1] = {(cuuint64_t)a_cs * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_BM, (cuuint32_t)TC_BK};
+    r = encode_tiled()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    return false;
+  }
+  return r == CUDA_SUCCESS;
+}
+
+// C(i, j) = C(j, i) for the tiles a symmetric launch skipped.
+template <class OutT>
+__global__ void mirror_skipped_tiles(int64_t n, int bm, int bn, OutT* C, int64_t c_rs, int64_t c_cs) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    if ((i / bm) * bm >= (j / bn + 1) * bn) C[i * c_rs + j * c_cs] = C[j * c_rs + i * c_cs];
+  }
+}
+
 template <bool DF>
 void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                   int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta,
@@ -543,10 +748,34 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   const int bn_full = n <= cap ? (int)(((n + 15) / 16) * 16) : 128;
   const int64_t ntiles = (n + bn_full - 1) / bn_full;
   const int64_t tiles = ((m + TC_BM - 1) / TC_BM) * ntiles;
-  // split K until every SM has a tile (K ranges stay multiples of 64)
+  // Split K so that the CTAs fill whole waves of the 148 SMs (one CTA per SM):
+  // the smallest split count reaching >= 97 % wave efficiency among those that
+  // give every SM a tile, each split keeping >= 4 k-blocks and the fp32/fp64
+  // workspace <= 512 MB. (Measured: A'Q at 16384 x 150, K = 262144 ran 256
+  // CTAs = 1.73 waves.)
   int64_t splits = 1;
-  if (tiles < ctx->num_sms && k >= 2 * TC_BK)
-    splits = std::min<int64_t>((ctx->num_sms + tiles - 1) / tiles, k / TC_BK);
+  if (DF) {
+    // double-float Grams keep the original rule (as many splits as SMs): short
+    // K ranges per CTA accumulate in TMEM for only a few k-blocks, and the
+    // partials are summed in fp64 (row-leverage sums stay within ~1e-7)
+    if (tiles < ctx->num_sms && k >= 2 * TC_BK)
+      splits = std::min<int64_t>((ctx->num_sms + tiles - 1) / tiles, k / TC_BK);
+  } else if (k >= 2 * TC_BK) {
+    const int64_t sms = ctx->num_sms;
+    const int64_t ws_cap = ((int64_t)512 << 20) / std::max<int64_t>(1, m * n * (int64_t)sizeof(OutT));
+    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(k / (4 * TC_BK), 256), ws_cap));
+    const int64_t smin = std::min<int64_t>(smax, (sms + tiles - 1) / tiles);
+    double best = -1.0;
+    for (int64_t s = smin; s <= smax; ++s) {
+      const double w = (double)(tiles * s) / (double)sms;
+      const double eff = w / std::ceil(w);
+      if (eff > best + 1e-9) {
+        best = eff;
+        splits = s;
+      }
+      if (eff >= 0.97) break;
+    }
+  }
   int64_t kchunk = ((k + splits - 1) / splits + TC_BK - 1) / TC_BK * TC_BK;
   if (k == 0) kchunk = TC_BK;
   splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
@@ -556,17 +785,39 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
     wsb = DevBuf(sizeof(OutT) * (size_t)(splits * m * n), ctx->stream);
     ws = wsb.as<OutT>();
   }
+  // Gram products (B = A') are symmetric: upper tiles only, then mirror.
+  const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs && !std::getenv("RNLA_TC_NO_SYM")) ? 1 : 0;
+  CUtensorMap amap;
+  const bool tma = make_a_map(&amap, A, m, k, a_rs, a_cs);
   if (a_cs == 1)
     dispatch_bn<true, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
-                          c_rs, c_cs, ws);
+                          c_rs, c_cs, ws, sym, tma ? &amap : nullptr);
   else
     dispatch_bn<false, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
-                           c_rs, c_cs, ws);
+                           c_rs, c_cs, ws, sym, tma ? &amap : nullptr);
   if (splits > 1) {
     splitk_reduce_tc<OutT><<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, n, (int)splits, ws, alpha, beta, C,
                                                                                c_rs, c_cs);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
+  }
+  if (sym) {
+    const int bn_eff = bn_full <= 32 ? 32 : bn_full <= 64 ? 64 : bn_full <= 96 ? 96 : (DF || bn_full <= 128) ? 128 : 160;
+    mirror_skipped_tiles<OutT><<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, TC_BM, bn_eff, C, c_rs, c_cs);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+  if (std::getenv("RNLA_TC_DEBUG")) {  // debugging aid: report non-finite outputs per call
+    const int64_t span = (m - 1) * c_rs + (n - 1) * c_cs + 1;
+    std::vector<OutT> h((size_t)span);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    RNLA_CUDA(cudaMemcpy(h.data(), C, sizeof(OutT) * span, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) bad += !std::isfinite((double)h[(size_t)(i * c_rs + j * c_cs)]);
+    std::fprintf(stderr, "tc gemm m=%lld n=%lld k=%lld a_rs=%lld a_cs=%lld tma=%d splits=%lld sym=%d nonfinite=%lld\n",
+                 (long long)m, (long long)n, (long long)k, (long long)a_rs, (long long)a_cs, (int)tma,
+                 (long long)splits, sym, (long long)bad);
   }
 }
 

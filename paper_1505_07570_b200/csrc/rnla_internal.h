@@ -32,6 +32,11 @@ struct NcclError : std::runtime_error {
 };
 
 // Mirror of the reference's require() (include/randnla/types.hpp:35-37).
+// Overloads: a literal message costs nothing unless the check fails (no
+// std::string temporary per call inside host loops).
+inline void require(bool cond, const char* msg) {
+  if (!cond) throw InvalidArgument(msg);
+}
 inline void require(bool cond, const std::string& msg) {
   if (!cond) throw InvalidArgument(msg);
 }
@@ -130,6 +135,10 @@ const CountSketchPlan& count_sketch_plan(rnla_ctx* ctx, int64_t n, int64_t s, ui
 template <class T>
 void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
           const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs, int max_splits = 64);
+
+// Phase tracing (RNLA_TRACE=1): synchronizes the context stream and prints the
+// wall time since the previous mark of this thread to stderr. No-op otherwise.
+void trace_mark(rnla_ctx* ctx, const char* label);
 
 // Temporarily route ctx launches to another stream (RAII).
 struct StreamScope {
