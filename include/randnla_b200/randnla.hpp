@@ -369,4 +369,45 @@ inline NystromFactor nystrom(const DenseMatrix& data, const KernelSpec& spec, In
   return f;
 }
 
+// spsd.hpp:86-94, 109-115 (src/spsd.cpp:131-168).
+struct SpsdSketch {
+  DenseMatrix Q, Z;
+  std::vector<Index> selected, secondary;
+  bool flagged = false;
+};
+
+namespace detail {
+inline SpsdSketch spsd_faster_call(const DenseMatrix& x, const KernelSpec* spec, Index s, Index p,
+                                   std::uint64_t seed) {
+  const Index n = x.rows();
+  SpsdSketch out;
+  out.Q = DenseMatrix(n, s);
+  out.Z = DenseMatrix(s, s);
+  out.selected.resize(static_cast<size_t>(s));
+  std::vector<Index> sec(static_cast<size_t>(std::max<Index>(1, std::min(n, p + s))));
+  Index nsec = 0;
+  int32_t flagged = 0;
+  rnla_mat xm = view(x), qm = view(out.Q), zm = view(out.Z);
+  if (spec)
+    check(rnla_spsd_faster(ctx(), &xm, spec->sigma, s, p, seed, &qm, &zm, out.selected.data(), sec.data(), &nsec,
+                           &flagged));
+  else
+    check(rnla_spsd_faster_dense(ctx(), &xm, s, p, seed, &qm, &zm, out.selected.data(), sec.data(), &nsec,
+                                 &flagged));
+  sec.resize(static_cast<size_t>(nsec));
+  out.secondary = sec;
+  out.flagged = flagged != 0;
+  return out;
+}
+}  // namespace detail
+
+// KernelView over `data` with `spec` (the reference's spsd_faster(const KernelView&, ...)).
+inline SpsdSketch spsd_faster(const DenseMatrix& data, const KernelSpec& spec, Index s, Index p, std::uint64_t seed) {
+  return detail::spsd_faster_call(data, &spec, s, p, seed);
+}
+// Dense SPSD K (the reference's spsd_faster(const DenseMatrix&, ...)).
+inline SpsdSketch spsd_faster(const DenseMatrix& k, Index s, Index p, std::uint64_t seed) {
+  return detail::spsd_faster_call(k, nullptr, s, p, seed);
+}
+
 }  // namespace randnla_b200

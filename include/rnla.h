@@ -246,6 +246,20 @@ rnla_status rnla_approx_eig(rnla_ctx* ctx, const rnla_mat* l, int64_t k, rnla_ma
 rnla_status rnla_nystrom_eig(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed,
                              int64_t target_k, int64_t k, rnla_mat* u, double* lam, int64_t* selected,
                              int64_t* kept);
+/* spsd_faster on a KernelView of the points x (n x d), spsd.hpp:113-115
+ * (src/spsd.cpp:131-168): S = landmarks (derive_seed(seed, 1)), Q = thin_qr(K[:, S]).Q
+ * (n x s), secondary rows P = leverage draws of Q's rows (derive_seed(seed, 2);
+ * all rows when p == n) united with S, Z = pinv(Q_P) K[P, P] pinv(Q_P)' (s x s,
+ * symmetrized). selected[s]; secondary needs room for min(n, p + s) indices,
+ * *n_secondary = |P|; *flagged = 1 when Q_P is rank deficient (threshold 1e-10).
+ * Kernel entries evaluated: n*s + |P|^2. */
+rnla_status rnla_spsd_faster(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, int64_t p, uint64_t seed,
+                             rnla_mat* q, rnla_mat* z, int64_t* selected, int64_t* secondary, int64_t* n_secondary,
+                             int32_t* flagged);
+/* The same on a dense SPSD K (n x n), spsd.hpp:111-112. */
+rnla_status rnla_spsd_faster_dense(rnla_ctx* ctx, const rnla_mat* k, int64_t s, int64_t p, uint64_t seed, rnla_mat* q,
+                                   rnla_mat* z, int64_t* selected, int64_t* secondary, int64_t* n_secondary,
+                                   int32_t* flagged);
 
 #ifdef __cplusplus
 }

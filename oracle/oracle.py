@@ -425,6 +425,33 @@ def approx_eig(l: np.ndarray, k: int):
     return u[:, :k], sv[:k] ** 2
 
 
+def spsd_faster(x: np.ndarray, sigma: float, s: int, p: int, seed: int, dense: bool = False):
+    """src/spsd.cpp:131-168 on a KernelView of x (or on the dense SPSD x when dense=True).
+    Returns (Q, Z, selected, secondary, flagged)."""
+    x = np.asarray(x, dtype=np.float64)
+    n = x.shape[0]
+    if not (1 <= s <= p <= n):
+        raise ValueError("spsd_faster: need s <= p <= n")
+    sel = sample_without_replacement(n, s, derive_seed(seed, 1))
+    c = x[:, sel] if dense else rbf_kernel(x, x[sel], sigma)
+    if not dense:
+        c[sel, np.arange(s)] = 1.0
+    q, _ = thin_qr(c)
+    if p == n:
+        sec = np.arange(n)
+    else:
+        lev = np.einsum("ij,ij->i", q, q)
+        sec = np.union1d(np.unique(sample_with_replacement(lev, p, derive_seed(seed, 2))), sel)
+    q_sub = q[sec]
+    k_sub = x[np.ix_(sec, sec)] if dense else rbf_kernel(x[sec], x[sec], sigma)
+    if not dense:
+        np.fill_diagonal(k_sub, 1.0)
+    flagged = numerical_rank(q_sub) < s
+    pinv = pseudo_inverse(q_sub)
+    z = pinv @ k_sub @ pinv.T
+    return q, 0.5 * (z + z.T), sel, sec, flagged
+
+
 def leverage_scores(a: np.ndarray, k: Optional[int] = None) -> np.ndarray:
     u, s, v = truncated_svd(a, k) if k else condensed_svd(a)
     return np.sum(v * v, axis=1)

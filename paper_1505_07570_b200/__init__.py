@@ -31,7 +31,7 @@ __all__ = [
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
     "count_sketch", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
     "leverage_sample_columns", "leverage_sample_rows", "thin_qr", "condensed_svd", "truncated_svd",
-    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig",
+    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig", "SpsdSketch", "spsd_faster",
     "shard_rows",
 ]
 
@@ -742,3 +742,40 @@ def nystrom_eig(k: KernelView, s: int, seed: int, target_k: int, n_eig: int, wan
                                        C.byref(kept)))
     k._add(n * s)
     return u, lam, sel, kept.value
+
+
+@dataclasses.dataclass
+class SpsdSketch:
+    """include/randnla/spsd.hpp:86-94: K ~ Q Z Q'."""
+    Q: object
+    Z: np.ndarray
+    selected: np.ndarray
+    secondary: np.ndarray
+    flagged: bool = False
+
+    def reconstruct(self):
+        q = self.Q.cpu().numpy() if _is_torch(self.Q) else np.asarray(self.Q)
+        return q @ self.Z @ q.T
+
+
+def spsd_faster(k, s: int, p: int, seed: int, ctx: Optional[Context] = None) -> SpsdSketch:
+    """Faster SPSD sketch (src/spsd.cpp:131-168) of a KernelView (entries evaluated on the
+    device: n*s + |P|^2) or of a dense SPSD matrix."""
+    view = k if isinstance(k, KernelView) else None
+    x = view.data() if view is not None else _as2d(k)
+    n = int(x.shape[0])
+    q = _empty_like(x, n, s, "F", dtype=None)
+    z = np.empty((s, s), dtype=np.float64, order="F")
+    sel = np.empty(s, dtype=np.int64)
+    sec = np.empty(max(1, min(n, p + s)), dtype=np.int64)
+    nsec, flagged = C.c_int64(), C.c_int32()
+    xm, qm, zm = _mat(x), _mat(q), _mat(z)
+    args = (C.byref(qm), C.byref(zm), sel.ctypes.data_as(_abi._I64P), sec.ctypes.data_as(_abi._I64P),
+            C.byref(nsec), C.byref(flagged))
+    if view is not None:
+        _check(_abi.lib().rnla_spsd_faster(_ctx(ctx).handle, C.byref(xm), float(view.spec().sigma), s, p,
+                                           C.c_uint64(seed), *args))
+        view._add(n * s + nsec.value * nsec.value)
+    else:
+        _check(_abi.lib().rnla_spsd_faster_dense(_ctx(ctx).handle, C.byref(xm), s, p, C.c_uint64(seed), *args))
+    return SpsdSketch(q, z, sel, sec[:nsec.value].copy(), bool(flagged.value))

@@ -102,6 +102,10 @@ SIGNATURES = {
     "rnla_approx_eig": (C.c_int, [_P, _M, C.c_int64, _M, _F64P]),
     "rnla_nystrom_eig": (
         C.c_int, [_P, _M, C.c_double, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, _M, _F64P, _I64P, _I64P]),
+    "rnla_spsd_faster": (
+        C.c_int, [_P, _M, C.c_double, C.c_int64, C.c_int64, C.c_uint64, _M, _M, _I64P, _I64P, _I64P, _I32P]),
+    "rnla_spsd_faster_dense": (
+        C.c_int, [_P, _M, C.c_int64, C.c_int64, C.c_uint64, _M, _M, _I64P, _I64P, _I64P, _I32P]),
 }
 
 

@@ -14,10 +14,20 @@
 namespace rnla {
 
 static thread_local std::string g_last_error;
+static thread_local rnla_ctx* g_cur_ctx = nullptr;  // context of the entry point running on this thread
+
+// A device/transport failure on one rank of an in-process shard group would
+// leave the other ranks waiting in their next collective: mark the group
+// broken so they fail fast instead (argument and numerical errors are
+// replicated decisions, raised on every rank alike).
+static void break_group_on_failure() {
+  if (g_cur_ctx && g_cur_ctx->group && g_cur_ctx->world > 1) group_mark_broken(g_cur_ctx->group);
+}
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 rnla_status guard(const std::function<void()>& f) {
+  g_cur_ctx = nullptr;
   try {
     f();
     return RNLA_OK;
@@ -35,15 +45,19 @@ rnla_status guard(const std::function<void()>& f) {
     return RNLA_ENUMERIC;
   } catch (const CudaError& e) {
     set_error(e.what());
+    break_group_on_failure();
     return RNLA_ECUDA;
   } catch (const NcclError& e) {
     set_error(e.what());
+    break_group_on_failure();
     return RNLA_ENCCL;
   } catch (const std::bad_alloc& e) {
     set_error("out of host memory");
+    break_group_on_failure();
     return RNLA_ENOMEM;
   } catch (const std::exception& e) {
     set_error(e.what());
+    break_group_on_failure();
     return RNLA_ECUDA;
   }
   }
@@ -74,6 +88,7 @@ StreamScope::~StreamScope() {
 
 void enter(rnla_ctx* ctx) {
   require(ctx != nullptr, "null rnla_ctx");
+  g_cur_ctx = ctx;
   RNLA_CUDA(cudaSetDevice(ctx->device));
 }
 

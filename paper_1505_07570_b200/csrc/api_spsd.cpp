@@ -268,6 +268,114 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// spsd_faster (src/spsd.cpp:131-168) on a KernelView (x = points) or a dense
+// SPSD K (dense_k): C = K[:, S] -> Q = thin_qr(C).Q; secondary rows P drawn
+// from the row leverage of Q (union S); Z = pinv(Q_P) K[P, P] pinv(Q_P)'.
+// The factorizations run in fp64 on the device; the draws on the host.
+template <class T>
+void spsd_faster_impl(rnla_ctx* ctx, const rnla_mat* x, bool dense_k, double sigma, int64_t s, int64_t p,
+                      uint64_t seed, const rnla_mat* q_out, const rnla_mat* z_out, int64_t* selected,
+                      int64_t* secondary, int64_t* n_secondary, int32_t* flagged) {
+  DevMat X = to_device(ctx, x);
+  const int64_t n = X.rows;
+  if (dense_k) require(X.rows == X.cols, "spsd_faster: K not square");
+  require(s >= 1 && s <= p && p <= n, "spsd_faster: need s <= p <= n");
+  // primary columns C = K[:, S], fp64 column-major n x s
+  DevBuf C64(sizeof(double) * n * s, ctx->stream), Ct(sizeof(T) * n * s, ctx->stream);
+  std::vector<int64_t> S;
+  if (!dense_k) {
+    Landmarks L = landmarks<T>(ctx, X, s, seed, n, 0);  // S from derive_seed(seed, 1) (src/spsd.cpp:136-137)
+    S = L.sel;
+    kernel_columns<T>(ctx, X, L, 0, n, sigma, Ct.as<T>(), 1, n);
+  } else {
+    S = sample_without_replacement_host(derive_seed(seed, 1), n, s);
+    DevBuf dS(sizeof(int64_t) * s, ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(dS.p, S.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    gather_columns<T>(ctx, n, s, X.as<T>(), X.rs, X.cs, dS.as<int64_t>(), nullptr, Ct.as<T>(), 1, n);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  if constexpr (std::is_same<T, double>::value)
+    RNLA_CUDA(cudaMemcpyAsync(C64.p, Ct.p, sizeof(double) * n * s, cudaMemcpyDeviceToDevice, ctx->stream));
+  else
+    copy2d_cast<float, double>(ctx, n, s, Ct.as<float>(), 1, n, C64.as<double>(), 1, n);
+  DevBuf R(sizeof(double) * s * s, ctx->stream);
+  thin_qr_dev(ctx, n, s, C64.as<double>(), R.as<double>());  // C64 <- Q
+  // secondary selection P (src/spsd.cpp:142-156)
+  std::vector<int64_t> P;
+  if (p == n) {
+    P.resize((size_t)n);
+    for (int64_t i = 0; i < n; ++i) P[(size_t)i] = i;
+  } else {
+    DevBuf lev(sizeof(double) * n, ctx->stream);
+    row_sqnorms<double>(ctx, n, s, C64.as<double>(), 1, n, lev.as<double>());
+    std::vector<double> h((size_t)n);
+    RNLA_CUDA(cudaMemcpyAsync(h.data(), lev.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    P = sample_with_replacement_host(derive_seed(seed, 2), h.data(), n, p);
+    P.insert(P.end(), S.begin(), S.end());  // sorted_union(p_idx, selected)
+    std::sort(P.begin(), P.end());
+    P.erase(std::unique(P.begin(), P.end()), P.end());
+  }
+  const int64_t np = (int64_t)P.size();
+  DevBuf dP(sizeof(int64_t) * np, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(dP.p, P.data(), sizeof(int64_t) * np, cudaMemcpyHostToDevice, ctx->stream));
+  // q_sub = Q[P, :] (np x s) and K_sub = K[P, P] (np x np), fp64 column-major
+  DevBuf qsub(sizeof(double) * np * s, ctx->stream), K64(sizeof(double) * np * np, ctx->stream),
+      Kt(sizeof(T) * np * np, ctx->stream);
+  gather_rows<double>(ctx, np, s, C64.as<double>(), 1, n, dP.as<int64_t>(), qsub.as<double>(), 1, np);
+  if (!dense_k) {
+    DevMat XP = alloc_dense(ctx, np, X.cols, true, X.dtype);
+    gather_rows<T>(ctx, np, X.cols, X.as<T>(), X.rs, X.cs, dP.as<int64_t>(), XP.as<T>(), XP.rs, XP.cs);
+    DevBuf sqP(sizeof(T) * np, ctx->stream), ident(sizeof(int64_t) * np, ctx->stream);
+    sq_norms<T>(ctx, np, X.cols, XP.as<T>(), XP.rs, XP.cs, nullptr, sqP.as<T>());
+    std::vector<int64_t> id((size_t)np);
+    for (int64_t i = 0; i < np; ++i) id[(size_t)i] = i;
+    RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * np, cudaMemcpyHostToDevice, ctx->stream));
+    rbf_block<T>(ctx, np, np, X.cols, XP.as<T>(), XP.rs, XP.cs, XP.as<T>(), XP.rs, XP.cs, nullptr, sqP.as<T>(),
+                 sqP.as<T>(), sigma, ident.as<int64_t>(), Kt.as<T>(), 1, np);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    DevBuf rowsP(sizeof(T) * np * n, ctx->stream);
+    gather_rows<T>(ctx, np, n, X.as<T>(), X.rs, X.cs, dP.as<int64_t>(), rowsP.as<T>(), 1, np);
+    gather_columns<T>(ctx, np, np, rowsP.as<T>(), 1, np, dP.as<int64_t>(), nullptr, Kt.as<T>(), 1, np);
+  }
+  if constexpr (std::is_same<T, double>::value)
+    RNLA_CUDA(cudaMemcpyAsync(K64.p, Kt.p, sizeof(double) * np * np, cudaMemcpyDeviceToDevice, ctx->stream));
+  else
+    copy2d_cast<float, double>(ctx, np, np, Kt.as<float>(), 1, np, K64.as<double>(), 1, np);
+  // rank probe (threshold 1e-10) and pinv(q_sub) (tol 1e-12) from one SVD
+  DevBuf Us(sizeof(double) * np * s, ctx->stream), Sv(sizeof(double) * s, ctx->stream),
+      Vs(sizeof(double) * s * s, ctx->stream), inv(sizeof(double) * s, ctx->stream),
+      Vi(sizeof(double) * s * s, ctx->stream), pinv(sizeof(double) * s * np, ctx->stream),
+      PK(sizeof(double) * s * np, ctx->stream), Z(sizeof(double) * s * s, ctx->stream),
+      Zs(sizeof(double) * s * s, ctx->stream);
+  svd_thin(ctx, np, s, qsub.as<double>(), 1, np, Us.as<double>(), Sv.as<double>(), Vs.as<double>());
+  std::vector<double> hs((size_t)s), hinv((size_t)s, 0.0);
+  RNLA_CUDA(cudaMemcpyAsync(hs.data(), Sv.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  int64_t rank = 0;
+  for (int64_t i = 0; i < s; ++i) {
+    if (hs[0] > 0.0 && hs[(size_t)i] > 1e-10 * hs[0]) ++rank;
+    if (hs[0] > 0.0 && hs[(size_t)i] > 1e-12 * hs[0]) hinv[(size_t)i] = 1.0 / hs[(size_t)i];
+  }
+  *flagged = rank < s ? 1 : 0;
+  RNLA_CUDA(cudaMemcpyAsync(inv.p, hinv.data(), sizeof(double) * s, cudaMemcpyHostToDevice, ctx->stream));
+  scale_cols_dev(ctx, s, s, Vs.as<double>(), inv.as<double>(), Vi.as<double>());
+  gemm<double>(ctx, s, np, s, 1.0, Vi.as<double>(), 1, s, Us.as<double>(), np, 1, 0.0, pinv.as<double>(), 1, s);
+  gemm<double>(ctx, s, np, np, 1.0, pinv.as<double>(), 1, s, K64.as<double>(), 1, np, 0.0, PK.as<double>(), 1, s);
+  gemm<double>(ctx, s, s, np, 1.0, PK.as<double>(), 1, s, pinv.as<double>(), s, 1, 0.0, Z.as<double>(), 1, s);
+  symmetrize(ctx, s, Z.as<double>(), Zs.as<double>());
+  OutMat qo(ctx, q_out, n, s, "spsd_faster: Q", false), zo(ctx, z_out, s, s, "spsd_faster: Z", false);
+  store_block(ctx, C64.as<double>(), n, s, n, qo);
+  store_block(ctx, Zs.as<double>(), s, s, s, zo);
+  qo.finish(ctx);
+  zo.finish(ctx);
+  std::copy(S.begin(), S.end(), selected);
+  std::copy(P.begin(), P.end(), secondary);
+  *n_secondary = np;
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 }  // namespace
 
 }  // namespace rnla
@@ -347,6 +455,37 @@ rnla_status rnla_nystrom_eig(rnla_ctx* ctx, const rnla_mat* x, double sigma, int
     require(k >= 1, "approx_eig: k > cols(L)");
     if (x->dtype == RNLA_F64) nystrom_eig_impl<double>(ctx, x, sigma, s, seed, target_k, k, u, lam, selected, kept);
     else nystrom_eig_impl<float>(ctx, x, sigma, s, seed, target_k, k, u, lam, selected, kept);
+  });
+}
+
+rnla_status rnla_spsd_faster(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, int64_t p, uint64_t seed,
+                             rnla_mat* q, rnla_mat* z, int64_t* selected, int64_t* secondary, int64_t* n_secondary,
+                             int32_t* flagged) {
+  return guard([&] {
+    enter(ctx);
+    require(sigma > 0.0, "KernelView: sigma <= 0");
+    check_mat(x, "spsd_faster: x");
+    require(ctx->world == 1, "spsd_faster: row-sharded contexts are not supported");
+    require(selected && secondary && n_secondary && flagged, "spsd_faster: null output");
+    if (x->dtype == RNLA_F64)
+      spsd_faster_impl<double>(ctx, x, false, sigma, s, p, seed, q, z, selected, secondary, n_secondary, flagged);
+    else
+      spsd_faster_impl<float>(ctx, x, false, sigma, s, p, seed, q, z, selected, secondary, n_secondary, flagged);
+  });
+}
+
+rnla_status rnla_spsd_faster_dense(rnla_ctx* ctx, const rnla_mat* k, int64_t s, int64_t p, uint64_t seed, rnla_mat* q,
+                                   rnla_mat* z, int64_t* selected, int64_t* secondary, int64_t* n_secondary,
+                                   int32_t* flagged) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(k, "spsd_faster: k");
+    require(ctx->world == 1, "spsd_faster: row-sharded contexts are not supported");
+    require(selected && secondary && n_secondary && flagged, "spsd_faster: null output");
+    if (k->dtype == RNLA_F64)
+      spsd_faster_impl<double>(ctx, k, true, 1.0, s, p, seed, q, z, selected, secondary, n_secondary, flagged);
+    else
+      spsd_faster_impl<float>(ctx, k, true, 1.0, s, p, seed, q, z, selected, secondary, n_secondary, flagged);
   });
 }
 

@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include "rnla_internal.h"
+#include "util.cuh"
 
 namespace rnla {
 
@@ -124,8 +125,7 @@ void launch_gather(rnla_ctx* ctx, const T* in, int64_t ld, const T* extra, int64
     const char* e = std::getenv("RNLA_CS_SMEM_KB");
     return e ? (size_t)std::atoi(e) * 1024 : (size_t)0;
   }();
-  if (pad) RNLA_CUDA(cudaFuncSetAttribute(cs_gather_kernel<T, TEAM, CPT, U>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pad));
+  if (pad) ensure_dyn_smem((const void*)cs_gather_kernel<T, TEAM, CPT, U>, pad);
   cs_gather_kernel<T, TEAM, CPT, U><<<grid, 128, pad, ctx->stream>>>(
       in, ld, extra, xs, L, Lo, plan.offsets.as<uint32_t>(), plan.rows.as<uint32_t>(), b0, b1, out, ldo, acc ? 1 : 0);
   RNLA_CUDA(cudaGetLastError());

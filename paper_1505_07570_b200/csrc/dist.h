@@ -16,6 +16,7 @@ double allreduce_scalar(rnla_ctx* ctx, double v);
 void allgather_blocks(rnla_ctx* ctx, const void* mine, void* all, size_t count, int dtype);
 rnla_group* group_create(int world);
 void group_destroy(rnla_group* g);
+void group_mark_broken(rnla_group* g);
 int group_world(const rnla_group* g);
 
 }  // namespace rnla

@@ -632,7 +632,7 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
   note_launch(ctx);
   const size_t smem = STAGES * STAGE + 1024 + 8 * (3 * STAGES + 5);
   auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES, DF, TMA_A>;
-  RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)kern, smem);
   dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)nblk, (unsigned)splits);
   CUtensorMap dummy{};
   kern<<<grid, TMA_A ? TC_THREADS + 32 : TC_THREADS, smem, ctx->stream>>>(

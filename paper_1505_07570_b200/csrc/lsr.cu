@@ -105,7 +105,7 @@ void launch_normal_gemv(rnla_ctx* ctx, int nblk, int64_t n, int64_t d, const T* 
                         int64_t b_stride, double beta, const double* w, double* g_part, double* rr_part) {
   const size_t smem = sizeof(double) * (size_t)(d + kWarps * d);
   auto k = normal_gemv_kernel<T, VPL>;
-  RNLA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   k<<<nblk, kWarps * 32, smem, ctx->stream>>>(A, ld, n, (int)d, b, b_stride, beta, w, g_part, rr_part);
   RNLA_CUDA(cudaGetLastError());
 }

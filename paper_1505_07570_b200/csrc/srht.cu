@@ -223,7 +223,7 @@ void launch_fwht_reg(rnla_ctx* ctx, dim3 grid, const T* src, int64_t ld, int64_t
                      double scale, T* out, int64_t out_rs, int64_t out_cs) {
   const size_t smem = fwht_reg_smem<T, LOGR, W, HI>();
   auto kern = fwht_reg_kernel<T, LOGR, W, HI>;
-  RNLA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)kern, smem);
   kern<<<grid, fwht_threads<T, LOGR, W>(), smem, ctx->stream>>>(src, ld, n, L, signs, qlo, c0, scratch, big_n, plan.grp_off.as<int32_t>(),
                                          plan.grp_t.as<int32_t>(), plan.grp_hi.as<int32_t>(), scale, out, out_rs,
                                          out_cs);
@@ -351,8 +351,8 @@ void srht_segments(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld,
   const double scale = 1.0 / std::sqrt((double)plan.s);
   const size_t smem_lo = sizeof(T) * ((size_t)1 << plan.qlo) * W;
   const size_t smem_hi = sizeof(T) * ((size_t)1 << plan.qhi) * W;
-  RNLA_CUDA(cudaFuncSetAttribute(srht_lo_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_lo));
-  RNLA_CUDA(cudaFuncSetAttribute(srht_hi_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_hi));
+  ensure_dyn_smem((const void*)srht_lo_kernel<T, W>, smem_lo);
+  ensure_dyn_smem((const void*)srht_hi_kernel<T, W>, smem_hi);
   for (int64_t t0 = 0; t0 < total_tiles; t0 += tiles_per_strip) {
     const int64_t nt = std::min(tiles_per_strip, total_tiles - t0);
     const int64_t c0 = t0 * W;

@@ -18,6 +18,7 @@
 
 #include "rnla_internal.h"
 #include "srht.h"
+#include "util.cuh"
 
 namespace rnla {
 
@@ -224,7 +225,7 @@ void launch_pass(rnla_ctx* ctx, dim3 grid, const CUtensorMap& src, const CUtenso
   constexpr int R = 1 << LOGR;
   const size_t smem = (size_t)R * TW * sizeof(float);
   auto k = fwht_tma_kernel<LOGR, HI>;
-  RNLA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   k<<<grid, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
                                         plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
                                         plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs);

@@ -56,6 +56,18 @@ __global__ void residual_sq_kernel(int64_t n, int64_t d, const T* __restrict__ A
 
 }  // namespace
 
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> cur;
+  int dev = 0;
+  RNLA_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[{kernel, dev}];
+  if (bytes <= c) return;
+  RNLA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  c = bytes;
+}
+
 int grid_for(rnla_ctx* ctx, int64_t work, int per_block) {
   const int64_t b = (work + per_block - 1) / per_block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx->num_sms * 16));

@@ -6,6 +6,11 @@ namespace rnla {
 
 int grid_for(rnla_ctx* ctx, int64_t work, int per_block);
 
+// Raise (never lower) a kernel's dynamic shared-memory limit on the current
+// device. The attribute is process-wide, so contexts launching the same kernel
+// from several host threads must not shrink it under each other.
+void ensure_dyn_smem(const void* kernel, size_t bytes);
+
 template <class S, class D>
 void copy2d_cast(rnla_ctx* ctx, int64_t rows, int64_t cols, const S* src, int64_t s_rs, int64_t s_cs, D* dst,
                  int64_t d_rs, int64_t d_cs);

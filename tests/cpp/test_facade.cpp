@@ -4,6 +4,7 @@
 // C++ facade include/randnla_b200/randnla.hpp, i.e. exactly how a reference
 // caller sees the B200 library. Built by tests/test_cpp_facade.py; exits
 // non-zero on the first failed CHECK.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -161,6 +162,15 @@ int main() {
     const DenseMatrix x = random_matrix(100, 5, 10);
     const NystromFactor nf = nystrom(x, KernelSpec{2.0}, 10, 11);
     CHECK(nf.L.cols() <= 8 && nf.L.rows() == 100 && nf.selected.size() == 10);
+  }
+  {  // faster SPSD: every primary index is in the secondary set (test_spsd.cpp:58-70)
+    const DenseMatrix x = random_matrix(120, 4, 4);
+    const SpsdSketch sk = spsd_faster(x, KernelSpec{1.5}, 10, 40, 6);
+    for (Index idx : sk.selected)
+      CHECK(std::find(sk.secondary.begin(), sk.secondary.end(), idx) != sk.secondary.end());
+    CHECK(sk.Q.rows() == 120 && sk.Q.cols() == 10 && sk.Z.rows() == 10);
+    for (Index i = 0; i < 10; ++i)
+      for (Index j = 0; j < 10; ++j) CHECK(sk.Z(i, j) == sk.Z(j, i));
   }
   std::printf("facade ok: %d checks\n", g_checks);
   return 0;

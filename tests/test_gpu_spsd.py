@@ -95,3 +95,46 @@ def test_nystrom_eig_fp32(ctx):
     L, _, _ = orc.nystrom(x.astype(np.float64), 6.0, 256, 3, 128)
     _, lo = orc.approx_eig(L, 16)
     assert np.max(np.abs(lam - lo) / lo) <= 1e-3
+
+
+def test_spsd_faster_entry_budget_and_error(ctx):
+    # tests/test_spsd.cpp:58-76
+    n, s, p = 120, 10, 40
+    x = orc.gaussian_matrix(n, 4, 4)
+    view = rn.KernelView(x, rn.KernelSpec(1.5))
+    sk = rn.spsd_faster(view, s, p, 6, ctx=ctx)
+    assert view.entries_evaluated() <= n * s + len(sk.secondary) ** 2
+    assert set(sk.selected.tolist()) <= set(sk.secondary.tolist())
+    k = orc.rbf_kernel(x, x, 1.5)
+    zb = sk.Q.T @ k @ sk.Q
+    best = np.linalg.norm(k - sk.Q @ zb @ sk.Q.T)
+    assert np.linalg.norm(k - sk.reconstruct()) <= 2.0 * best + 1e-12
+    assert np.array_equal(sk.Z, sk.Z.T)
+
+
+def test_spsd_faster_full_secondary_is_best_core(ctx):
+    # tests/test_spsd.cpp:78-85 (dense K)
+    x = orc.gaussian_matrix(50, 3, 5)
+    k = orc.rbf_kernel(x, x, 1.0)
+    sk = rn.spsd_faster(k, 8, 50, 7, ctx=ctx)
+    zb = sk.Q.T @ k @ sk.Q
+    assert np.linalg.norm(sk.Z - zb) <= 1e-8 * np.linalg.norm(zb)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_spsd_faster_matches_oracle(ctx, dtype):
+    rng = np.random.default_rng(9)
+    x = (rng.standard_normal((4000, 8)) * 1.5).astype(dtype)
+    sk = rn.spsd_faster(rn.KernelView(dev(x), rn.KernelSpec(2.5)), 60, 400, 31, ctx=ctx)
+    q, z, sel, sec, flagged = orc.spsd_faster(x.astype(np.float64), 2.5, 60, 400, 31)
+    assert np.array_equal(sk.selected, sel)
+    assert sk.flagged == flagged
+    Q = sk.Q.cpu().numpy()
+    tol = 1e-9 if dtype == np.float64 else 1e-4
+    assert np.max(np.abs(Q - q)) <= tol * 10
+    if dtype == np.float64:
+        # leverage draws are bit-exact given the scores; the scores agree to ~1e-15
+        assert np.array_equal(sk.secondary, sec)
+        assert np.linalg.norm(sk.Z - z) <= 1e-8 * np.linalg.norm(z)
+    with pytest.raises(ValueError, match="s <= p <= n"):
+        rn.spsd_faster(rn.KernelView(x, rn.KernelSpec(2.5)), 60, 50, 1, ctx=ctx)

@@ -262,3 +262,19 @@ def test_oracle_lsr_preconditioned_reference_properties():
         assert it <= 80
     with pytest.raises(ValueError):
         orc.lsr_preconditioned(a, b, 2.0, 1)
+
+
+def test_oracle_spsd_faster_reference_properties():
+    # tests/test_spsd.cpp:58-85 restated on the oracle
+    x = orc.gaussian_matrix(120, 4, 4)
+    q, z, sel, sec, flagged = orc.spsd_faster(x, 1.5, 10, 40, 6)
+    assert set(sel) <= set(sec)
+    k = orc.rbf_kernel(x, x, 1.5)
+    zb = q.T @ k @ q
+    best = np.linalg.norm(k - q @ zb @ q.T)
+    assert np.linalg.norm(k - q @ z @ q.T) <= 2.0 * best + 1e-12
+    x = orc.gaussian_matrix(50, 3, 5)
+    k = orc.rbf_kernel(x, x, 1.0)
+    q, z, _, _, _ = orc.spsd_faster(k, 1.0, 8, 50, 7, dense=True)
+    zb = q.T @ k @ q
+    assert np.linalg.norm(z - zb) <= 1e-8 * np.linalg.norm(zb)
