@@ -232,6 +232,32 @@ inline SvdFactors truncated_svd(const DenseMatrix& a, Index k) {
   return f;
 }
 
+inline SvdFactors condensed_svd(const DenseMatrix& a) {
+  const Index r = std::min(a.rows(), a.cols());
+  DenseMatrix u(a.rows(), r), v(a.cols(), r);
+  std::vector<double> sv(static_cast<size_t>(std::max<Index>(r, 1)));
+  Index rank = 0;
+  rnla_mat am = detail::view(a), um = detail::view(u), vm = detail::view(v);
+  detail::check(rnla_condensed_svd(detail::ctx(), &am, &um, sv.data(), &vm, &rank));
+  SvdFactors f;
+  f.U = DenseMatrix(a.rows(), rank);
+  f.V = DenseMatrix(a.cols(), rank);
+  f.singular_values = Vector(rank);
+  for (Index j = 0; j < rank; ++j) {
+    f.singular_values(j) = sv[static_cast<size_t>(j)];
+    for (Index i = 0; i < a.rows(); ++i) f.U(i, j) = u(i, j);
+    for (Index i = 0; i < a.cols(); ++i) f.V(i, j) = v(i, j);
+  }
+  return f;
+}
+
+inline DenseMatrix pseudo_inverse(const DenseMatrix& a, double tol = 1e-12) {
+  DenseMatrix p(a.cols(), a.rows());
+  rnla_mat am = detail::view(a), pm = detail::view(p);
+  detail::check(rnla_pseudo_inverse(detail::ctx(), &am, tol, &pm));
+  return p;
+}
+
 // ---------------- randsvd.hpp ----------------
 struct KsvdResult {
   SvdFactors factors;
@@ -312,6 +338,38 @@ inline LsrSolution lsr_sketched(const DenseMatrix& a, const Vector& b, const Ske
   rnla_sketch_spec cs = spec.to_c();
   detail::check(rnla_lsr_sketched(detail::ctx(), &am, &bm, &cs, sol.x.data(), &sol.objective, &flagged));
   sol.flagged = flagged != 0;
+  return sol;
+}
+
+// regression.hpp:20-27: x = A^+ b (objective on the host).
+inline LsrSolution lsr_exact(const DenseMatrix& a, const Vector& b) {
+  if (a.rows() < a.cols()) throw std::invalid_argument("lsr_exact: n < d");
+  if (a.rows() != b.size()) throw std::invalid_argument("lsr_exact: dimension mismatch");
+  const DenseMatrix p = pseudo_inverse(a);
+  LsrSolution sol;
+  sol.x = Vector(a.cols());
+  for (Index j = 0; j < a.cols(); ++j) {
+    double s = 0.0;
+    for (Index i = 0; i < a.rows(); ++i) s += p(j, i) * b(i);
+    sol.x(j) = s;
+  }
+  for (Index i = 0; i < a.rows(); ++i) {
+    double r = -b(i);
+    for (Index j = 0; j < a.cols(); ++j) r += a(i, j) * sol.x(j);
+    sol.objective += r * r;
+  }
+  return sol;
+}
+
+inline LsrSolution lsr_cg(const DenseMatrix& a, const Vector& b, double tol, int maxit) {
+  if (a.rows() < a.cols()) throw std::invalid_argument("lsr_cg: n < d");
+  LsrSolution sol;
+  sol.x = Vector(a.cols());
+  int32_t it = 0, conv = 0;
+  rnla_mat am = detail::view(a), bm = detail::view(b);
+  detail::check(rnla_lsr_cg(detail::ctx(), &am, &bm, tol, maxit, sol.x.data(), &sol.objective, &it, &conv));
+  sol.iterations = it;
+  sol.converged = conv != 0;
   return sol;
 }
 

@@ -226,6 +226,12 @@ rnla_status rnla_lsr_sketched(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* 
  * objective |Ax - b|^2 and kappa(A R_Y^-1) are skipped when their pointers
  * are NULL. Each iteration is one fused pass over A: A'(b - A T z). d <= 1024.
  * RNLA_ENUMERIC when the sketched matrix is singular twice. */
+/* lsr_cg, regression.hpp:24-27 (src/regression.cpp:38-66): CG on the normal
+ * equations, converged when |A'(Ax - b)| <= tol |A'b|; each iteration is one
+ * fused pass over A. x[d]; objective (nullable) = |Ax - b|^2; *converged
+ * (nullable). d <= 1024. */
+rnla_status rnla_lsr_cg(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b, double tol, int32_t maxit, double* x,
+                        double* objective, int32_t* iterations, int32_t* converged);
 rnla_status rnla_lsr_preconditioned(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b, double eps, uint64_t seed,
                                     int64_t sketch_size, int32_t use_cg, int32_t sketch_kind, double* x,
                                     double* objective, int32_t* iterations, double* kappa_estimate);

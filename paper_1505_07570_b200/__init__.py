@@ -31,7 +31,7 @@ __all__ = [
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
     "count_sketch", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
     "leverage_sample_columns", "leverage_sample_rows", "thin_qr", "condensed_svd", "truncated_svd",
-    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig", "SpsdSketch", "spsd_faster",
+    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_cg", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig", "SpsdSketch", "spsd_faster",
     "shard_rows",
 ]
 
@@ -607,6 +607,19 @@ def lsr_sketched(a, b, spec: SketchSpec, ctx: Optional[Context] = None) -> LsrSo
     _check(_abi.lib().rnla_lsr_sketched(_ctx(ctx).handle, C.byref(am), C.byref(bm), C.byref(cs),
                                         x.ctypes.data_as(_abi._F64P), C.byref(obj), C.byref(flagged)))
     return LsrSolution(x=x, objective=float(obj.value), flagged=bool(flagged.value))
+
+
+def lsr_cg(a, b, tol: float, maxit: int, ctx: Optional[Context] = None) -> LsrSolution:
+    """CG on the normal equations (src/regression.cpp:38-66), one fused pass over A per iteration."""
+    a2 = _as2d(a)
+    b2 = _as2d(b)
+    x = np.empty(a2.shape[1], dtype=np.float64)
+    obj = C.c_double()
+    it, conv = C.c_int32(), C.c_int32()
+    am, bm = _mat(a2), _mat(b2)
+    _check(_abi.lib().rnla_lsr_cg(_ctx(ctx).handle, C.byref(am), C.byref(bm), float(tol), int(maxit),
+                                  x.ctypes.data_as(_abi._F64P), C.byref(obj), C.byref(it), C.byref(conv)))
+    return LsrSolution(x=x, objective=float(obj.value), iterations=int(it.value), converged=bool(conv.value))
 
 
 @dataclasses.dataclass(frozen=True)

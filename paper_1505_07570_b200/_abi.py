@@ -95,6 +95,7 @@ SIGNATURES = {
     "rnla_faster_ksvd": (
         C.c_int, [_P, _M, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, _M, _F64P, _M, _I64P, _I32P, _F64P]),
     "rnla_lsr_sketched": (C.c_int, [_P, _M, _M, _S, _F64P, _F64P, _I32P]),
+    "rnla_lsr_cg": (C.c_int, [_P, _M, _M, C.c_double, C.c_int32, _F64P, _F64P, _I32P, _I32P]),
     "rnla_lsr_preconditioned": (
         C.c_int, [_P, _M, _M, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _F64P, _F64P, _I32P, _F64P]),
     "rnla_rbf_kernel": (C.c_int, [_P, _M, _M, C.c_double, _M]),

@@ -213,9 +213,69 @@ void lsr_preconditioned_impl(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b
   }
 }
 
+// lsr_cg (src/regression.cpp:38-66): CG on A'A x = A'b; every iteration's
+// A'(A p) is one fused pass (beta = 0 gives -A'A p).
+template <class T>
+void lsr_cg_impl(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b, double tol, int32_t maxit, double* x_out,
+                 double* objective, int32_t* iterations, int32_t* converged) {
+  const int64_t n = a->rows, d = a->cols;
+  int64_t total = n;
+  global_row_offset(ctx, n, &total);
+  require(total >= d, "lsr_cg: n < d");
+  DevMat A = as_rowmajor(ctx, to_device(ctx, a));
+  DevMat B = to_device(ctx, b);
+  Pass<T> pass(ctx, A, B.as<T>(), B.rs);
+  HVec x((size_t)d, 0.0);
+  HVec r = pass(1.0, x);  // A'b
+  const double target = tol * norm2(r);
+  HVec p = r;
+  double rs = dot(r, r);
+  int it = 0;
+  bool conv = std::sqrt(rs) <= target;
+  while (it < maxit && std::sqrt(rs) > target) {
+    HVec ap = pass(0.0, p);
+    for (auto& v : ap) v = -v;
+    const double alpha = rs / dot(p, ap);
+    for (int64_t i = 0; i < d; ++i) {
+      x[(size_t)i] += alpha * p[(size_t)i];
+      r[(size_t)i] -= alpha * ap[(size_t)i];
+    }
+    const double rs_new = dot(r, r);
+    for (int64_t i = 0; i < d; ++i) p[(size_t)i] = r[(size_t)i] + (rs_new / rs) * p[(size_t)i];
+    rs = rs_new;
+    ++it;
+    conv = std::sqrt(rs) <= target;
+  }
+  std::copy(x.begin(), x.end(), x_out);
+  *iterations = it;
+  if (converged) *converged = conv ? 1 : 0;
+  if (objective) {
+    double r2 = 0.0;
+    pass(1.0, x, &r2);
+    *objective = r2;
+  }
+}
+
 }  // namespace
 
 }  // namespace rnla
+
+using namespace rnla;
+
+extern "C" rnla_status rnla_lsr_cg(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b, double tol, int32_t maxit,
+                                   double* x, double* objective, int32_t* iterations, int32_t* converged) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(a, "lsr_cg: a");
+    check_mat(b, "lsr_cg: b");
+    require(a->rows == b->rows && b->cols == 1, "lsr_cg: dimension mismatch");
+    require(a->dtype == b->dtype, "lsr_cg: a and b dtypes differ");
+    require(x != nullptr && iterations != nullptr, "lsr_cg: null output");
+    require(normal_gemv_supported(a->cols), "lsr_cg: d above 1024 is not supported");
+    if (a->dtype == RNLA_F64) lsr_cg_impl<double>(ctx, a, b, tol, maxit, x, objective, iterations, converged);
+    else lsr_cg_impl<float>(ctx, a, b, tol, maxit, x, objective, iterations, converged);
+  });
+}
 
 using namespace rnla;
 

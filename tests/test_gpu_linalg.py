@@ -235,3 +235,16 @@ def test_lsr_preconditioned_large_d_fused_pass(ctx):
     r = a @ exact - b
     assert abs(sol.objective - r @ r) <= 1e-10 * (r @ r)
     assert sol.kappa_estimate is None
+
+
+def test_lsr_cg_converges_to_exact(ctx):
+    # tests/test_regression.cpp:34-42
+    a = orc.gaussian_matrix(100, 10, 3)
+    b = orc.gaussian_matrix(100, 1, 4)[:, 0]
+    exact = np.linalg.lstsq(a, b, rcond=None)[0]
+    cg = rn.lsr_cg(a, b, 1e-12, 200, ctx=ctx)
+    assert cg.converged
+    assert np.linalg.norm(cg.x - exact) <= 1e-8 * np.linalg.norm(exact)
+    assert cg.iterations <= 11
+    r = a @ exact - b
+    assert abs(cg.objective - r @ r) <= 1e-10 * (r @ r)
