@@ -53,26 +53,28 @@ struct TileLoader {
       As[i][p] = (TS)regs[r];
     }
   }
-  // B element (p, j) at B[p*rs + j*cs]; smem holds Bs[j][p].
+  // B element (p, j) at B[p*rs + j*cs]; smem holds Bs[j][p]. NB = tile width (64 or 32).
+  template <int NB = BN>
   __device__ __forceinline__ void load_b(const T* B, int64_t rs, int64_t cs, int64_t kdim, int64_t n, int64_t k0,
                                          int64_t n0, int tid) {
     const bool kcontig = (rs == 1 && cs != 1);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < NB * BK / THREADS; ++r) {
       const int idx = tid + THREADS * r;
-      const int j = kcontig ? idx / BK : idx % BN;
-      const int p = kcontig ? idx % BK : idx / BN;
+      const int j = kcontig ? idx / BK : idx % NB;
+      const int p = kcontig ? idx % BK : idx / NB;
       const int64_t gj = n0 + j, gp = k0 + p;
       regs[r] = (gj < n && gp < kdim) ? B[gp * rs + gj * cs] : T(0);
     }
   }
+  template <int NB = BN>
   __device__ __forceinline__ void store_b(TS (*Bs)[BK + PAD], int64_t rs, int64_t cs, int tid) {
     const bool kcontig = (rs == 1 && cs != 1);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < NB * BK / THREADS; ++r) {
       const int idx = tid + THREADS * r;
-      const int j = kcontig ? idx / BK : idx % BN;
-      const int p = kcontig ? idx % BK : idx / BN;
+      const int j = kcontig ? idx / BK : idx % NB;
+      const int p = kcontig ? idx % BK : idx / NB;
       Bs[j][p] = (TS)regs[r];
     }
   }
@@ -81,73 +83,76 @@ struct TileLoader {
 // grid: (ceil(n/BN), ceil(m/BM), splits). Writes alpha*acc + beta*C when
 // ws == nullptr, else the raw partial to ws[z*m*n + i*n + j]. TI = input
 // element type (float inputs are widened exactly to fp64 on the way to smem).
-template <class TI>
+// NB = 64: 2 x 2 warps of 32 x 32; NB = 32 (narrow outputs such as the
+// s = 30 sketches of config 0): 4 x 1 warps of 16 x 32, so no half-empty tiles.
+template <class TI, int NB = BN>
 __global__ void __launch_bounds__(THREADS) gemm_f64_dmma(int64_t m, int64_t n, int64_t kdim, int64_t kchunk,
                                                          double alpha, const TI* __restrict__ A, int64_t a_rs,
                                                          int64_t a_cs, const TI* __restrict__ B, int64_t b_rs,
                                                          int64_t b_cs, double beta, double* C, int64_t c_rs,
                                                          int64_t c_cs, double* ws, int sym_upper) {
+  constexpr int WN = NB == 64 ? 2 : 1, MI = NB == 64 ? 4 : 2, NI = 4;
   // sym_upper: C is symmetric (A = B'); tiles strictly below the diagonal are
   // skipped and mirrored afterwards (half the Gram flops).
   if (sym_upper && blockIdx.y > blockIdx.x) return;
   __shared__ __align__(16) double As[2][BM][BK + PAD];
-  __shared__ __align__(16) double Bs[2][BN][BK + PAD];
+  __shared__ __align__(16) double Bs[2][NB][BK + PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / WN, wn = warp % WN;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * NB;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = min(kdim, kbeg + kchunk);
 
-  double acc[4][4][2];
+  double acc[MI][NI][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < MI; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   TileLoader<TI, double> la, lb;
   int buf = 0;
   if (kbeg < kend) {
     la.load_a(A, a_rs, a_cs, m, kend, m0, kbeg, tid);
-    lb.load_b(B, b_rs, b_cs, kend, n, kbeg, n0, tid);
+    lb.template load_b<NB>(B, b_rs, b_cs, kend, n, kbeg, n0, tid);
     la.store_a(As[0], a_rs, a_cs, tid);
-    lb.store_b(Bs[0], b_rs, b_cs, tid);
+    lb.template store_b<NB>(Bs[0], b_rs, b_cs, tid);
   }
   __syncthreads();
   for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
     const bool more = k0 + BK < kend;
     if (more) {
       la.load_a(A, a_rs, a_cs, m, kend, m0, k0 + BK, tid);
-      lb.load_b(B, b_rs, b_cs, kend, n, k0 + BK, n0, tid);
+      lb.template load_b<NB>(B, b_rs, b_cs, kend, n, k0 + BK, n0, tid);
     }
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[MI], bf[NI];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = As[buf][wm * 32 + mi * 8 + g][kk + t];
+      for (int mi = 0; mi < MI; ++mi) af[mi] = As[buf][wm * (MI * 8) + mi * 8 + g][kk + t];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[buf][wn * 32 + ni * 8 + g][kk + t];
+      for (int ni = 0; ni < NI; ++ni) bf[ni] = Bs[buf][wn * (NI * 8) + ni * 8 + g][kk + t];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
     if (more) {
       la.store_a(As[buf ^ 1], a_rs, a_cs, tid);
-      lb.store_b(Bs[buf ^ 1], b_rs, b_cs, tid);
+      lb.template store_b<NB>(Bs[buf ^ 1], b_rs, b_cs, tid);
     }
     __syncthreads();
     buf ^= 1;
   }
 
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t i = m0 + wm * 32 + mi * 8 + g;
-        const int64_t j = n0 + wn * 32 + ni * 8 + 2 * t + h;
+        const int64_t i = m0 + wm * (MI * 8) + mi * 8 + g;
+        const int64_t j = n0 + wn * (NI * 8) + ni * 8 + 2 * t + h;
         if (i < m && j < n) {
           if (ws) {
             ws[(int64_t)blockIdx.z * m * n + i * n + j] = acc[mi][ni][h];
@@ -262,7 +267,9 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
       return;
     }
   }
-  const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  // narrow outputs (n mod 64 in 1..32) use 32-wide tiles for the fp64 kernel
+  const int nb = (std::is_same<T, double>::value && ((n % 64) != 0) && ((n % 64) <= 32)) ? 32 : BN;
+  const int64_t tiles = ((m + BM - 1) / BM) * ((n + nb - 1) / nb);
   // Split K until there are ~4 CTAs per SM, keeping >= 256 k per split.
   int64_t splits = 1;
   const int64_t want = (int64_t)ctx->num_sms * 4;
@@ -281,10 +288,14 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
     ws = DevBuf(sizeof(T) * (size_t)(splits * m * n), ctx->stream);
     wsp = ws.as<T>();
   }
-  dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
+  dim3 grid((unsigned)((n + nb - 1) / nb), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
   if constexpr (std::is_same<T, double>::value) {
-    gemm_f64_dmma<double><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C,
-                                                    c_rs, c_cs, wsp, 0);
+    if (nb == 32)
+      gemm_f64_dmma<double, 32><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs,
+                                                                   b_cs, beta, C, c_rs, c_cs, wsp, 0);
+    else
+      gemm_f64_dmma<double><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs,
+                                                               beta, C, c_rs, c_cs, wsp, 0);
   } else {
     gemm_f32_simt<<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C,
                                                     c_rs, c_cs, wsp);
