@@ -57,6 +57,15 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
                                             uint64_t pol) {
   asm volatile(
@@ -80,45 +89,35 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                : "memory");
 }
 
-// LOGR = log2 of the rows per tile (9 or 10); R/2 threads.
+// One tile issue (thread 0): the TMA boxes of task (bx, tile) into `sm`, completing on `bar`.
 template <int LOGR, bool HI>
-__global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_kernel(
-    const __grid_constant__ CUtensorMap src_map, const __grid_constant__ CUtensorMap dst_map,
-    const int8_t* __restrict__ signs, int64_t n, int qlo, int64_t big_n, int64_t L, int64_t c0,
-    const int32_t* __restrict__ grp_off, const int32_t* __restrict__ grp_t, const int32_t* __restrict__ grp_hi,
-    float scale, float* __restrict__ out, int64_t out_rs, int64_t out_cs) {
+__device__ __forceinline__ void fwht_issue(float* sm, uint64_t* bar, const CUtensorMap* src_map, int bx, int tile,
+                                           int qlo, int64_t big_n, int64_t c0) {
+  constexpr int R = 1 << LOGR;
+  mbar_expect(su32(bar), R * TW * 4);
+  const uint64_t pol = policy_evict_first();
+  for (int b = 0; b < R / 256; ++b) {
+    const uint32_t dst = su32(sm + b * 256 * TW);
+    if (HI)  // scratch viewed as [jh][il][TW] per strip: rows jh = b*256.. of this il
+      tma_load_3d(dst, src_map, 0, bx, tile * (int)(big_n >> qlo) + b * 256, su32(bar), pol);
+    else  // input A (row-major n x L): columns c0 + tile*16.., rows bx*R + b*256..
+      tma_load_2d(dst, src_map, (int)(c0 + tile * TW), bx * R + b * 256, su32(bar), pol);
+  }
+}
+
+// The transform of one landed tile (all R/2 threads): phases A and B, then the
+// low pass stores the tile to the scratch (TMA) and the high pass writes the
+// sampled outputs. Ends with the tile buffer free again.
+template <int LOGR, bool HI>
+__device__ __forceinline__ void fwht_tile(float* sm, int bx, int tile, int g0, int g1, const CUtensorMap* dst_map,
+                                          const int8_t* __restrict__ signs, int64_t n, int64_t big_n, int64_t L,
+                                          int64_t c0, const int32_t* __restrict__ grp_t,
+                                          const int32_t* __restrict__ grp_hi, float scale, float* __restrict__ out,
+                                          int64_t out_rs, int64_t out_cs) {
   constexpr int R = 1 << LOGR;
   constexpr int G = R / 64;  // rows per phase-B group
   constexpr int NT = R / 2;
-  extern __shared__ __align__(128) float sm[];  // [R][TW], dense (TMA box layout)
-  __shared__ __align__(8) uint64_t bar;
-  const int bx = HI ? blockIdx.x : blockIdx.y;   // HI: il; LO: row block
-  const int tile = HI ? blockIdx.y : blockIdx.x;  // column tile within the strip
-  int g0 = 0, g1 = 0;
-  if (HI) {
-    g0 = grp_off[bx];
-    g1 = grp_off[bx + 1];
-    if (g0 == g1) return;  // no sampled output has these low bits (uniform per CTA)
-  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    mbar_init1(su32(&bar));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    mbar_expect(su32(&bar), R * TW * 4);
-    const uint64_t pol = policy_evict_first();
-    for (int b = 0; b < R / 256; ++b) {
-      const uint32_t dst = su32(sm + b * 256 * TW);
-      if (HI)  // scratch viewed as [jh][il][TW] per strip: rows jh = b*256.. of this il
-        tma_load_3d(dst, &src_map, 0, bx, tile * (int)(big_n >> qlo) + b * 256, su32(&bar), pol);
-      else  // input A (row-major n x L): columns c0 + tile*16.., rows bx*R + b*256..
-        tma_load_2d(dst, &src_map, (int)(c0 + tile * TW), bx * R + b * 256, su32(&bar), pol);
-    }
-  }
-  mbar_wait0(su32(&bar));
-
   // ---- phase A ----
   const int p = lane >> 4, c = lane & 15;
   float v[32];
@@ -179,7 +178,7 @@ __global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_
     if (tid == 0) {
       const uint64_t pol = policy_evict_last();
       for (int b = 0; b < R / 256; ++b)
-        tma_store_2d(&dst_map, 0, (int)(tile * big_n + rbase + b * 256), su32(sm + b * 256 * TW), pol);
+        tma_store_2d(dst_map, 0, (int)(tile * big_n + rbase + b * 256), su32(sm + b * 256 * TW), pol);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
@@ -191,6 +190,87 @@ __global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_
       const int64_t col = col_base + cc;
       if (col < L) out[(int64_t)grp_t[g] * out_rs + col * out_cs] = sm[grp_hi[g] * TW + cc] * scale;
     }
+    __syncthreads();
+  }
+}
+
+// LOGR = log2 of the rows per tile (9 or 10); R/2 threads; one tile per CTA.
+template <int LOGR, bool HI>
+__global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_kernel(
+    const __grid_constant__ CUtensorMap src_map, const __grid_constant__ CUtensorMap dst_map,
+    const int8_t* __restrict__ signs, int64_t n, int qlo, int64_t big_n, int64_t L, int64_t c0,
+    const int32_t* __restrict__ grp_off, const int32_t* __restrict__ grp_t, const int32_t* __restrict__ grp_hi,
+    float scale, float* __restrict__ out, int64_t out_rs, int64_t out_cs) {
+  extern __shared__ __align__(128) float sm[];  // [R][TW], dense (TMA box layout)
+  __shared__ __align__(8) uint64_t bar;
+  const int bx = HI ? blockIdx.x : blockIdx.y;   // HI: il; LO: row block
+  const int tile = HI ? blockIdx.y : blockIdx.x;  // column tile within the strip
+  int g0 = 0, g1 = 0;
+  if (HI) {
+    g0 = grp_off[bx];
+    g1 = grp_off[bx + 1];
+    if (g0 == g1) return;  // no sampled output has these low bits (uniform per CTA)
+  }
+  if (threadIdx.x == 0) {
+    mbar_init1(su32(&bar));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) fwht_issue<LOGR, HI>(sm, &bar, &src_map, bx, tile, qlo, big_n, c0);
+  mbar_wait0(su32(&bar));
+  fwht_tile<LOGR, HI>(sm, bx, tile, g0, g1, &dst_map, signs, n, big_n, L, c0, grp_t, grp_hi, scale, out, out_rs,
+                      out_cs);
+}
+
+// Persistent, double-buffered form: each CTA walks tasks blockIdx.x, +gridDim.x, ...
+// (task = x + gx * y; LO: x = column tile, y = row block; HI: x = il, y = tile) and
+// lands the NEXT task's tile by TMA while it transforms the current one.
+template <int LOGR, bool HI>
+__global__ void __launch_bounds__((1 << LOGR) / 2, 1) fwht_tma_persist(
+    const __grid_constant__ CUtensorMap src_map, const __grid_constant__ CUtensorMap dst_map,
+    const int8_t* __restrict__ signs, int64_t n, int qlo, int64_t big_n, int64_t L, int64_t c0,
+    const int32_t* __restrict__ grp_off, const int32_t* __restrict__ grp_t, const int32_t* __restrict__ grp_hi,
+    float scale, float* __restrict__ out, int64_t out_rs, int64_t out_cs, int gx, int gy) {
+  constexpr int R = 1 << LOGR;
+  extern __shared__ __align__(128) float smem[];  // two [R][TW] tile buffers
+  __shared__ __align__(8) uint64_t bars[2];
+  const int tasks = gx * gy;
+  auto live = [&](int task) {
+    if (!HI) return true;
+    const int il = task % gx;
+    return grp_off[il] != grp_off[il + 1];
+  };
+  auto next_live = [&](int task) {
+    while (task < tasks && !live(task)) task += gridDim.x;
+    return task;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init1(su32(&bars[0]));
+    mbar_init1(su32(&bars[1]));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int task, int b) {
+    const int x = task % gx, y = task / gx;
+    const int bx = HI ? x : y, tile = HI ? y : x;
+    fwht_issue<LOGR, HI>(smem + b * R * TW, &bars[b], &src_map, bx, tile, qlo, big_n, c0);
+  };
+  int cur = next_live((int)blockIdx.x);
+  if (cur < tasks && threadIdx.x == 0) issue(cur, 0);
+  uint32_t phase = 0;  // bit b: parity of the next completion of bars[b]
+  int b = 0;
+  while (cur < tasks) {
+    const int nxt = next_live(cur + (int)gridDim.x);
+    if (nxt < tasks && threadIdx.x == 0) issue(nxt, b ^ 1);  // buffer b^1 was released at the end of the last task
+    mbar_wait_parity(su32(&bars[b]), (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const int x = cur % gx, y = cur / gx;
+    const int bx = HI ? x : y, tile = HI ? y : x;
+    const int g0 = HI ? grp_off[bx] : 0, g1 = HI ? grp_off[bx + 1] : 0;
+    fwht_tile<LOGR, HI>(smem + b * R * TW, bx, tile, g0, g1, &dst_map, signs, n, big_n, L, c0, grp_t, grp_hi, scale,
+                        out, out_rs, out_cs);
+    cur = nxt;
+    b ^= 1;
   }
 }
 
@@ -223,12 +303,31 @@ template <int LOGR, bool HI>
 void launch_pass(rnla_ctx* ctx, dim3 grid, const CUtensorMap& src, const CUtensorMap& dst, const SrhtPlan& plan,
                  int64_t L, int64_t c0, float scale, float* out, int64_t out_rs, int64_t out_cs) {
   constexpr int R = 1 << LOGR;
-  const size_t smem = (size_t)R * TW * sizeof(float);
-  auto k = fwht_tma_kernel<LOGR, HI>;
-  ensure_dyn_smem((const void*)k, smem);
-  k<<<grid, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
-                                        plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
-                                        plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs);
+  // The persistent double-buffered form (RNLA_SRHT_PERSIST=1) measured slower on config 2
+  // (3.25 vs 2.60 ms): one 512-thread CTA per SM keeps fewer tiles in flight than three
+  // one-shot CTAs, so one tile per CTA stays the default.
+  static const bool one_shot = std::getenv("RNLA_SRHT_PERSIST") == nullptr;
+  if (one_shot) {
+    const size_t smem = (size_t)R * TW * sizeof(float);
+    auto k = fwht_tma_kernel<LOGR, HI>;
+    ensure_dyn_smem((const void*)k, smem);
+    k<<<grid, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
+                                          plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
+                                          plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs);
+  } else {
+    // persistent, double-buffered: two tiles per CTA, as many CTAs as fit
+    const size_t smem = 2 * (size_t)R * TW * sizeof(float);
+    auto k = fwht_tma_persist<LOGR, HI>;
+    ensure_dyn_smem((const void*)k, smem);
+    int per_sm = 1;
+    RNLA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, R / 2, smem));
+    const int64_t tasks = (int64_t)grid.x * grid.y;
+    const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(tasks, (int64_t)ctx->num_sms * std::max(1, per_sm)));
+    k<<<ctas, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
+                                          plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
+                                          plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs, (int)grid.x,
+                                          (int)grid.y);
+  }
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
