@@ -317,12 +317,23 @@ template <bool KCONTIG, int NS>
 __device__ __forceinline__ void convert_tile_inplace(uint8_t* base, int gtid, int grp) {
   constexpr int UPT = (TC_BM * 8) / TC_GROUP;
   constexpr int A_TILE = TC_BM * 128;
+  // K-contiguous tiles: each 8-lane phase takes one 16-B chunk index q of 8
+  // consecutive rows, whose SW128 positions (q ^ (r & 7)) are all distinct, so
+  // both the swizzled fp32 reads and the bf16 writes are bank-conflict free.
+  auto coords = [](int u, int& r, int& q) {
+    if (KCONTIG) {
+      r = (u & 7) + 8 * (u >> 6);
+      q = (u >> 3) & 7;
+    } else {
+      unit_coords<false>(u, TC_BM, r, q);
+    }
+  };
   float f[UPT][8];
 #pragma unroll
   for (int i = 0; i < UPT; ++i) {
     const int u = gtid + i * TC_GROUP;
     int r, q;
-    unit_coords<KCONTIG>(u, TC_BM, r, q);
+    coords(u, r, q);
     if (KCONTIG) {
       const uint8_t* row = base + (q >> 2) * (A_TILE) + r * 128;
       const int g0 = (q & 3) * 2;
@@ -341,7 +352,7 @@ __device__ __forceinline__ void convert_tile_inplace(uint8_t* base, int gtid, in
   for (int i = 0; i < UPT; ++i) {
     const int u = gtid + i * TC_GROUP;
     int r, q;
-    unit_coords<KCONTIG>(u, TC_BM, r, q);
+    coords(u, r, q);
     uint4 pc[NS];
     split8n<NS>(f[i], pc);
     const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
@@ -699,10 +710,10 @@ EncodeTiledFn encode_tiled() {
 }
 
 bool make_a_map(CUtensorMap* map, const float* A, int64_t m, int64_t k, int64_t a_rs, int64_t a_cs) {
-  // Opt-in (RNLA_TC_TMA=1): measured 38.1 vs 38.6 ms on config 3 (the A path
-  // is not latency-bound), and one full-suite run stalled once with it on, so
-  // the register-staged loader stays the default until that is understood.
-  static const bool off = std::getenv("RNLA_TC_TMA") == nullptr || std::getenv("RNLA_TC_NO_TMA") != nullptr;
+  // Default on (RNLA_TC_NO_TMA=1 falls back to the register-staged loader):
+  // config 3 37.5 vs 38.8 ms once the converter's 8-lane phases read one chunk
+  // of 8 consecutive rows (conflict-free SW128 reads and writes).
+  static const bool off = std::getenv("RNLA_TC_NO_TMA") != nullptr;
   if (off || !encode_tiled() || (reinterpret_cast<uintptr_t>(A) & 15) || m >= INT32_MAX || k >= INT32_MAX) return false;
   const cuuint32_t es[2] = {1, 1};
   CUresult r;
