@@ -398,7 +398,10 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   static_assert(TCOLS <= 512, "BN too large for promoted accumulation");
   constexpr uint32_t TMEM_COLS = TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment of the shared-window offset by pointer arithmetic on the
+  // __shared__ array (an integer round trip would turn every tile access into
+  // a generic LD.E/ST.E instead of LDS/STS).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // full[S], empty[S], xfull[2], xfree[2], tfull[S] (TMA_A: the A tile and B image landed)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* tfull = bars + 2 * STAGES + 4;
