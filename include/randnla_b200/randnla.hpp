@@ -459,6 +459,41 @@ inline SpsdSketch spsd_faster_call(const DenseMatrix& x, const KernelSpec* spec,
 }
 }  // namespace detail
 
+// ---------------- cur.hpp (kernel-lazy faster CUR) ----------------
+struct CurFactors {
+  DenseMatrix C, U, R;
+  std::vector<Index> col_indices, row_indices, secondary_rows, secondary_cols;
+  long entries_visited = 0;
+  bool flagged = false;
+};
+
+// cur.hpp:44-52 (src/cur.cpp:188-212).
+inline CurFactors cur_faster_kernel(const DenseMatrix& xtest, const DenseMatrix& xtrain, double sigma, Index c,
+                                    Index r, std::uint64_t seed) {
+  const Index m = xtest.rows(), n = xtrain.rows(), p = 2 * (c + r);
+  CurFactors f;
+  f.C = DenseMatrix(m, c);
+  f.U = DenseMatrix(c, r);
+  f.R = DenseMatrix(r, n);
+  f.col_indices.resize(static_cast<size_t>(std::max<Index>(c, 0)));
+  f.row_indices.resize(static_cast<size_t>(std::max<Index>(r, 0)));
+  std::vector<Index> sr(static_cast<size_t>(std::max<Index>(1, std::min(m, p + r)))),
+      sc(static_cast<size_t>(std::max<Index>(1, std::min(n, p + c))));
+  Index nsr = 0, nsc = 0, ent = 0;
+  int32_t flagged = 0;
+  rnla_mat a = detail::view(xtest), b = detail::view(xtrain), cm = detail::view(f.C), um = detail::view(f.U),
+           rm = detail::view(f.R);
+  detail::check(rnla_cur_faster_kernel(detail::ctx(), &a, &b, sigma, c, r, seed, &cm, &um, &rm, f.col_indices.data(),
+                                       f.row_indices.data(), sr.data(), &nsr, sc.data(), &nsc, &ent, &flagged));
+  sr.resize(static_cast<size_t>(nsr));
+  sc.resize(static_cast<size_t>(nsc));
+  f.secondary_rows = sr;
+  f.secondary_cols = sc;
+  f.entries_visited = static_cast<long>(ent);
+  f.flagged = flagged != 0;
+  return f;
+}
+
 // KernelView over `data` with `spec` (the reference's spsd_faster(const KernelView&, ...)).
 inline SpsdSketch spsd_faster(const DenseMatrix& data, const KernelSpec& spec, Index s, Index p, std::uint64_t seed) {
   return detail::spsd_faster_call(data, &spec, s, p, seed);

@@ -262,6 +262,17 @@ rnla_status rnla_nystrom_eig(rnla_ctx* ctx, const rnla_mat* x, double sigma, int
 rnla_status rnla_spsd_faster(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, int64_t p, uint64_t seed,
                              rnla_mat* q, rnla_mat* z, int64_t* selected, int64_t* secondary, int64_t* n_secondary,
                              int32_t* flagged);
+/* cur_faster_kernel, cur.hpp:44-52 (src/cur.cpp:47-104, 188-212): CUR of the
+ * implicit RBF cross kernel K*_ij = kappa(xtest_i, xtrain_j) (m x n) with
+ * uniform primary (c columns, r rows) and secondary (p = 2(c + r)) draws:
+ * C (m x c), U (c x r), R (r x n); col_idx[c], row_idx[r]; the secondary
+ * rows / cols (room for min(m, p + r) / min(n, p + c)) with their counts;
+ * *entries (nullable) = m c + r n + |P_C| |P_R|; *flagged when C[P_C,:] or
+ * R[:,P_R] is rank deficient (threshold 1e-10). */
+rnla_status rnla_cur_faster_kernel(rnla_ctx* ctx, const rnla_mat* xtest, const rnla_mat* xtrain, double sigma,
+                                   int64_t c, int64_t r, uint64_t seed, rnla_mat* cmat, rnla_mat* umat, rnla_mat* rmat,
+                                   int64_t* col_idx, int64_t* row_idx, int64_t* sec_rows, int64_t* n_sec_rows,
+                                   int64_t* sec_cols, int64_t* n_sec_cols, int64_t* entries, int32_t* flagged);
 /* The same on a dense SPSD K (n x n), spsd.hpp:111-112. */
 rnla_status rnla_spsd_faster_dense(rnla_ctx* ctx, const rnla_mat* k, int64_t s, int64_t p, uint64_t seed, rnla_mat* q,
                                    rnla_mat* z, int64_t* selected, int64_t* secondary, int64_t* n_secondary,

@@ -452,6 +452,28 @@ def spsd_faster(x: np.ndarray, sigma: float, s: int, p: int, seed: int, dense: b
     return q, 0.5 * (z + z.T), sel, sec, flagged
 
 
+def cur_faster(a: np.ndarray, c: int, r: int, seed: int):
+    """src/cur.cpp:47-104 with the uniform sampler and default p_c = p_r = 2(c + r);
+    the kernel variant (:188-212) calls it on K* = rbf_kernel(xtest, xtrain).
+    Returns (C, U, R, col_idx, row_idx, sec_rows, sec_cols, flagged)."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if not (1 <= c <= n):
+        raise ValueError("cur: c out of [1, n]")
+    if not (1 <= r <= m):
+        raise ValueError("cur: r out of [1, m]")
+    p_c, p_r = min(2 * (c + r), m), min(2 * (c + r), n)
+    ci = sample_without_replacement(n, c, derive_seed(seed, 1))
+    ri = sample_without_replacement(m, r, derive_seed(seed, 2))
+    pc = np.union1d(sample_without_replacement(m, p_c, derive_seed(seed, 3)), ri)
+    pr = np.union1d(sample_without_replacement(n, p_r, derive_seed(seed, 4)), ci)
+    cm, rm = a[:, ci], a[ri, :]
+    c_sub, r_sub = cm[pc], rm[:, pr]
+    flagged = numerical_rank(c_sub) < min(c_sub.shape) or numerical_rank(r_sub) < min(r_sub.shape)
+    u = pseudo_inverse(c_sub) @ a[np.ix_(pc, pr)] @ pseudo_inverse(r_sub)
+    return cm, u, rm, ci, ri, pc, pr, flagged
+
+
 def leverage_scores(a: np.ndarray, k: Optional[int] = None) -> np.ndarray:
     u, s, v = truncated_svd(a, k) if k else condensed_svd(a)
     return np.sum(v * v, axis=1)

@@ -31,7 +31,7 @@ __all__ = [
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
     "count_sketch", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
     "leverage_sample_columns", "leverage_sample_rows", "thin_qr", "condensed_svd", "truncated_svd",
-    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_cg", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig", "SpsdSketch", "spsd_faster",
+    "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_cg", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig", "SpsdSketch", "spsd_faster", "CurFactors", "cur_faster_kernel",
     "shard_rows",
 ]
 
@@ -792,3 +792,43 @@ def spsd_faster(k, s: int, p: int, seed: int, ctx: Optional[Context] = None) -> 
     else:
         _check(_abi.lib().rnla_spsd_faster_dense(_ctx(ctx).handle, C.byref(xm), s, p, C.c_uint64(seed), *args))
     return SpsdSketch(q, z, sel, sec[:nsec.value].copy(), bool(flagged.value))
+
+
+@dataclasses.dataclass
+class CurFactors:
+    """include/randnla/cur.hpp:12-29: A ~ C U R."""
+    C: object
+    U: np.ndarray
+    R: object
+    col_indices: np.ndarray
+    row_indices: np.ndarray
+    secondary_rows: np.ndarray
+    secondary_cols: np.ndarray
+    entries_visited: int = 0
+    flagged: bool = False
+
+    def reconstruct(self):
+        c = self.C.cpu().numpy() if _is_torch(self.C) else np.asarray(self.C)
+        r = self.R.cpu().numpy() if _is_torch(self.R) else np.asarray(self.R)
+        return c @ (self.U @ r)
+
+
+def cur_faster_kernel(xtest, xtrain, sigma: float, c: int, r: int, seed: int,
+                      ctx: Optional[Context] = None) -> CurFactors:
+    """CUR of the implicit RBF cross kernel (src/cur.cpp:188-212), entries evaluated on the device."""
+    xt, xr = _as2d(xtest), _as2d(xtrain)
+    m, n = int(xt.shape[0]), int(xr.shape[0])
+    p = 2 * (c + r)
+    cm = _empty_like(xt, m, c, "F", dtype=None)
+    um = np.empty((c, r), dtype=np.float64, order="F")
+    rm = _empty_like(xt, r, n, "F", dtype=None)
+    ci, ri = np.empty(c, dtype=np.int64), np.empty(r, dtype=np.int64)
+    sr, sc = np.empty(max(1, min(m, p + r)), dtype=np.int64), np.empty(max(1, min(n, p + c)), dtype=np.int64)
+    nsr, nsc, ent, fl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+    a, b, cc, uu, rr = _mat(xt), _mat(xr), _mat(cm), _mat(um), _mat(rm)
+    _check(_abi.lib().rnla_cur_faster_kernel(
+        _ctx(ctx).handle, C.byref(a), C.byref(b), float(sigma), c, r, C.c_uint64(seed), C.byref(cc), C.byref(uu),
+        C.byref(rr), ci.ctypes.data_as(_abi._I64P), ri.ctypes.data_as(_abi._I64P), sr.ctypes.data_as(_abi._I64P),
+        C.byref(nsr), sc.ctypes.data_as(_abi._I64P), C.byref(nsc), C.byref(ent), C.byref(fl)))
+    return CurFactors(cm, um, rm, ci, ri, sr[:nsr.value].copy(), sc[:nsc.value].copy(), int(ent.value),
+                      bool(fl.value))

@@ -105,6 +105,9 @@ SIGNATURES = {
         C.c_int, [_P, _M, C.c_double, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, _M, _F64P, _I64P, _I64P]),
     "rnla_spsd_faster": (
         C.c_int, [_P, _M, C.c_double, C.c_int64, C.c_int64, C.c_uint64, _M, _M, _I64P, _I64P, _I64P, _I32P]),
+    "rnla_cur_faster_kernel": (
+        C.c_int, [_P, _M, _M, C.c_double, C.c_int64, C.c_int64, C.c_uint64, _M, _M, _M, _I64P, _I64P, _I64P, _I64P,
+                  _I64P, _I64P, _I64P, _I32P]),
     "rnla_spsd_faster_dense": (
         C.c_int, [_P, _M, C.c_int64, C.c_int64, C.c_uint64, _M, _M, _I64P, _I64P, _I64P, _I32P]),
 }

@@ -1,13 +1,13 @@
 // rnla_cli -- command-line drop-in for the hot-path subcommands of the
 // reference CLI (tools/randnla_cli.cpp:127-445): sketch, lsr, ksvd, spsd,
-// nystrom. Same flags, one JSON RunReport per line on stdout
+// nystrom, cur (kernel mode). Same flags, one JSON RunReport per line on stdout
 // (schemas/run_report.schema.json: command, seed, parameters, metrics,
 // status, elapsed_ms, message; keys sorted like the reference's std::map),
 // a human summary on stderr, exit codes 0 ok / 2 flagged / 1 error. Matrix
 // files: Matrix Market (.mtx/.mm, array or coordinate, general or symmetric)
 // or CSV (src/io.cpp:47-230). Every computation runs through the C ABI
 // (include/rnla.h) via the C++ facade; the other reference subcommands
-// (verify, cur, apps, bench) are outside the B200 build and report an error.
+// (verify, dense cur, apps, bench) are outside the B200 build and report an error.
 #include <algorithm>
 #include <charconv>
 #include <chrono>
@@ -486,9 +486,33 @@ int main(int argc, char** argv) {
         const DenseMatrix kernel = rbf_kernel(x, x, sigma);
         rep.metrics["error_rel"] = fro(minus(kernel, mul(f.L, f.L, false, true))) / fro(kernel);
         rep.metrics["rank"] = (double)f.L.cols();
+      } else if (cmd == "cur") {
+        Args a = parse(argc, argv,
+                       {"--input", "--train", "--test", "--sigma", "--method", "--c", "--r", "--p-c", "--p-r", "--seed",
+                        "--output"},
+                       {"--leverage"}, {"--c", "--r", "--seed"}, {"--input", "--train", "--test"});
+        rep.seed = a.u64("--seed");
+        const Index c = a.i64("--c", 10), r = a.i64("--r", 10);
+        rep.parameters = {{"method", a.str("--method", "faster")}, {"c", std::to_string(c)}, {"r", std::to_string(r)}};
+        if (a.has("--input")) {
+          rep.parameters["input"] = a.str("--input");
+          throw std::runtime_error("dense CUR (cur_prototype / cur_faster) is not part of the B200 hot path; "
+                                   "use --train/--test (cur_faster_kernel)");
+        }
+        if (!a.has("--train") || !a.has("--test"))
+          throw std::invalid_argument("provide --input (dense) or --train and --test (kernel)");
+        rep.parameters["train"] = a.str("--train");
+        rep.parameters["test"] = a.str("--test");
+        const DenseMatrix xtrain = load_matrix(a.str("--train")), xtest = load_matrix(a.str("--test"));
+        const CurFactors f = cur_faster_kernel(xtest, xtrain, a.f64("--sigma", 1.0), c, r, rep.seed);
+        if (a.has("--output")) save_matrix(mul(f.C, mul(f.U, f.R)), a.str("--output"));
+        rep.metrics["entries_visited"] = (double)f.entries_visited;
+        rep.metrics["core_rows"] = (double)f.U.rows();
+        rep.metrics["core_cols"] = (double)f.U.cols();
+        if (f.flagged) rep.status = "flagged";
       } else {
         throw UsageError("The following argument was not expected: " + cmd +
-                             " (this build provides sketch, lsr, ksvd, spsd, nystrom)",
+                             " (this build provides sketch, lsr, ksvd, spsd, nystrom, cur)",
                          109);
       }
     } catch (const UsageError&) {

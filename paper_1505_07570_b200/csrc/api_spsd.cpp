@@ -376,6 +376,131 @@ void spsd_faster_impl(rnla_ctx* ctx, const rnla_mat* x, bool dense_k, double sig
   RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// pinv (tol 1e-12 sigma_1, src/core.cpp:78-88) of a column-major fp64 rows x cols
+// block into out (cols x rows), and its numerical rank at 1e-10 (the reference's
+// ColPivHouseholderQR threshold) -- one thin SVD of the tall orientation.
+int64_t pinv_rank_dev(rnla_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* out) {
+  const bool wide = rows < cols;
+  const int64_t m = wide ? cols : rows, n = wide ? rows : cols;  // SVD of the m x n tall view
+  DevBuf U(sizeof(double) * m * n, ctx->stream), S(sizeof(double) * n, ctx->stream), V(sizeof(double) * n * n, ctx->stream),
+      inv(sizeof(double) * n, ctx->stream), Vi(sizeof(double) * n * n, ctx->stream);
+  if (!wide) svd_thin(ctx, m, n, A, 1, rows, U.as<double>(), S.as<double>(), V.as<double>());
+  else svd_thin(ctx, m, n, A, rows, 1, U.as<double>(), S.as<double>(), V.as<double>());
+  std::vector<double> hs((size_t)n), hinv((size_t)n, 0.0);
+  RNLA_CUDA(cudaMemcpyAsync(hs.data(), S.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  int64_t rank = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (hs[0] > 0.0 && hs[(size_t)i] > 1e-10 * hs[0]) ++rank;
+    if (hs[0] > 0.0 && hs[(size_t)i] > 1e-12 * hs[0]) hinv[(size_t)i] = 1.0 / hs[(size_t)i];
+  }
+  RNLA_CUDA(cudaMemcpyAsync(inv.p, hinv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  scale_cols_dev(ctx, n, n, V.as<double>(), inv.as<double>(), Vi.as<double>());
+  // tall: pinv = V S^+ U' (n x m);  wide (A' = U S V'): pinv(A) = U S^+ V' (m x n)
+  if (!wide)
+    gemm<double>(ctx, n, m, n, 1.0, Vi.as<double>(), 1, n, U.as<double>(), m, 1, 0.0, out, 1, n);
+  else
+    gemm<double>(ctx, m, n, n, 1.0, U.as<double>(), 1, m, Vi.as<double>(), n, 1, 0.0, out, 1, m);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return rank;
+}
+
+// cur_faster_kernel (src/cur.cpp:47-104, 188-212): the implicit RBF cross
+// kernel K*_ij = kappa(xtest_i, xtrain_j), uniform primary and secondary draws
+// (derive_seed(seed, 1..4)), U = pinv(C[P_C, :]) K*[P_C, P_R] pinv(R[:, P_R]).
+// Visits m c + r n + |P_C| |P_R| entries.
+template <class T>
+void cur_faster_kernel_impl(rnla_ctx* ctx, const rnla_mat* xt, const rnla_mat* xr, double sigma, int64_t c, int64_t r,
+                            uint64_t seed, const rnla_mat* c_out, const rnla_mat* u_out, const rnla_mat* r_out,
+                            int64_t* col_idx, int64_t* row_idx, int64_t* sec_rows, int64_t* n_sec_rows,
+                            int64_t* sec_cols, int64_t* n_sec_cols, int64_t* entries, int32_t* flagged) {
+  DevMat Xt = to_device(ctx, xt), Xr = to_device(ctx, xr);
+  const int64_t m = Xt.rows, n = Xr.rows, d = Xt.cols;
+  require(c >= 1 && c <= n, "cur: c out of [1, n]");
+  require(r >= 1 && r <= m, "cur: r out of [1, m]");
+  const int64_t p_c = std::min<int64_t>(2 * (c + r), m), p_r = std::min<int64_t>(2 * (c + r), n);
+  const std::vector<int64_t> SC = sample_without_replacement_host(derive_seed(seed, 1), n, c);
+  const std::vector<int64_t> SR = sample_without_replacement_host(derive_seed(seed, 2), m, r);
+  std::vector<int64_t> PC = sample_without_replacement_host(derive_seed(seed, 3), m, p_c);
+  std::vector<int64_t> PR = sample_without_replacement_host(derive_seed(seed, 4), n, p_r);
+  auto unite = [](std::vector<int64_t> a, const std::vector<int64_t>& b) {
+    a.insert(a.end(), b.begin(), b.end());
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+    return a;
+  };
+  PC = unite(PC, SR);
+  PR = unite(PR, SC);
+  const int64_t npc = (int64_t)PC.size(), npr = (int64_t)PR.size();
+  auto upload = [&](const std::vector<int64_t>& v) {
+    DevBuf b(sizeof(int64_t) * std::max<size_t>(v.size(), 1), ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(int64_t) * v.size(), cudaMemcpyHostToDevice, ctx->stream));
+    return b;
+  };
+  DevBuf dSC = upload(SC), dSR = upload(SR), dPC = upload(PC), dPR = upload(PR);
+  // squared norms: all test rows, all train rows (the cached norms of CrossKernel)
+  DevBuf sqt(sizeof(T) * m, ctx->stream), sqr(sizeof(T) * n, ctx->stream);
+  sq_norms<T>(ctx, m, d, Xt.as<T>(), Xt.rs, Xt.cs, nullptr, sqt.as<T>());
+  sq_norms<T>(ctx, n, d, Xr.as<T>(), Xr.rs, Xr.cs, nullptr, sqr.as<T>());
+  auto gather_sq = [&](const DevBuf& sq, const DevBuf& idx, int64_t cnt) {
+    DevBuf g(sizeof(T) * cnt, ctx->stream);
+    gather_columns<T>(ctx, 1, cnt, sq.as<T>(), 1, 1, idx.as<int64_t>(), nullptr, g.as<T>(), 1, 1);
+    return g;
+  };
+  DevBuf sqSC = gather_sq(sqr, dSC, c), sqPR = gather_sq(sqr, dPR, npr), sqSR = gather_sq(sqt, dSR, r),
+         sqPC = gather_sq(sqt, dPC, npc);
+  auto to64 = [&](const DevBuf& src, int64_t cnt) {
+    DevBuf o(sizeof(double) * cnt, ctx->stream);
+    if constexpr (std::is_same<T, double>::value)
+      RNLA_CUDA(cudaMemcpyAsync(o.p, src.p, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      copy2d_cast<float, double>(ctx, cnt, 1, src.as<float>(), 1, cnt, o.as<double>(), 1, cnt);
+    return o;
+  };
+  // C = K*[:, S_C] (m x c), R = K*[S_R, :] (r x n), block = K*[P_C, P_R]; column-major
+  DevBuf Ct(sizeof(T) * m * c, ctx->stream), Rt(sizeof(T) * r * n, ctx->stream), Bt(sizeof(T) * npc * npr, ctx->stream);
+  rbf_block<T>(ctx, m, c, d, Xt.as<T>(), Xt.rs, Xt.cs, Xr.as<T>(), Xr.rs, Xr.cs, dSC.as<int64_t>(), sqt.as<T>(),
+               sqSC.as<T>(), sigma, nullptr, Ct.as<T>(), 1, m);
+  {
+    DevMat XS = alloc_dense(ctx, r, d, true, Xt.dtype);
+    gather_rows<T>(ctx, r, d, Xt.as<T>(), Xt.rs, Xt.cs, dSR.as<int64_t>(), XS.as<T>(), XS.rs, XS.cs);
+    rbf_block<T>(ctx, r, n, d, XS.as<T>(), XS.rs, XS.cs, Xr.as<T>(), Xr.rs, Xr.cs, nullptr, sqSR.as<T>(), sqr.as<T>(),
+                 sigma, nullptr, Rt.as<T>(), 1, r);
+    DevMat XP = alloc_dense(ctx, npc, d, true, Xt.dtype);
+    gather_rows<T>(ctx, npc, d, Xt.as<T>(), Xt.rs, Xt.cs, dPC.as<int64_t>(), XP.as<T>(), XP.rs, XP.cs);
+    rbf_block<T>(ctx, npc, npr, d, XP.as<T>(), XP.rs, XP.cs, Xr.as<T>(), Xr.rs, Xr.cs, dPR.as<int64_t>(),
+                 sqPC.as<T>(), sqPR.as<T>(), sigma, nullptr, Bt.as<T>(), 1, npc);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  DevBuf C64 = to64(Ct, m * c), R64 = to64(Rt, r * n), B64 = to64(Bt, npc * npr);
+  // c_sub = C[P_C, :] (npc x c), r_sub = R[:, P_R] (r x npr)
+  DevBuf csub(sizeof(double) * npc * c, ctx->stream), rsub(sizeof(double) * r * npr, ctx->stream),
+      pc(sizeof(double) * c * npc, ctx->stream), pr(sizeof(double) * npr * r, ctx->stream),
+      t1(sizeof(double) * c * npr, ctx->stream), U(sizeof(double) * c * r, ctx->stream);
+  gather_rows<double>(ctx, npc, c, C64.as<double>(), 1, m, dPC.as<int64_t>(), csub.as<double>(), 1, npc);
+  gather_columns<double>(ctx, r, npr, R64.as<double>(), 1, r, dPR.as<int64_t>(), nullptr, rsub.as<double>(), 1, r);
+  const int64_t rank_c = pinv_rank_dev(ctx, npc, c, csub.as<double>(), pc.as<double>());
+  const int64_t rank_r = pinv_rank_dev(ctx, r, npr, rsub.as<double>(), pr.as<double>());
+  *flagged = (rank_c < std::min(npc, c) || rank_r < std::min(r, npr)) ? 1 : 0;
+  gemm<double>(ctx, c, npr, npc, 1.0, pc.as<double>(), 1, c, B64.as<double>(), 1, npc, 0.0, t1.as<double>(), 1, c);
+  gemm<double>(ctx, c, r, npr, 1.0, t1.as<double>(), 1, c, pr.as<double>(), 1, npr, 0.0, U.as<double>(), 1, c);
+  OutMat co(ctx, c_out, m, c, "cur: C", false), uo(ctx, u_out, c, r, "cur: U", false), ro(ctx, r_out, r, n, "cur: R", false);
+  store_block(ctx, C64.as<double>(), m, c, m, co);
+  store_block(ctx, U.as<double>(), c, r, c, uo);
+  store_block(ctx, R64.as<double>(), r, n, r, ro);
+  co.finish(ctx);
+  uo.finish(ctx);
+  ro.finish(ctx);
+  std::copy(SC.begin(), SC.end(), col_idx);
+  std::copy(SR.begin(), SR.end(), row_idx);
+  std::copy(PC.begin(), PC.end(), sec_rows);
+  std::copy(PR.begin(), PR.end(), sec_cols);
+  *n_sec_rows = npc;
+  *n_sec_cols = npr;
+  if (entries) *entries = m * c + r * n + npc * npr;
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 }  // namespace
 
 }  // namespace rnla
@@ -486,6 +611,29 @@ rnla_status rnla_spsd_faster_dense(rnla_ctx* ctx, const rnla_mat* k, int64_t s, 
       spsd_faster_impl<double>(ctx, k, true, 1.0, s, p, seed, q, z, selected, secondary, n_secondary, flagged);
     else
       spsd_faster_impl<float>(ctx, k, true, 1.0, s, p, seed, q, z, selected, secondary, n_secondary, flagged);
+  });
+}
+
+rnla_status rnla_cur_faster_kernel(rnla_ctx* ctx, const rnla_mat* xtest, const rnla_mat* xtrain, double sigma,
+                                   int64_t c, int64_t r, uint64_t seed, rnla_mat* cmat, rnla_mat* umat, rnla_mat* rmat,
+                                   int64_t* col_idx, int64_t* row_idx, int64_t* sec_rows, int64_t* n_sec_rows,
+                                   int64_t* sec_cols, int64_t* n_sec_cols, int64_t* entries, int32_t* flagged) {
+  return guard([&] {
+    enter(ctx);
+    require(sigma > 0.0, "cur_faster_kernel: sigma <= 0");
+    check_mat(xtest, "cur_faster_kernel: xtest");
+    check_mat(xtrain, "cur_faster_kernel: xtrain");
+    require(xtest->cols == xtrain->cols, "cur_faster_kernel: dimension mismatch");
+    require(xtest->dtype == xtrain->dtype, "cur_faster_kernel: dtype mismatch");
+    require(ctx->world == 1, "cur_faster_kernel: row-sharded contexts are not supported");
+    require(col_idx && row_idx && sec_rows && n_sec_rows && sec_cols && n_sec_cols && flagged,
+            "cur_faster_kernel: null output");
+    if (xtest->dtype == RNLA_F64)
+      cur_faster_kernel_impl<double>(ctx, xtest, xtrain, sigma, c, r, seed, cmat, umat, rmat, col_idx, row_idx,
+                                     sec_rows, n_sec_rows, sec_cols, n_sec_cols, entries, flagged);
+    else
+      cur_faster_kernel_impl<float>(ctx, xtest, xtrain, sigma, c, r, seed, cmat, umat, rmat, col_idx, row_idx,
+                                    sec_rows, n_sec_rows, sec_cols, n_sec_cols, entries, flagged);
   });
 }
 

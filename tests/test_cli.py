@@ -146,3 +146,22 @@ def test_cli_ksvd_spsd_nystrom(tmp_path):
     code, reps, _ = run("spsd", "--method", "prototype", "--data", tmp_path / "x.csv", "--sigma", "2", "--s", "10",
                         "--seed", "6")
     assert code == 0 and 0.0 <= reps[0]["metrics"]["error_rel"] < 1.0
+
+
+@pytest.mark.gpu
+def test_cli_cur_kernel(tmp_path):
+    xtest = orc.gaussian_matrix(45, 3, 15)
+    xtrain = orc.gaussian_matrix(60, 3, 16)
+    save_csv(tmp_path / "te.csv", xtest)
+    save_csv(tmp_path / "tr.csv", xtrain)
+    code, reps, _ = run("cur", "--train", tmp_path / "tr.csv", "--test", tmp_path / "te.csv", "--sigma", "1.3",
+                        "--c", "7", "--r", "6", "--seed", "17", "--output", tmp_path / "cur.mtx")
+    assert code in (0, 2), reps
+    check_schema(reps[0])
+    ks = orc.rbf_kernel(xtest, xtrain, 1.3)
+    C, U, R, ci, ri, pc, pr, flagged = orc.cur_faster(ks, 7, 6, 17)
+    m = reps[0]["metrics"]
+    assert m["core_rows"] == 7 and m["core_cols"] == 6
+    assert m["entries_visited"] == 45 * 7 + 6 * 60 + len(pc) * len(pr)
+    code, reps, _ = run("cur", "--input", tmp_path / "tr.csv", "--c", "2", "--r", "2", "--seed", "1")
+    assert code == 1 and "not part of the B200 hot path" in reps[0]["message"]

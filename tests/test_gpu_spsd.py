@@ -138,3 +138,42 @@ def test_spsd_faster_matches_oracle(ctx, dtype):
         assert np.linalg.norm(sk.Z - z) <= 1e-8 * np.linalg.norm(z)
     with pytest.raises(ValueError, match="s <= p <= n"):
         rn.spsd_faster(rn.KernelView(x, rn.KernelSpec(2.5)), 60, 50, 1, ctx=ctx)
+
+
+@pytest.mark.parametrize("seed", [17, 18, 19])
+def test_cur_faster_kernel_matches_oracle(ctx, seed):
+    # tests/test_cur.cpp:74-93: the lazy kernel CUR equals cur_faster on K*
+    xtest = orc.gaussian_matrix(45, 3, 15)
+    xtrain = orc.gaussian_matrix(60, 3, 16)
+    f = rn.cur_faster_kernel(xtest, xtrain, 1.3, 7, 6, seed, ctx=ctx)
+    ks = orc.rbf_kernel(xtest, xtrain, 1.3)
+    C, U, R, ci, ri, pc, pr, flagged = orc.cur_faster(ks, 7, 6, seed)
+    assert np.array_equal(f.col_indices, ci) and np.array_equal(f.row_indices, ri)
+    assert np.array_equal(f.secondary_rows, pc) and np.array_equal(f.secondary_cols, pr)
+    assert f.flagged == flagged
+    assert np.allclose(f.C, C, rtol=0, atol=1e-14) and np.allclose(f.R, R, rtol=0, atol=1e-14)
+    assert np.linalg.norm(f.U - U) <= 1e-8 * np.linalg.norm(U)
+    assert f.entries_visited <= 45 * 7 + 60 * 6 + len(f.secondary_rows) * len(f.secondary_cols)
+
+
+def test_cur_faster_kernel_preconditions(ctx):
+    # tests/test_cur.cpp:95-103
+    xtest = orc.gaussian_matrix(1, 3, 20)
+    xtrain = orc.gaussian_matrix(30, 3, 21)
+    with pytest.raises(ValueError, match="r out of"):
+        rn.cur_faster_kernel(xtest, xtrain, 1.0, 5, 3, 1, ctx=ctx)
+    ok = rn.cur_faster_kernel(xtest, xtrain, 1.0, 5, 1, 1, ctx=ctx)
+    assert ok.R.shape[0] == 1
+
+
+def test_cur_faster_kernel_fp32_large(ctx):
+    rng = np.random.default_rng(3)
+    xtest = rng.standard_normal((3000, 16)).astype(np.float32)
+    xtrain = rng.standard_normal((5000, 16)).astype(np.float32)
+    f = rn.cur_faster_kernel(dev(xtest), dev(xtrain), 4.0, 80, 60, 9, ctx=ctx)
+    ks = orc.rbf_kernel(xtest.astype(np.float64), xtrain.astype(np.float64), 4.0)
+    C, U, R, ci, ri, pc, pr, flagged = orc.cur_faster(ks, 80, 60, 9)
+    assert np.array_equal(f.secondary_rows, pc) and np.array_equal(f.secondary_cols, pr)
+    rec = f.C.cpu().numpy().astype(np.float64) @ f.U @ f.R.cpu().numpy().astype(np.float64)
+    ref = C @ U @ R
+    assert np.linalg.norm(rec - ref) <= 1e-3 * np.linalg.norm(ref)
