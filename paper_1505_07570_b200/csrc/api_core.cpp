@@ -321,6 +321,10 @@ void rnla_ctx_destroy(rnla_ctx* ctx) {
   ctx->gauss_ops.clear();
   ctx->srht_plans.clear();
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->green) {
+    for (auto s : {ctx->green->gather[0], ctx->green->gather[1], ctx->green->gemm}) cudaStreamSynchronize(s);
+    ctx->green.reset();
+  }
   if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));

@@ -70,10 +70,27 @@ std::shared_ptr<SrhtPlan> srht_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_
 // Gaussian stage under the count sketch does not overlap, the gather kernel
 // holds the register file), s / world on a row-sharded job so each rank
 // multiplies the chunks it owns after a per-chunk ncclReduce.
+// SM count for the GEMM side of a green-context split on one GPU (RNLA_GREEN_SMS, 0 = off).
+static int green_gemm_sms() {
+  static const int v = std::getenv("RNLA_GREEN_SMS") ? std::atoi(std::getenv("RNLA_GREEN_SMS")) : 0;
+  return v;
+}
+static constexpr int64_t kGreenChunks = 16;
+
 static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k) {
   if (const char* e = std::getenv("RNLA_GAUSS_KC")) return std::max<int64_t>(16, std::atoll(e));
   const int64_t w = std::max(1, ctx->world);
+  if (w == 1 && green_gemm_sms() > 0) return std::max<int64_t>(16, (k + kGreenChunks - 1) / kGreenChunks);
   return std::max<int64_t>(16, (k + w - 1) / w);
+}
+
+static rnla::GreenSplit* green_for(rnla_ctx* ctx) {
+  if (ctx->world != 1 || green_gemm_sms() <= 0) return nullptr;
+  if (!ctx->green_tried) {
+    ctx->green_tried = true;
+    ctx->green = make_green_split(ctx->device, green_gemm_sms());
+  }
+  return ctx->green.get();
 }
 template <class T>
 void gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s,
@@ -119,12 +136,31 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
   for (auto& e : ev) RNLA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cudaEvent_t start = ev[(size_t)chunks], done = ev[(size_t)chunks + 1];
   RNLA_CUDA(cudaEventRecord(start, ctx->stream));
-  RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, start, 0));
-  RNLA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, start, 0));
+  // One GPU with a green-context split: gather chunks on the gather SMs, the
+  // first n_b GEMM chunks on the GEMM SMs under the gather, the rest on the
+  // whole GPU once the gather is done (same chunk order -> same bits).
+  rnla::GreenSplit* green = green_for(ctx);
+  int64_t n_b = chunks;
+  cudaStream_t gemm_st = ctx->aux_stream;
+  cudaStream_t gather_st[2] = {ctx->stream, ctx->copy_stream};
+  if (green) {
+    gather_st[0] = green->gather[0];
+    gather_st[1] = green->gather[1];
+    gemm_st = green->gemm;
+    // chunks the GEMM SMs finish while the gather runs: gather time ~ bytes / HBM,
+    // GEMM time ~ flops / DMMA rate scaled by the SM share
+    const double ts = (double)n * (double)Lo * sizeof(T) / 6.4e12;
+    const double tg = 2.0 * (double)s * (double)s2 * (double)Lo / (sizeof(T) == 8 ? 25e12 : 400e12);
+    const double f = (double)green->gemm_sms / (double)(green->gemm_sms + green->gather_sms);
+    n_b = std::max<int64_t>(0, std::min<int64_t>(chunks, (int64_t)((double)chunks * f * ts / std::max(tg, 1e-12))));
+    if (const char* e = std::getenv("RNLA_GREEN_CHUNKS_B")) n_b = std::min<int64_t>(chunks, std::atoll(e));
+  }
+  RNLA_CUDA(cudaStreamWaitEvent(gemm_st, start, 0));
+  RNLA_CUDA(cudaStreamWaitEvent(gather_st[0], start, 0));
+  RNLA_CUDA(cudaStreamWaitEvent(gather_st[1], start, 0));
   bool first = true;
   // Gather chunks alternate between two streams so one chunk's last partial
   // wave overlaps the next chunk instead of draining the GPU.
-  cudaStream_t gather_st[2] = {ctx->stream, ctx->copy_stream};
   try {
     for (int64_t c = 0; c < chunks; ++c) {
       const int64_t b0 = c * KC, b1 = std::min(s, b0 + KC);
@@ -134,8 +170,18 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
                                  b1);
         RNLA_CUDA(cudaEventRecord(ev[(size_t)c], ctx->stream));
       }
-      RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ev[(size_t)c], 0));
-      StreamScope on_aux(ctx, ctx->aux_stream);
+    }
+    for (int64_t c = 0; c < chunks; ++c) {
+      const int64_t b0 = c * KC, b1 = std::min(s, b0 + KC);
+      if (green && c == n_b) {
+        // hand the remaining chunks to the whole GPU after the gather and the GEMM SMs' last chunk
+        RNLA_CUDA(cudaEventRecord(done, gemm_st));
+        RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, done, 0));
+        for (int64_t q = 0; q < chunks; ++q) RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ev[(size_t)q], 0));
+        gemm_st = ctx->aux_stream;
+      }
+      RNLA_CUDA(cudaStreamWaitEvent(gemm_st, ev[(size_t)c], 0));
+      StreamScope on_aux(ctx, gemm_st);
       const int owner = (int)(c % ctx->world);
       if (ctx->world > 1) reduce_to(ctx, mid.as<T>() + b0 * Lo, (size_t)((b1 - b0) * Lo), dt, owner);
       if (owner == ctx->rank) {
@@ -143,10 +189,14 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
         first = false;
       }
     }
-    if (first) RNLA_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(T) * (size_t)(s2 * Lo), ctx->aux_stream));
-    RNLA_CUDA(cudaEventRecord(done, ctx->aux_stream));
+    if (first) RNLA_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(T) * (size_t)(s2 * Lo), gemm_st));
+    RNLA_CUDA(cudaEventRecord(done, gemm_st));
     RNLA_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+    // the gather streams' last chunks are covered by the GEMM dependencies
   } catch (...) {
+    cudaStreamSynchronize(gemm_st);
+    cudaStreamSynchronize(gather_st[0]);
+    cudaStreamSynchronize(gather_st[1]);
     cudaStreamSynchronize(ctx->aux_stream);
     for (auto& e : ev) cudaEventDestroy(e);
     throw;
@@ -193,7 +243,7 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
   const int kind = spec->kind;
   const bool sharded = ctx->world > 1;
   static const bool force_pipeline = std::getenv("RNLA_PIPELINE") != nullptr;  // tuning knob
-  if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN && (sharded || force_pipeline)) {
+  if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN && (sharded || force_pipeline || green_gemm_sms() > 0)) {
     combined_gaussian_pipelined<T>(ctx, M, ld, extra, xs, n, L, spec, row_offset, out, o_rs, o_cs);
     return;
   }

@@ -90,6 +90,17 @@ struct DenseOperator {  // G / sqrt(s) as the reference forms it, device fp64/fp
   int dtype = RNLA_F64;
 };
 
+// SM-partitioned streams from two CUDA green contexts (green.cpp).
+struct GreenSplit {
+  void* ctx_gather = nullptr;  // CUgreenCtx
+  void* ctx_gemm = nullptr;
+  cudaStream_t gather[2] = {nullptr, nullptr};
+  cudaStream_t gemm = nullptr;
+  int gather_sms = 0, gemm_sms = 0;
+  ~GreenSplit();
+};
+std::unique_ptr<GreenSplit> make_green_split(int device, int gemm_sms);
+
 }  // namespace rnla
 
 struct rnla_ctx {
@@ -108,6 +119,8 @@ struct rnla_ctx {
   std::map<std::tuple<int64_t, int64_t, int64_t, uint64_t>, std::unique_ptr<rnla::CountSketchPlan>> cs_plans;
   std::map<std::tuple<int64_t, int64_t, uint64_t, int>, std::unique_ptr<rnla::DenseOperator>> gauss_ops;
   std::map<std::tuple<int64_t, int64_t, uint64_t>, std::shared_ptr<rnla::SrhtPlan>> srht_plans;
+  std::unique_ptr<rnla::GreenSplit> green;  // lazily created (combined sketch pipelining)
+  bool green_tried = false;
 };
 
 namespace rnla {
