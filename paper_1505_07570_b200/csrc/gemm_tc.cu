@@ -760,27 +760,35 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   // 4 of the double-float mode), else 128-column tiles
   const int cap = DF ? 128 : 160;
   const int bn_full = n <= cap ? (int)(((n + 15) / 16) * 16) : 128;
-  const int64_t ntiles = (n + bn_full - 1) / bn_full;
-  const int64_t tiles = ((m + TC_BM - 1) / TC_BM) * ntiles;
+  // Gram products (B = A') are symmetric: upper tiles only, then mirror; the
+  // split-K sizing below counts only the tiles that run.
+  const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs && !std::getenv("RNLA_TC_NO_SYM")) ? 1 : 0;
+  const int bn_eff = bn_full <= 32 ? 32 : bn_full <= 64 ? 64 : bn_full <= 96 ? 96 : (DF || bn_full <= 128) ? 128 : 160;
+  const int64_t mtiles = (m + TC_BM - 1) / TC_BM, ntiles_eff = (n + bn_eff - 1) / bn_eff;
+  int64_t tiles = mtiles * ntiles_eff;
+  if (sym) {
+    tiles = 0;
+    for (int64_t mt = 0; mt < mtiles; ++mt)
+      for (int64_t nt = 0; nt < ntiles_eff; ++nt) tiles += (mt * TC_BM < (nt + 1) * bn_eff) ? 1 : 0;
+  }
   // Split K so that the CTAs fill whole waves of the 148 SMs (one CTA per SM):
   // the smallest split count reaching >= 97 % wave efficiency among those that
   // give every SM a tile, each split keeping >= 4 k-blocks and the fp32/fp64
   // workspace <= 512 MB. (Measured: A'Q at 16384 x 150, K = 262144 ran 256
   // CTAs = 1.73 waves.)
   int64_t splits = 1;
-  if (DF) {
-    // double-float Grams keep the original rule (as many splits as SMs): short
-    // K ranges per CTA accumulate in TMEM for only a few k-blocks, and the
-    // partials are summed in fp64 (row-leverage sums stay within ~1e-7)
+  if (DF && tiles <= 8) {
+    // small double-float Grams keep the one-tile-per-SM rule: short K ranges
+    // per CTA accumulate in TMEM for only a few k-blocks, and the partials are
+    // summed in fp64 (row-leverage sums stay within ~1e-7)
     if (tiles < ctx->num_sms && k >= 2 * TC_BK)
       splits = std::min<int64_t>((ctx->num_sms + tiles - 1) / tiles, k / TC_BK);
   } else if (k >= 2 * TC_BK) {
     const int64_t sms = ctx->num_sms;
     const int64_t ws_cap = ((int64_t)512 << 20) / std::max<int64_t>(1, m * n * (int64_t)sizeof(OutT));
     const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(k / (4 * TC_BK), 256), ws_cap));
-    const int64_t smin = std::min<int64_t>(smax, (sms + tiles - 1) / tiles);
     double best = -1.0;
-    for (int64_t s = smin; s <= smax; ++s) {
+    for (int64_t s = 1; s <= smax; ++s) {
       const double w = (double)(tiles * s) / (double)sms;
       const double eff = w / std::ceil(w);
       if (eff > best + 1e-9) {
@@ -799,8 +807,6 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
     wsb = DevBuf(sizeof(OutT) * (size_t)(splits * m * n), ctx->stream);
     ws = wsb.as<OutT>();
   }
-  // Gram products (B = A') are symmetric: upper tiles only, then mirror.
-  const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs && !std::getenv("RNLA_TC_NO_SYM")) ? 1 : 0;
   CUtensorMap amap;
   const bool tma = make_a_map(&amap, A, m, k, a_rs, a_cs);
   if (a_cs == 1)
@@ -816,7 +822,6 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
     note_launch(ctx);
   }
   if (sym) {
-    const int bn_eff = bn_full <= 32 ? 32 : bn_full <= 64 ? 64 : bn_full <= 96 ? 96 : (DF || bn_full <= 128) ? 128 : 160;
     mirror_skipped_tiles<OutT><<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, TC_BM, bn_eff, C, c_rs, c_cs);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
