@@ -32,7 +32,22 @@ namespace rnla {
 
 namespace {
 
-constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES_MAX = 4;
+// k per pipeline stage: 64 (SWIZZLE_128B bf16 rows). 32 (SWIZZLE_64B) keeps
+// twice as many stages in the same shared memory; measured on B200 it is no
+// faster (config 3 36.9 vs 36.6 ms, leverage Gram 30.6 vs 30.0 ms) and its
+// register-staged fallback spills, so it stays a build option.
+#ifndef RNLA_TC_BK
+#define RNLA_TC_BK 64
+#endif
+constexpr int TC_BM = 128, TC_BK = RNLA_TC_BK, TC_STAGES_MAX = 8;
+static_assert(TC_BK == 64 || TC_BK == 32, "TC_BK must be 32 or 64");
+constexpr int ROWB = TC_BK * 2;  // bytes per K-major bf16 tile row
+constexpr int QPR = TC_BK / 8;   // 16-B chunks per tile row
+// physical 16-B chunk of logical chunk q in row r: SW128 (q ^ (r & 7)) or SW64 (q ^ ((r >> 1) & 3))
+__host__ __device__ constexpr uint32_t swz(int r, int q) {
+  return TC_BK == 64 ? (uint32_t)(q ^ (r & 7)) : (uint32_t)(q ^ ((r >> 1) & 3));
+}
+__host__ __device__ constexpr uint32_t tile_off(int r, int q) { return (uint32_t)r * ROWB + (swz(r, q) << 4); }
 // Producer groups of 4 warps take k-blocks round-robin (more groups = more
 // A bytes in flight per SM: the loads are register-staged).
 #ifndef RNLA_TC_NGROUPS
@@ -67,15 +82,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-// Shared-memory matrix descriptor, K-major SWIZZLE_128B: rows of 128 B,
-// 8-row atoms of 1024 B (SBO), LBO unused (1), version 1 (sm_100).
+// Shared-memory matrix descriptor, K-major swizzled: rows of ROWB bytes,
+// 8-row atoms of 8*ROWB bytes (SBO), LBO unused (1), version 1 (sm_100);
+// layout code 2 = SWIZZLE_128B, 4 = SWIZZLE_64B.
 __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;            // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: next 8-row group
-  d |= (uint64_t)1 << 46;            // version = 1
-  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  d |= (uint64_t)1 << 16;                     // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)((8 * ROWB) >> 4) << 32;     // SBO: next 8-row group
+  d |= (uint64_t)1 << 46;                     // version = 1
+  d |= (uint64_t)(TC_BK == 64 ? 2 : 4) << 61;  // swizzle mode
   return d;
 }
 
@@ -98,7 +114,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                : "memory");
 }
 
-constexpr int TC_PROMOTE_KB = 8;  // k-blocks (x64 k) per TMEM partial sum
+constexpr int TC_PROMOTE_KB = 512 / TC_BK;  // k-blocks per TMEM partial sum (512 k)
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
   asm volatile(
@@ -175,9 +191,9 @@ __device__ __forceinline__ void split8(const float* f, uint4& hi, uint4& lo) {
 // hi/lo tiles (row r at r*128 B, 16-B chunk q at (q ^ (r & 7)) * 16).
 template <bool KCONTIG>
 __device__ __forceinline__ void unit_coords(int u, int R, int& r, int& q) {
-  if (KCONTIG) {  // 8 lanes cover one row's 64 k: 256 B contiguous
-    r = u >> 3;
-    q = u & 7;
+  if (KCONTIG) {  // QPR lanes cover one row's TC_BK k contiguous
+    r = u / QPR;
+    q = u % QPR;
   } else {  // lanes run along rows (MN-contiguous in global)
     r = u % R;
     q = u / R;
@@ -234,7 +250,7 @@ __device__ __forceinline__ void prefetch_tile_l2(const float* __restrict__ X, in
 template <bool KCONTIG, int R, int NT, int NS>
 __device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int64_t rs, int64_t ks, int64_t rows,
                                                 int64_t r0, int64_t k0, int64_t kend, uint8_t* base, int tid) {
-  constexpr int UNITS = R * 8;  // (row, 8-k chunk)
+  constexpr int UNITS = R * QPR;  // (row, 8-k chunk)
   constexpr int UPT = (UNITS + NT - 1) / NT;
   float f[UPT][8];
 #pragma unroll
@@ -254,9 +270,9 @@ __device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int
       unit_coords<KCONTIG>(u, R, r, q);
       uint4 pc[NS];
       split8n<NS>(f[i], pc);
-      const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
+      const uint32_t off = tile_off(r, q);
 #pragma unroll
-      for (int p = 0; p < NS; ++p) *reinterpret_cast<uint4*>(base + p * (R * 128) + off) = pc[p];
+      for (int p = 0; p < NS; ++p) *reinterpret_cast<uint4*>(base + p * (R * ROWB) + off) = pc[p];
     }
   }
 }
@@ -269,10 +285,10 @@ __device__ __forceinline__ void load_split_tile(const float* __restrict__ X, int
 template <int NS>
 __global__ void split_b_image(int64_t K, int64_t N, const float* __restrict__ B, int64_t b_rs, int64_t b_cs, int BN,
                               int64_t nkb, int64_t nblk, uint8_t* __restrict__ img) {
-  const int64_t total = nblk * nkb * BN * 8;
+  const int64_t total = nblk * nkb * BN * QPR;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(u & 7);
-    const int64_t rest0 = u >> 3;
+    const int q = (int)(u % QPR);
+    const int64_t rest0 = u / QPR;
     const int j = (int)(rest0 % BN);
     const int64_t rest = rest0 / BN;
     const int64_t kb = rest % nkb, nb = rest / nkb;
@@ -282,10 +298,10 @@ __global__ void split_b_image(int64_t K, int64_t N, const float* __restrict__ B,
     for (int t = 0; t < 8; ++t) f[t] = (gj < N && gk + t < K) ? B[(gk + t) * b_rs + gj * b_cs] : 0.f;
     uint4 pc[NS];
     split8n<NS>(f, pc);
-    uint8_t* tile = img + (nb * nkb + kb) * (int64_t)(NS * BN * 128);
-    const uint32_t off = (uint32_t)j * 128u + (uint32_t)((q ^ (j & 7)) << 4);
+    uint8_t* tile = img + (nb * nkb + kb) * (int64_t)(NS * BN * ROWB);
+    const uint32_t off = tile_off(j, q);
 #pragma unroll
-    for (int p = 0; p < NS; ++p) *reinterpret_cast<uint4*>(tile + p * BN * 128 + off) = pc[p];
+    for (int p = 0; p < NS; ++p) *reinterpret_cast<uint4*>(tile + p * BN * ROWB + off) = pc[p];
   }
 }
 
@@ -315,15 +331,16 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 // ring instead of by registers.
 template <bool KCONTIG, int NS>
 __device__ __forceinline__ void convert_tile_inplace(uint8_t* base, int gtid, int grp) {
-  constexpr int UPT = (TC_BM * 8) / TC_GROUP;
-  constexpr int A_TILE = TC_BM * 128;
+  constexpr int UPT = (TC_BM * QPR) / TC_GROUP;
+  constexpr int A_TILE = TC_BM * ROWB;
+  constexpr int FBOX = TC_BM * 128;  // one TMA box: 128 rows x 32 fp32 (128 B, SWIZZLE_128B)
   // K-contiguous tiles: each 8-lane phase takes one 16-B chunk index q of 8
-  // consecutive rows, whose SW128 positions (q ^ (r & 7)) are all distinct, so
-  // both the swizzled fp32 reads and the bf16 writes are bank-conflict free.
+  // consecutive rows, whose swizzled positions are all distinct, so both the
+  // fp32 reads and the bf16 writes are bank-conflict free.
   auto coords = [](int u, int& r, int& q) {
     if (KCONTIG) {
-      r = (u & 7) + 8 * (u >> 6);
-      q = (u >> 3) & 7;
+      r = (u & 7) + 8 * (u / (8 * QPR));
+      q = (u >> 3) % QPR;
     } else {
       unit_coords<false>(u, TC_BM, r, q);
     }
@@ -334,15 +351,15 @@ __device__ __forceinline__ void convert_tile_inplace(uint8_t* base, int gtid, in
     const int u = gtid + i * TC_GROUP;
     int r, q;
     coords(u, r, q);
-    if (KCONTIG) {
-      const uint8_t* row = base + (q >> 2) * (A_TILE) + r * 128;
+    if (KCONTIG) {  // fp32 k 8q..8q+7: box q / 4, 16-B granules 2 (q % 4) and +1 of the SW128 row
+      const uint8_t* row = base + (q >> 2) * FBOX + r * 128;
       const int g0 = (q & 3) * 2;
       const float4 a = *reinterpret_cast<const float4*>(row + ((g0 ^ (r & 7)) << 4));
       const float4 b = *reinterpret_cast<const float4*>(row + (((g0 + 1) ^ (r & 7)) << 4));
       f[i][0] = a.x; f[i][1] = a.y; f[i][2] = a.z; f[i][3] = a.w;
       f[i][4] = b.x; f[i][5] = b.y; f[i][6] = b.z; f[i][7] = b.w;
     } else {
-      const float* tile = reinterpret_cast<const float*>(base);  // [64 k][128 rows]
+      const float* tile = reinterpret_cast<const float*>(base);  // [TC_BK k][128 rows]
 #pragma unroll
       for (int t = 0; t < 8; ++t) f[i][t] = tile[(8 * q + t) * TC_BM + r];
     }
@@ -355,7 +372,7 @@ __device__ __forceinline__ void convert_tile_inplace(uint8_t* base, int gtid, in
     coords(u, r, q);
     uint4 pc[NS];
     split8n<NS>(f[i], pc);
-    const uint32_t off = (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4);
+    const uint32_t off = tile_off(r, q);
 #pragma unroll
     for (int p = 0; p < NS; ++p) *reinterpret_cast<uint4*>(base + p * A_TILE + off) = pc[p];
   }
@@ -382,12 +399,12 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   // symmetric products (C = A'A): tiles strictly below the diagonal are skipped
   // (uniformly for the whole CTA, before any barrier) and mirrored afterwards
   if (sym && (int64_t)blockIdx.x * TC_BM >= ((int64_t)blockIdx.y + 1) * BN) return;
-  constexpr int PKB = DF ? 4 : TC_PROMOTE_KB;
+  constexpr int PKB = DF ? 256 / TC_BK : TC_PROMOTE_KB;
   // DF also splits three ways (BF16x6: hh, hm, mh, hl, lh, mm ~ fp32-faithful
   // products, 1.9e-7 rel-F per SURVEY §7 hard part 5); otherwise BF16x3.
   constexpr int NS = DF ? 3 : 2;
-  constexpr int A_TILE = TC_BM * 128;  // bytes per bf16 tile (128 rows x 64 k)
-  constexpr int B_TILE = BN * 128;
+  constexpr int A_TILE = TC_BM * ROWB;  // bytes per bf16 tile (128 rows x TC_BK k)
+  constexpr int B_TILE = BN * ROWB;
   constexpr int STAGE = NS * (A_TILE + B_TILE);
   // TMEM: two MMA partial-sum buffers X0, X1 and the promoted accumulator Y.
   // The tensor core's fp32 accumulation does not round to nearest (measured:
@@ -462,9 +479,10 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         const uint32_t bar = smem_u32(&tfull[st]);
         mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 + NS * B_TILE));
         const int k0 = (int)(kbeg + (int64_t)kb * TC_BK);
-        if (A_KC) {
-          tma_load_2d_g2s(smem_u32(base), &amap, k0, (int)m0, bar);
-          tma_load_2d_g2s(smem_u32(base + A_TILE), &amap, k0 + 32, (int)m0, bar);
+        if (A_KC) {  // one 128-row x 32-fp32 SWIZZLE_128B box per 32 k
+#pragma unroll
+          for (int b = 0; b < TC_BK / 32; ++b)
+            tma_load_2d_g2s(smem_u32(base + b * TC_BM * 128), &amap, k0 + 32 * b, (int)m0, bar);
         } else {
           tma_load_2d_g2s(smem_u32(base), &amap, (int)m0, k0, bar);
         }
@@ -637,10 +655,10 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
                typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
                typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap) {
   constexpr int NS = DF ? 3 : 2;
-  constexpr size_t STAGE = NS * (TC_BM * 128 + BN * 128);
+  constexpr size_t STAGE = NS * (TC_BM * ROWB + BN * ROWB);
   const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
-  DevBuf img(NS * (size_t)BN * 128 * (size_t)(nkb * nblk), ctx->stream);
-  split_b_image<NS><<<grid_for(ctx, nblk * nkb * BN * 8, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb,
+  DevBuf img(NS * (size_t)BN * ROWB * (size_t)(nkb * nblk), ctx->stream);
+  split_b_image<NS><<<grid_for(ctx, nblk * nkb * BN * QPR, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb,
                                                                                        nblk, img.as<uint8_t>());
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
@@ -661,9 +679,9 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
                  int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
                  typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
                  typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap) {
-  // as many stages as fit in ~220 KB of shared memory (at most 4)
+  // as many stages as fit in ~220 KB of shared memory (at most TC_STAGES_MAX)
 #define RNLA_ST(BNV) \
-  std::min(4, (220 * 1024) / ((DF ? 3 : 2) * (TC_BM * 128 + (BNV) * 128)))
+  std::min(TC_STAGES_MAX, (220 * 1024) / ((DF ? 3 : 2) * (TC_BM * ROWB + (BNV) * ROWB)))
 #define RNLA_TC(BNV)                                                                                           \
   do {                                                                                                         \
     if (amap)                                                                                                  \
