@@ -24,6 +24,18 @@ void scale_rows_dev(rnla_ctx* ctx, int64_t r, int64_t n, const double* V, const 
 // out (n x r, col-major) = V * diag(d).
 void scale_cols_dev(rnla_ctx* ctx, int64_t n, int64_t r, const double* V, const double* d, double* out);
 double sum_squares_dev(rnla_ctx* ctx, const double* p, int64_t count);
+// out[e] uniform in [-1, 1) from a counter hash of (seed, e): deterministic start blocks.
+void hash_uniform_dev(rnla_ctx* ctx, int64_t count, uint64_t seed, double* out);
+// out[j] = |YZ(:, j) - theta[j] VZ(:, j)|^2 for n x k col-major YZ, VZ (theta on the device).
+void ritz_residual_dev(rnla_ctx* ctx, int64_t n, int64_t k, const double* YZ, const double* VZ, const double* theta,
+                       double* out);
+
+// Top-k eigenpairs of the symmetric n x n fp64 matrix A (device, col-major) by
+// block subspace iteration with Rayleigh-Ritz: lam (host, k, descending) and
+// V (device, n x k, matching columns). Returns false (outputs untouched) when
+// the problem is too small for a block of 2k or it did not converge; callers
+// then use the direct solver (api_linalg.cpp).
+bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, double* lam, double* V);
 
 // g = A'(beta*b - A w) and *rr = |beta*b - A w|^2 in one pass over the
 // row-major A (n x d, row stride ld; d <= 1024), fp64 accumulation; g and rr

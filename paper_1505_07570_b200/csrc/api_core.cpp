@@ -251,6 +251,50 @@ static void ctx_init(rnla_ctx* c, int device) {
   c->cublas = b;
 }
 
+static void ctx_release(rnla_ctx* ctx) {
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) {
+    ctx_release(ctx->side.get());
+    ctx->side.reset();
+  }
+  ctx->cs_plans.clear();
+  ctx->gauss_ops.clear();
+  ctx->srht_plans.clear();
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->green) {
+    for (auto s : {ctx->green->gather[0], ctx->green->gather[1], ctx->green->gemm}) cudaStreamSynchronize(s);
+    ctx->green.reset();
+  }
+  if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
+  if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
+  if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
+  ctx->nccl = ctx->cusolver = ctx->cublas = nullptr;
+  cudaStreamDestroy(ctx->copy_stream);
+  cudaStreamDestroy(ctx->aux_stream);
+  cudaStreamDestroy(ctx->stream);
+}
+
+}  // extern "C"
+
+namespace rnla {
+rnla_ctx* side_ctx(rnla_ctx* ctx) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!ctx->side) {
+    auto c = std::make_unique<rnla_ctx>();
+    ctx_init(c.get(), ctx->device);
+    // the main stream of the helper is the high-priority one
+    std::swap(c->stream, c->aux_stream);
+    cusolverDnSetStream(static_cast<cusolverDnHandle_t>(c->cusolver), c->stream);
+    cublasSetStream(static_cast<cublasHandle_t>(c->cublas), c->stream);
+    ctx->side = std::move(c);
+  }
+  return ctx->side.get();
+}
+}  // namespace rnla
+
+extern "C" {
+
 rnla_status rnla_ctx_create(int device, rnla_ctx** out) {
   return guard([&] {
     require(out != nullptr, "rnla_ctx_create: null out");
@@ -315,22 +359,7 @@ rnla_status rnla_ctx_create_dist(int device, int world, int rank, const void* nc
 
 void rnla_ctx_destroy(rnla_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
-  ctx->cs_plans.clear();
-  ctx->gauss_ops.clear();
-  ctx->srht_plans.clear();
-  cudaStreamSynchronize(ctx->stream);
-  if (ctx->green) {
-    for (auto s : {ctx->green->gather[0], ctx->green->gather[1], ctx->green->gemm}) cudaStreamSynchronize(s);
-    ctx->green.reset();
-  }
-  if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
-  if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
-  if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
-  cudaStreamDestroy(ctx->copy_stream);
-  cudaStreamDestroy(ctx->aux_stream);
-  cudaStreamDestroy(ctx->stream);
+  ctx_release(ctx);
   delete ctx;
 }
 

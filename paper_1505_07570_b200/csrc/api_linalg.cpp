@@ -6,6 +6,7 @@
 // src/sketch.cpp:125-167. Small factorizations run on the device in fp64
 // (linalg.cu); the passes over A are the GEMM kernels of gemm.cu.
 #include <cmath>
+#include <cstdio>
 #include <limits>
 #include <numeric>
 
@@ -232,6 +233,78 @@ struct KsvdWork {
     }
   }
 };
+
+// Block subspace iteration with Rayleigh-Ritz for the top-k eigenpairs of a
+// symmetric A (the Nystrom approx_eig subproblem M = T'(C'C)T, SURVEY §8(a)
+// row 20; the reference takes them from a full BDCSVD, src/spsd.cpp:257-265).
+// Block b = max(2k, k + 32): the top-k Ritz pairs converge at the rate
+// lam_{b+1} / lam_k per iteration (config 4: 0.065), and a cluster straddling
+// k (config 4: lam_64 / lam_65 = 1.0036) is resolved by the Rayleigh-Ritz step
+// inside the block rather than by the iteration. An iteration is one n x n x b
+// DMMA GEMM and one CholeskyQR pass; a Rayleigh-Ritz checkpoint (b x b eig,
+// ~2 ms of cuSOLVER latency at b = 128) runs after two iterations and then
+// after as many more as the Ritz values predict the residual needs. Converged
+// when every top-k residual |A v - theta v| <= 1e-12 theta_1.
+bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, double* lam, double* V) {
+  const int64_t b = std::max<int64_t>(2 * k, k + 32);
+  if (k < 1 || 2 * b > n || std::getenv("RNLA_EIG_DIRECT")) return false;
+  constexpr int kMaxIt = 80;
+  constexpr double kTol = 1e-12;
+  DevBuf Q(sizeof(double) * n * b, ctx->stream), Y(sizeof(double) * n * b, ctx->stream),
+      H(sizeof(double) * b * b, ctx->stream), Hs(sizeof(double) * b * b, ctx->stream),
+      th(sizeof(double) * b, ctx->stream), Zk(sizeof(double) * b * k, ctx->stream),
+      YZ(sizeof(double) * n * k, ctx->stream), VZ(sizeof(double) * n * k, ctx->stream),
+      thd(sizeof(double) * k, ctx->stream), res(sizeof(double) * k, ctx->stream);
+  hash_uniform_dev(ctx, n * b, 0x6a09e667f3bcc909ull, Y.as<double>());
+  std::vector<double> ht((size_t)b), hr((size_t)k), td((size_t)k);
+  int next_rr = 2, rr_count = 0;
+  for (int it = 0; it < kMaxIt; ++it) {
+    // Q = orth(Y) (CholeskyQR2 + Householder fallback at checkpoints, one
+    // CholeskyQR pass in between); Y = A Q
+    const bool rr = it == next_rr;
+    RNLA_CUDA(cudaMemcpyAsync(Q.p, Y.p, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (rr || !cholqr_inplace(ctx, n, b, Q.as<double>())) {
+      RNLA_CUDA(cudaMemcpyAsync(Q.p, Y.p, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, ctx->stream));
+      KsvdWork<double>::orth(ctx, n, b, Q.as<double>(), false);
+    }
+    gemm<double>(ctx, n, b, n, 1.0, A, 1, n, Q.as<double>(), 1, n, 0.0, Y.as<double>(), 1, n);
+    if (!rr) continue;
+    ++rr_count;
+    // Rayleigh-Ritz: H = Q'AQ = (Z, theta); top-k Ritz vectors Q Z_k, images Y Z_k
+    gemm<double>(ctx, b, b, n, 1.0, Q.as<double>(), n, 1, Y.as<double>(), 1, n, 0.0, H.as<double>(), 1, b);
+    symmetrize(ctx, b, H.as<double>(), Hs.as<double>());
+    eig_sym(ctx, b, Hs.as<double>(), th.as<double>());  // ascending
+    RNLA_CUDA(cudaMemcpyAsync(ht.data(), th.p, sizeof(double) * b, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < k; ++t) td[(size_t)t] = ht[(size_t)(b - 1 - t)];
+    copy2d<double>(ctx, b, k, Hs.as<double>() + (b - 1) * b, 1, -b, Zk.as<double>(), 1, b);
+    gemm<double>(ctx, n, k, b, 1.0, Q.as<double>(), 1, n, Zk.as<double>(), 1, b, 0.0, VZ.as<double>(), 1, n);
+    gemm<double>(ctx, n, k, b, 1.0, Y.as<double>(), 1, n, Zk.as<double>(), 1, b, 0.0, YZ.as<double>(), 1, n);
+    RNLA_CUDA(cudaMemcpyAsync(thd.p, td.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
+    ritz_residual_dev(ctx, n, k, YZ.as<double>(), VZ.as<double>(), thd.as<double>(), res.as<double>());
+    RNLA_CUDA(cudaMemcpyAsync(hr.data(), res.p, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double top = std::abs(td[0]);
+    if (!(top > 0.0)) return false;
+    double worst = 0.0;
+    for (int64_t t = 0; t < k; ++t) worst = std::max(worst, std::sqrt(hr[(size_t)t]) / top);
+    if (worst <= kTol) {
+      std::copy(td.begin(), td.end(), lam);
+      RNLA_CUDA(cudaMemcpyAsync(V, VZ.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      char label[96];
+      std::snprintf(label, sizeof label, "eig_top_subspace: %d iterations, %d Rayleigh-Ritz", it, rr_count);
+      trace_mark(ctx, label);
+      return true;
+    }
+    // iterations to the tolerance at the rate theta_b / theta_k (the Ritz
+    // values under-estimate lam_b, so cap the rate from below and re-check)
+    const double rate = std::min(0.9, std::max(0.02, std::abs(ht[0]) / std::abs(td[(size_t)k - 1])));
+    const double need = std::log(kTol / worst) / std::log(rate);
+    next_rr = it + std::max(1, std::min(20, (int)std::ceil(need)));
+  }
+  return false;
+}
 
 template <class T>
 void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, uint64_t seed,

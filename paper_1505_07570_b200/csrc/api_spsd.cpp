@@ -4,7 +4,9 @@
 // Reference: /root/reference/proj/src/spsd.cpp:33-72 (rbf_kernel, KernelView),
 // :181-222 (nystrom), :257-265 (approx_eig).
 #include <cmath>
+#include <exception>
 #include <limits>
+#include <thread>
 
 #include "algos.h"
 #include "dist.h"
@@ -163,10 +165,79 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   const int64_t r_off = global_row_offset(ctx, n_local, &n);
   const int64_t kk = target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
   require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
+  trace_mark(ctx, "nystrom_eig: enter");
   Landmarks L = landmarks<T>(ctx, X, s, seed, n, r_off);
+  trace_mark(ctx, "nystrom_eig: landmarks");
   const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(n_local, 16384));
   DevBuf Cb(sizeof(T) * blk * s, ctx->stream);
   DevBuf G(sizeof(double) * s * s, ctx->stream), W(sizeof(double) * s * s, ctx->stream);
+  // W = K[S, S]: its rows are the landmark rows of C (recomputed directly).
+  {
+    DevBuf Wt(sizeof(T) * s * s, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
+    std::vector<int64_t> id((size_t)s);
+    for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
+    RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    rbf_block<T>(ctx, s, s, X.cols, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, nullptr,
+                 L.sqS.as<T>(), L.sqS.as<T>(), sigma, ident.as<int64_t>(), Wt.as<T>(), 1, s);
+    if constexpr (std::is_same<T, double>::value)
+      RNLA_CUDA(cudaMemcpyAsync(W.p, Wt.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      copy2d_cast<float, double>(ctx, s, s, Wt.as<float>(), 1, s, W.as<double>(), 1, s);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  trace_mark(ctx, "nystrom_eig: W");
+  // Full-rank route. When target_k >= s and every eigenvalue of W clears the
+  // floor, the reference keeps all of them: L = C U Lambda^-1/2 = C W^-1/2,
+  // and approx_eig(L) depends on L only through L L' = C W^-1 C'. With the
+  // Cholesky factor W = R'R, L' = C R^-1 has the same L L', hence the same
+  // singular values and left singular vectors, so eig(W) (a 28 ms cuSOLVER
+  // tridiagonalization at s = 2048) becomes potrf + one triangular inverse.
+  // The floor test is conservative: lam_min(W) >= 1 / |R^-1|_F^2 and
+  // lam_max(W) <= |W|_F, with a 4x margin (config 4: lam_min / floor = 6.8e3).
+  // Otherwise the eigendecomposition route below runs.
+  DevBuf Tm;  // s x kp: L = C Tm
+  int64_t kp = 0;
+  if (kk >= s && !std::getenv("RNLA_NYSTROM_EIGW")) {
+    DevBuf Ws(sizeof(double) * s * s, ctx->stream), R(sizeof(double) * s * s, ctx->stream),
+        Ri(sizeof(double) * s * s, ctx->stream);
+    symmetrize(ctx, s, W.as<double>(), Ws.as<double>());
+    RNLA_CUDA(cudaMemcpyAsync(R.p, Ws.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (cholesky_upper(ctx, s, R.as<double>())) {
+      upper_inverse(ctx, s, R.as<double>(), Ri.as<double>());
+      const double inv_fro2 = sum_squares_dev(ctx, Ri.as<double>(), s * s);
+      const double w_fro = std::sqrt(sum_squares_dev(ctx, Ws.as<double>(), s * s));
+      const double floor_ub = std::numeric_limits<double>::epsilon() * w_fro * static_cast<double>(n);
+      if (std::isfinite(inv_fro2) && inv_fro2 > 0.0 && 1.0 / inv_fro2 > 4.0 * floor_ub) {
+        Tm = std::move(Ri);
+        kp = s;
+      }
+    }
+    trace_mark(ctx, "nystrom_eig: Cholesky route test");
+  }
+  // Otherwise eig(W) (cuSOLVER syevd, latency-bound) runs on the helper
+  // context from a second host thread while this thread accumulates C'C
+  // (DMMA-bound), its kernels dispatched first from the high-priority stream.
+  EigW e;
+  std::exception_ptr eig_err;
+  const bool need_eig = kp == 0;
+  const bool overlap = need_eig && !std::getenv("RNLA_NYSTROM_SERIAL");
+  rnla_ctx* side = overlap ? side_ctx(ctx) : nullptr;
+  std::thread eig_thread;
+  if (overlap)
+    eig_thread = std::thread([&] {
+      try {
+        RNLA_CUDA(cudaSetDevice(side->device));
+        e = nystrom_core(side, W.as<double>(), s, n, kk);
+      } catch (...) {
+        eig_err = std::current_exception();
+      }
+    });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{eig_thread};
   RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * s * s, ctx->stream));
   for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
     const int64_t rows = std::min(blk, n_local - r0);
@@ -184,56 +255,59 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
                       s);
   }
   if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(s * s), RNLA_F64);  // C'C over row shards
-  // W = K[S, S]: its rows are the landmark rows of C (recomputed directly).
-  {
-    DevBuf Wt(sizeof(T) * s * s, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
-    std::vector<int64_t> id((size_t)s);
-    for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
-    RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
-    rbf_block<T>(ctx, s, s, X.cols, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, nullptr,
-                 L.sqS.as<T>(), L.sqS.as<T>(), sigma, ident.as<int64_t>(), Wt.as<T>(), 1, s);
-    if constexpr (std::is_same<T, double>::value)
-      RNLA_CUDA(cudaMemcpyAsync(W.p, Wt.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
-    else
-      copy2d_cast<float, double>(ctx, s, s, Wt.as<float>(), 1, s, W.as<double>(), 1, s);
-    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  trace_mark(ctx, "nystrom_eig: C'C gram");
+  if (overlap) {
+    eig_thread.join();
+    if (eig_err) std::rethrow_exception(eig_err);
+    ctx->launches += side->launches;
+    side->launches = 0;
+  } else if (need_eig) {
+    e = nystrom_core(ctx, W.as<double>(), s, n, kk);
   }
-  EigW e = nystrom_core(ctx, W.as<double>(), s, n, kk);
-  require(k >= 1 && k <= e.kept, "approx_eig: k exceeds rank(L)");
-  DevBuf Tm = whitened(ctx, e, s);  // s x kept
-  // M = T' G T (kept x kept), symmetric
-  const int64_t kp = e.kept;
+  if (need_eig) {
+    trace_mark(ctx, "nystrom_eig: eig(W)");
+    Tm = whitened(ctx, e, s);
+    kp = e.kept;
+  }
+  require(k >= 1 && k <= kp, "approx_eig: k exceeds rank(L)");
+  // M = T' G T (kp x kp), symmetric
   DevBuf GT(sizeof(double) * s * kp, ctx->stream), M(sizeof(double) * kp * kp, ctx->stream),
       Ms(sizeof(double) * kp * kp, ctx->stream), ev(sizeof(double) * kp, ctx->stream);
   gemm<double>(ctx, s, kp, s, 1.0, G.as<double>(), 1, s, Tm.as<double>(), 1, s, 0.0, GT.as<double>(), 1, s);
   gemm<double>(ctx, kp, kp, s, 1.0, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, 0.0, M.as<double>(), 1, kp);
   symmetrize(ctx, kp, M.as<double>(), Ms.as<double>());
-  // Only the top k eigenpairs are needed: syevdx on an index range when k is
-  // well below kp (most of the back-transformation is skipped), else syevd.
+  trace_mark(ctx, "nystrom_eig: M = T'GT");
+  // Only the top k eigenpairs are needed: block subspace iteration (a few
+  // n x n x 2k GEMMs) when k is well below kp, else syevdx on an index range,
+  // else the full syevd.
   std::vector<double> top((size_t)k);
-  const double* vtop = nullptr;  // eigenvector of the largest eigenvalue; the next ones at stride -kp
-  if (2 * k <= kp && !std::getenv("RNLA_EIG_FULL")) {
-    const int64_t found = eig_sym_top(ctx, kp, Ms.as<double>(), k, ev.as<double>());
-    if (found != k) throw NumericError("approx_eig: partial eigensolver returned fewer pairs");
-    std::vector<double> h((size_t)k);
-    RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
-    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int64_t t = 0; t < k; ++t) top[(size_t)t] = h[(size_t)(k - 1 - t)];
-    vtop = Ms.as<double>() + (k - 1) * kp;
-  } else {
-    eig_sym(ctx, kp, Ms.as<double>(), ev.as<double>());
-    std::vector<double> h((size_t)kp);
-    RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * kp, cudaMemcpyDeviceToHost, ctx->stream));
-    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int64_t t = 0; t < k; ++t) top[(size_t)t] = h[(size_t)(kp - 1 - t)];
-    vtop = Ms.as<double>() + (kp - 1) * kp;
+  DevBuf Vk(sizeof(double) * kp * k, ctx->stream);  // descending eigenvectors
+  if (!eig_top_subspace(ctx, kp, Ms.as<double>(), k, top.data(), Vk.as<double>())) {
+    const double* vtop = nullptr;  // eigenvector of the largest eigenvalue; the next ones at stride -kp
+    if (2 * k <= kp && !std::getenv("RNLA_EIG_FULL")) {
+      const int64_t found = eig_sym_top(ctx, kp, Ms.as<double>(), k, ev.as<double>());
+      if (found != k) throw NumericError("approx_eig: partial eigensolver returned fewer pairs");
+      std::vector<double> h((size_t)k);
+      RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t t = 0; t < k; ++t) top[(size_t)t] = h[(size_t)(k - 1 - t)];
+      vtop = Ms.as<double>() + (k - 1) * kp;
+    } else {
+      eig_sym(ctx, kp, Ms.as<double>(), ev.as<double>());
+      std::vector<double> h((size_t)kp);
+      RNLA_CUDA(cudaMemcpyAsync(h.data(), ev.p, sizeof(double) * kp, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t t = 0; t < k; ++t) top[(size_t)t] = h[(size_t)(kp - 1 - t)];
+      vtop = Ms.as<double>() + (kp - 1) * kp;
+    }
+    copy2d<double>(ctx, kp, k, vtop, 1, -kp, Vk.as<double>(), 1, kp);
   }
   for (int64_t t = 0; t < k; ++t) lam_out[t] = top[(size_t)t];
+  trace_mark(ctx, "nystrom_eig: top-k eig(M)");
   if (u_out) {
     // P = T V_k diag(1/sigma) (s x k), U = C P, sign-fixed like condensed_svd's U.
-    DevBuf Vk(sizeof(double) * kp * k, ctx->stream), P(sizeof(double) * s * k, ctx->stream),
-        isg(sizeof(double) * k, ctx->stream), Vs(sizeof(double) * kp * k, ctx->stream);
-    copy2d<double>(ctx, kp, k, vtop, 1, -kp, Vk.as<double>(), 1, kp);
+    DevBuf P(sizeof(double) * s * k, ctx->stream), isg(sizeof(double) * k, ctx->stream),
+        Vs(sizeof(double) * kp * k, ctx->stream);
     std::vector<double> inv((size_t)k);
     for (int64_t t = 0; t < k; ++t) inv[(size_t)t] = 1.0 / std::sqrt(top[(size_t)t]);
     RNLA_CUDA(cudaMemcpyAsync(isg.p, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
@@ -262,6 +336,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
     fix_column_signs_sharded<double>(ctx, n_local, k, U64.as<double>(), 1, n_local, nullptr, 0, 0, 0, true);
     store_block(ctx, U64.as<double>(), n_local, k, n_local, uo);
     uo.finish(ctx);
+    trace_mark(ctx, "nystrom_eig: U lift");
   }
   std::copy(L.sel.begin(), L.sel.end(), selected);
   *kept_out = kp;

@@ -85,8 +85,15 @@ struct TileLoader {
 // element type (float inputs are widened exactly to fp64 on the way to smem).
 // NB = 64: 2 x 2 warps of 32 x 32; NB = 32 (narrow outputs such as the
 // s = 30 sketches of config 0): 4 x 1 warps of 16 x 32, so no half-empty tiles.
-template <class TI, int NB = BN>
-__global__ void __launch_bounds__(THREADS) gemm_f64_dmma(int64_t m, int64_t n, int64_t kdim, int64_t kchunk,
+// MINB = resident CTAs per SM the register allocation must allow: 3 for the
+// fp64-input 64-wide tile (244 -> 168 registers, no spills), 4 for the
+// fp32-input Gram tile, which then covers a 2048^2 symmetric Gram (528 tiles)
+// in one wave of 592 slots instead of two of 444.
+#ifndef RNLA_DMMA_F32_MINB
+#define RNLA_DMMA_F32_MINB 4
+#endif
+template <class TI, int NB = BN, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB) gemm_f64_dmma(int64_t m, int64_t n, int64_t kdim, int64_t kchunk,
                                                          double alpha, const TI* __restrict__ A, int64_t a_rs,
                                                          int64_t a_cs, const TI* __restrict__ B, int64_t b_rs,
                                                          int64_t b_cs, double beta, double* C, int64_t c_rs,
@@ -291,10 +298,10 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
   dim3 grid((unsigned)((n + nb - 1) / nb), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
   if constexpr (std::is_same<T, double>::value) {
     if (nb == 32)
-      gemm_f64_dmma<double, 32><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs,
+      gemm_f64_dmma<double, 32, 1><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs,
                                                                    b_cs, beta, C, c_rs, c_cs, wsp, 0);
     else
-      gemm_f64_dmma<double><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs,
+      gemm_f64_dmma<double, 64, 3><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs,
                                                                beta, C, c_rs, c_cs, wsp, 0);
   } else {
     gemm_f32_simt<<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C,
@@ -310,15 +317,38 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
   }
 }
 
+// Smallest split-K count whose CTAs keep >= 85 % of the last wave of `slots`
+// busy (else the best one), with >= 256 k per split.
+static int64_t wave_splits(int64_t active, int64_t slots, int64_t k, int64_t cap) {
+  if (active <= 0 || slots <= 0 || k < 512) return 1;
+  int64_t best = 1;
+  double best_eff = 0.0;
+  for (int64_t s = 1; s <= std::max<int64_t>(1, std::min<int64_t>(cap, k / 256)); ++s) {
+    const int64_t ctas = active * s;
+    const double eff = (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+    if (eff >= 0.85) return s;
+    if (eff > best_eff + 1e-9) best_eff = eff, best = s;
+  }
+  return best;
+}
+
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                      int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
                      int64_t c_cs) {
   if (m == 0 || n == 0) return;
-  const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
-  int64_t splits = 1;
-  const int64_t want = (int64_t)ctx->num_sms * 4;
-  if (tiles < want && k >= 512)
-    splits = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>((want + tiles - 1) / tiles, k / 256), 64));
+  // Gram products (B = A') are symmetric: compute the upper tiles only.
+  const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs) ? 1 : 0;
+  const int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
+  const int64_t active = sym ? tm * (tm + 1) / 2 : tm * tn;
+  static const int per_sm = [] {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gemm_f64_dmma<float, 64, RNLA_DMMA_F32_MINB>, THREADS, 0) !=
+            cudaSuccess ||
+        b < 1)
+      b = 1;
+    return b;
+  }();
+  int64_t splits = wave_splits(active, (int64_t)per_sm * ctx->num_sms, k, 64);
   int64_t kchunk = ((k + splits - 1) / splits + BK - 1) / BK * BK;
   if (k == 0) kchunk = BK;
   splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
@@ -328,10 +358,8 @@ void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alph
     ws = DevBuf(sizeof(double) * (size_t)(splits * m * n), ctx->stream);
     wsp = ws.as<double>();
   }
-  // Gram products (B = A') are symmetric: compute the upper tiles only.
-  const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs) ? 1 : 0;
   dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
-  gemm_f64_dmma<float><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta,
+  gemm_f64_dmma<float, 64, RNLA_DMMA_F32_MINB><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta,
                                                           C, c_rs, c_cs, wsp, sym);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);

@@ -284,6 +284,19 @@ bool cholesky_upper(rnla_ctx* ctx, int64_t n, double* G) {
   return hinfo == 0;
 }
 
+bool cholqr_inplace(rnla_ctx* ctx, int64_t m, int64_t n, double* Y) {
+  DevBuf G(sizeof(double) * n * n, ctx->stream);
+  gemm<double>(ctx, n, n, m, 1.0, Y, m, 1, Y, 1, m, 0.0, G.as<double>(), 1, n);
+  if (!cholesky_upper(ctx, n, G.as<double>())) return false;
+  const double one = 1.0;
+  if (cublasDtrsm(static_cast<cublasHandle_t>(ctx->cublas), CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                  CUBLAS_DIAG_NON_UNIT, (int)m, (int)n, &one, G.as<double>(), (int)n, Y, (int)m) !=
+      CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDtrsm failed");
+  note_launch(ctx);
+  return true;
+}
+
 bool diag_ratio_ok(rnla_ctx* ctx, int64_t n, const double* R, double thresh) {
   std::vector<double> d((size_t)n);
   RNLA_CUDA(cudaMemcpy2DAsync(d.data(), sizeof(double), R, sizeof(double) * (n + 1), sizeof(double), n,

@@ -32,6 +32,9 @@ void svd_thin(rnla_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t a_rs
 
 // In-place upper Cholesky G = R'R of column-major G (n x n); false if not positive definite.
 bool cholesky_upper(rnla_ctx* ctx, int64_t n, double* G);
+// One CholeskyQR pass on the m x n col-major Y in place (Y := Y R^-1, R'R = Y'Y);
+// false (Y untouched) on a Cholesky breakdown.
+bool cholqr_inplace(rnla_ctx* ctx, int64_t m, int64_t n, double* Y);
 // min |R_ii| > thresh * max |R_ii| and all finite (CholeskyQR breakdown test).
 bool diag_ratio_ok(rnla_ctx* ctx, int64_t n, const double* R, double thresh);
 // Rinv = R^-1 for upper-triangular column-major R (entries below the diagonal ignored).

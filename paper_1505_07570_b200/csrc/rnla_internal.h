@@ -121,6 +121,10 @@ struct rnla_ctx {
   std::map<std::tuple<int64_t, int64_t, uint64_t>, std::shared_ptr<rnla::SrhtPlan>> srht_plans;
   std::unique_ptr<rnla::GreenSplit> green;  // lazily created (combined sketch pipelining)
   bool green_tried = false;
+  // Helper context on the same device (own high-priority stream and library
+  // handles) for independent work run from a second host thread, e.g. eig(W)
+  // under the Nystrom C'C Gram; created lazily by side_ctx().
+  std::unique_ptr<rnla_ctx> side;
 };
 
 namespace rnla {
@@ -152,6 +156,8 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
 // Phase tracing (RNLA_TRACE=1): synchronizes the context stream and prints the
 // wall time since the previous mark of this thread to stderr. No-op otherwise.
 void trace_mark(rnla_ctx* ctx, const char* label);
+// The lazily created helper context of ctx (see rnla_ctx::side); world 1, no group.
+rnla_ctx* side_ctx(rnla_ctx* ctx);
 
 // Temporarily route ctx launches to another stream (RAII).
 struct StreamScope {

@@ -161,7 +161,52 @@ __global__ void sumsq_kernel(const double* __restrict__ p, int64_t count, double
     if (threadIdx.x == 0) partial[blockIdx.x] = v;
   }
 }
+__global__ void hash_uniform_kernel(int64_t count, uint64_t seed, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(e + 1));
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    out[e] = (double)(z >> 11) * 0x1.0p-52 - 1.0;
+  }
+}
+// out[j] = |YZ(:, j) - theta[j] * VZ(:, j)|^2, one block per column
+__global__ void ritz_residual_kernel(int64_t n, const double* __restrict__ YZ, const double* __restrict__ VZ,
+                                     const double* __restrict__ theta, double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  const double t = theta[j];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double r = YZ[i + j * n] - t * VZ[i + j * n];
+    acc += r * r;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) out[j] = v;
+  }
+}
 }  // namespace
+
+void hash_uniform_dev(rnla_ctx* ctx, int64_t count, uint64_t seed, double* out) {
+  if (count == 0) return;
+  hash_uniform_kernel<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(count, seed, out);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+void ritz_residual_dev(rnla_ctx* ctx, int64_t n, int64_t k, const double* YZ, const double* VZ, const double* theta,
+                       double* out) {
+  if (k == 0) return;
+  ritz_residual_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(n, YZ, VZ, theta, out);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
 
 void scale_rows_dev(rnla_ctx* ctx, int64_t r, int64_t n, const double* V, const double* s, double* out) {
   if (r * n == 0) return;

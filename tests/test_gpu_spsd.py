@@ -86,6 +86,39 @@ def test_nystrom_eig_gram_route_matches_oracle(ctx):
     assert np.max(np.abs(np.abs(u[:, :4]) - np.abs(uo[:, :4]))) <= 1e-6
 
 
+@pytest.mark.parametrize("n,s,k,sigma", [(3000, 200, 12, 3.0), (6000, 400, 40, 4.0)])
+def test_nystrom_eig_full_rank_route(ctx, n, s, k, sigma):
+    # target_k = s with a well-conditioned W: the Cholesky route (L' = C R^-1)
+    # replaces eig(W); approx_eig outputs must match the reference's eig route.
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 8)) * 2
+    view = rn.KernelView(x, rn.KernelSpec(sigma))
+    u, lam, sel, kept = rn.nystrom_eig(view, s, 9, s, k, ctx=ctx)
+    L, sel_o, lam_w = orc.nystrom(x, sigma, s, 9, s)
+    uo, lo = orc.approx_eig(L, k)
+    assert kept == L.shape[1] == s and np.array_equal(sel, sel_o)
+    assert np.max(np.abs(lam - lo) / lo) <= 1e-8
+    # sign-fixed columns, compared where the eigenvalue is separated from its neighbours
+    rel = np.abs(np.diff(lo)) / lo[1:]
+    sep = [t for t in range(k - 1) if rel[t] > 1e-3 and (t == 0 or rel[t - 1] > 1e-3)]
+    assert sep
+    assert np.max(np.abs(u[:, sep] - uo[:, sep])) <= 1e-6
+
+
+def test_nystrom_eig_rank_deficient_falls_back(ctx):
+    # duplicated points make W singular: the floor drops eigenvalues (kept < s),
+    # so the eigendecomposition route must run and match the oracle.
+    rng = np.random.default_rng(11)
+    base = rng.standard_normal((400, 3))
+    x = np.vstack([base, base, base])
+    view = rn.KernelView(x, rn.KernelSpec(2.0))
+    _, lam, sel, kept = rn.nystrom_eig(view, 300, 5, 300, 6, ctx=ctx)
+    L, sel_o, _ = orc.nystrom(x, 2.0, 300, 5, 300)
+    _, lo = orc.approx_eig(L, 6)
+    assert np.array_equal(sel, sel_o) and kept == L.shape[1] < 300
+    assert np.max(np.abs(lam - lo) / lo) <= 1e-6
+
+
 def test_nystrom_eig_fp32(ctx):
     rng = np.random.default_rng(5)
     means = rng.standard_normal((4, 16)) * 3
