@@ -337,6 +337,7 @@ void srht_segments(rnla_ctx* ctx, const SrhtPlan& plan, const T* in, int64_t ld,
                    int64_t out_cs) {
   if (L == 0) return;
   if constexpr (std::is_same<T, float>::value) {
+    if (!std::getenv("RNLA_SRHT_GENERIC") && srht_acc_f32(ctx, plan, in, ld, L, out, out_rs, out_cs)) return;
     if (!std::getenv("RNLA_SRHT_GENERIC") && srht_tma_f32(ctx, plan, in, ld, L, out, out_rs, out_cs)) return;
   }
   if (!std::getenv("RNLA_SRHT_GENERIC") && srht_fast<T>(ctx, plan, in, ld, L, out, out_rs, out_cs)) return;

@@ -1,5 +1,7 @@
 // srht.h -- SRHT operator plan (signs, sampled indices grouped by low bits).
 #pragma once
+#include <cuda.h>
+
 #include "rnla_internal.h"
 
 namespace rnla {
@@ -13,6 +15,9 @@ struct SrhtPlan {
   DevBuf grp_off, grp_t, grp_hi;   // samples grouped by idx & (2^qlo - 1)
   int64_t block_off = 0;           // block plans: global index of the block's first row
   DevBuf out_sign;                 // block plans: (-1)^popcount(block_off & idx_t), fp64[s]
+  // One-pass accumulating path (srht_acc.cu), built on first use: per-(tile,
+  // row-group) sign bit masks and the packed (high, low) bits of each sample.
+  mutable DevBuf acc_mask, acc_samp;
   SrhtPlan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed);
   // Plan of one aligned block (2^b rows at block_off, `present` of them real)
   // of a global operator whose sampled indices are idx[0..s).
@@ -32,6 +37,17 @@ inline int64_t srht_strip_mb() {
 // TMA-fed fp32 path (srht_tma.cu); false when the shape/alignment does not apply.
 bool srht_tma_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
                   int64_t out_rs, int64_t out_cs);
+
+// One-pass fp32 path with the sampled outputs accumulated in TMEM
+// (srht_acc.cu); false when the shape/alignment does not apply.
+bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
+                  int64_t out_rs, int64_t out_cs);
+
+// TMA tensor map over a row-major fp32 matrix (rows x cols, row pitch ld
+// elements), boxes of box_rows x box_cols (srht_tma.cu).
+bool tma_encode_available();
+void tma_map_rows_f32(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols,
+                      uint32_t box_rows);
 
 // out_t[c] (t < s, c < L) at out[t*out_rs + c*out_cs]; segment j at in + j*ld.
 template <class T>

@@ -1,0 +1,386 @@
+// srht_acc.cu -- one-pass fp32 SRHT: every sampled output is accumulated on
+// chip, so A is read from HBM exactly once and nothing of size n is written.
+//
+// Reference: srht_sketch / fwht_inplace (/root/reference/proj/src/sketch.cpp:44-81):
+//   out[t][c] = (1/sqrt(s)) * sum_j (-1)^popcount(idx_t & j) * sign_j * A[j][c].
+// With j = 4096*jh + jl and idx_t = 4096*th + tl (Sylvester order):
+//   out[t] = (1/sqrt s) * sum_jh (-1)^popcount(th & jh) * Y_jh[tl],
+//   Y_jh   = H_4096 (sign . A[4096 jh .. 4096 jh + 4095])       (one tile)
+// so each 4096-row tile needs only its own 12-bit transform, and every one of
+// the s <= 4096 sampled outputs receives one signed add per tile.
+//
+// Work: a CTA owns an 8-column slice (one 32-B sector per row) and a run of
+// consecutive tiles. The tile lives in registers (512 threads x 64 values):
+//   phase 1: thread (g, c) takes rows g + 64e (e < 64) from the TMA ring as
+//            the chunks land, sign flip, 6 register stages over e (bits 6-11);
+//   phase 2: through a swizzled smem tile, thread (a, c) takes rows 64a + b,
+//            6 register stages over b (bits 0-5), Y written back in place;
+//   gather : thread t owns samples 8t .. 8t+7 (all 8 columns = 64 fp32) whose
+//            running sums live in TMEM (tcgen05.ld / tcgen05.st, 256 columns)
+//            and adds (-1)^popcount(th & jh) * Y[tl] from smem.
+// Four consecutive CTAs take the four 8-column slices of one 128-B line over
+// the same tile run, so each line is fetched from HBM once. A run that crosses
+// a slice boundary flushes its sums to a partial buffer; a small finalize
+// kernel adds the (<= 3) partials of each slice in a fixed order and scales.
+// The stage order differs from the reference loop, so results agree to fp32
+// rounding (gate 1e-4 rel-F), not bitwise; the fp64 path stays bit-exact.
+#include <cuda.h>
+
+#include "rnla_internal.h"
+#include "srht.h"
+#include "util.cuh"
+
+namespace rnla {
+
+namespace {
+
+constexpr int LO = 12, ROWS = 1 << LO;  // rows per tile
+constexpr int W = 8;                     // fp32 columns per CTA
+constexpr int NT = 512;                  // threads: 64 row groups x 8 columns
+constexpr int CH = 512;                  // rows per chunk (16 KB = two 256-row TMA boxes)
+constexpr int NCH = ROWS / CH;           // 8 chunks per tile
+constexpr int EPC = CH / 64;             // values per thread per chunk
+constexpr int RING = 6;                  // chunk slots (96 KB in flight)
+constexpr int SMAX = 4096;               // sampled outputs held on chip
+constexpr int TMEM_COLS = 256;           // 128 lanes x 256 fp32 = 4096 samples x 8 columns
+static_assert(NCH == 8, "chunk N belongs to tile N >> 3");
+
+constexpr size_t RING_BYTES = (size_t)RING * CH * W * 4;
+constexpr size_t TILE_BYTES = (size_t)ROWS * W * 4;
+constexpr size_t SMEM_BYTES = RING_BYTES + TILE_BYTES + 2 * RING * 8 + 16;
+
+struct AccArgs {
+  const unsigned long long* mask;  // [JH][64]: bit e of (jh, g) = sign of row 4096 jh + g + 64 e is -1
+  const uint32_t* samp;            // [SMAX]: tl | th << 12
+  float* part;                     // [KQ * segmax][4][SMAX][W] running sums per (run segment, slice)
+  int64_t qt;                      // quad-tiles = Q * JH (quad = 4 slices = 32 columns)
+  int jh_count, jh_log, kq, segmax;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]), "=r"(u[8]),
+        "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]), "r"(u[8]), "r"(u[9]),
+      "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])
+      : "memory");
+}
+
+// Physical row of tile row r: the low two bits are XORed with bits 6-7, so the
+// four row groups a warp touches in phase 2 (rows 64a + b, a = 4w..4w+3) sit in
+// different 8-bank groups; phase 1 (rows g + 64e) stays conflict-free too.
+__device__ __forceinline__ int swz(int r) { return r ^ ((r >> 6) & 3); }
+
+__device__ __forceinline__ void butterfly64(float* v) {
+#pragma unroll
+  for (int h = 1; h < 64; h <<= 1)
+#pragma unroll
+    for (int e = 0; e < 64; ++e)
+      if (!(e & h)) {
+        const float x = v[e], y = v[e + h];
+        v[e] = x + y;
+        v[e + h] = x - y;
+      }
+}
+
+__global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__ CUtensorMap amap, AccArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);               // [RING][CH][W]
+  float* tile = reinterpret_cast<float*>(smem + RING_BYTES);  // [ROWS][W], swizzled rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + TILE_BYTES);  // full[RING], empty[RING]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RING);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = tid >> 3, c = tid & 7;  // phase 1: row group g; phase 2: row group a = g
+  const int kq = blockIdx.x >> 2, r = blockIdx.x & 3;
+  const int64_t start = (int64_t)kq * a.qt / a.kq, end = (int64_t)(kq + 1) * a.qt / a.kq;
+  const int ntiles = (int)(end - start);
+  const int jhn = a.jh_count;
+  const int q_first = (int)(start / jhn);
+  const int total_chunks = ntiles * NCH;
+
+  if (tid == 0) {
+    for (int i = 0; i < RING; ++i) {
+      mbar_init(su32(&bars[i]), 1);              // full: one expect_tx arrival + the bytes
+      mbar_init(su32(&bars[RING + i]), NT / 32);  // empty: one arrival per warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+  // this warp's TMEM window: lanes 32 (warp % 4) .., columns 64 (warp / 4) ..
+  const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+
+  const int qt0 = (int)start;  // quad-tile indices fit in int (Q * JH <= 2^30 checked on the host)
+  // Producer (thread 0): chunk N lands in slot N % RING. After reading chunk G
+  // it waits until every warp has read chunk G - 1 (usually long done) and
+  // refills that slot with chunk G + RING - 1, so RING - 1 chunks stay in flight
+  // through phase 2 and the gather.
+  auto issue = [&](int N, int slot) {
+    const int qti = qt0 + (N >> 3), kk = N & (NCH - 1);
+    const int q = qti >> a.jh_log, jh = qti & (jhn - 1);
+    mbar_expect(su32(&bars[slot]), CH * W * 4);
+#pragma unroll
+    for (int b = 0; b < CH / 256; ++b)
+      tma_load_2d(su32(ring + ((size_t)slot * CH + b * 256) * W), &amap, (4 * q + r) * W, jh * ROWS + kk * CH + b * 256,
+                  su32(&bars[slot]));
+  };
+  if (tid == 0)
+    for (int N = 0; N < RING - 1 && N < total_chunks; ++N) issue(N, N);
+
+  int cslot = 0;
+  uint32_t cpar = 0;
+  unsigned long long msk = ntiles > 0 ? a.mask[(size_t)(qt0 & (jhn - 1)) * 64 + g] : 0ull;
+  float v[64];
+  for (int i = 0; i < ntiles; ++i) {
+    const int qti = qt0 + i;
+    const int q = qti >> a.jh_log, jh = qti & (jhn - 1);
+    const bool first = (i == 0) || jh == 0, last = (i == ntiles - 1) || jh == jhn - 1;
+    const unsigned long long msk_next = i + 1 < ntiles ? a.mask[(size_t)((qti + 1) & (jhn - 1)) * 64 + g] : 0ull;
+
+    // ---- phase 1: rows g + 64e as the chunks land (chunk kk holds e = EPC kk .. EPC kk + EPC - 1) ----
+#pragma unroll
+    for (int kk = 0; kk < NCH; ++kk) {
+      mbar_wait(su32(&bars[cslot]), cpar);
+      const float* src = ring + (size_t)cslot * CH * W;
+#pragma unroll
+      for (int j = 0; j < EPC; ++j) {
+        const int e = EPC * kk + j;
+        const uint32_t bits = __float_as_uint(src[(g + 64 * j) * W + c]);
+        v[e] = __uint_as_float(bits ^ ((uint32_t)(msk >> e) << 31));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(su32(&bars[RING + cslot]));
+      if (tid == 0) {
+        const int G = i * NCH + kk, Gn = G + RING - 1;
+        if (Gn < total_chunks) {
+          const int pslot = cslot == 0 ? RING - 1 : cslot - 1;  // slot of chunk G - 1 = slot of Gn
+          if (G >= 1) mbar_wait(su32(&bars[RING + pslot]), cslot == 0 ? cpar ^ 1u : cpar);
+          issue(Gn, pslot);
+        }
+      }
+      if (++cslot == RING) {
+        cslot = 0;
+        cpar ^= 1u;
+      }
+    }
+    msk = msk_next;
+    butterfly64(v);
+    __syncthreads();  // A: the previous tile's gather has finished reading `tile`
+#pragma unroll
+    for (int e = 0; e < 64; ++e) tile[swz(g + 64 * e) * W + c] = v[e];
+    __syncthreads();  // B
+    // ---- phase 2: rows 64a + b (a = g), written back in place ----
+#pragma unroll
+    for (int b = 0; b < 64; ++b) v[b] = tile[swz(64 * g + b) * W + c];
+    butterfly64(v);
+#pragma unroll
+    for (int b = 0; b < 64; ++b) tile[swz(64 * g + b) * W + c] = v[b];
+
+    // ---- gather: samples 8 tid .. 8 tid + 7, all W columns ----
+    float acc[64];
+    const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(a.samp) + 2 * tid);
+    const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(a.samp) + 2 * tid + 1);
+    __syncthreads();  // D: Y complete
+    if (first) {
+#pragma unroll
+      for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) tmem_ld16(taddr + 16 * m, acc + 16 * m);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    }
+    const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int tl = (int)(ws[k] & (ROWS - 1));
+      const uint32_t th = ws[k] >> LO;
+      const float sg = (__popc(th & (uint32_t)jh) & 1) ? -1.f : 1.f;
+      const float4* y = reinterpret_cast<const float4*>(tile + (size_t)swz(tl) * W);
+      const float4 y0 = y[0], y1 = y[1];
+      acc[8 * k + 0] = fmaf(sg, y0.x, acc[8 * k + 0]);
+      acc[8 * k + 1] = fmaf(sg, y0.y, acc[8 * k + 1]);
+      acc[8 * k + 2] = fmaf(sg, y0.z, acc[8 * k + 2]);
+      acc[8 * k + 3] = fmaf(sg, y0.w, acc[8 * k + 3]);
+      acc[8 * k + 4] = fmaf(sg, y1.x, acc[8 * k + 4]);
+      acc[8 * k + 5] = fmaf(sg, y1.y, acc[8 * k + 5]);
+      acc[8 * k + 6] = fmaf(sg, y1.z, acc[8 * k + 6]);
+      acc[8 * k + 7] = fmaf(sg, y1.w, acc[8 * k + 7]);
+    }
+    if (last) {
+      const int seg = q - q_first;
+      float4* dst = reinterpret_cast<float4*>(
+          a.part + ((((size_t)kq * a.segmax + seg) * 4 + r) * SMAX + (size_t)8 * tid) * W);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) dst[m] = make_float4(acc[4 * m], acc[4 * m + 1], acc[4 * m + 2], acc[4 * m + 3]);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) tmem_st16(taddr + 16 * m, acc + 16 * m);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// out[t][col] = scale * sum of the run partials of col's slice, in run order.
+__global__ void srht_acc_finalize(const float* __restrict__ part, const int32_t* __restrict__ qtab, int maxl,
+                                  int64_t s, int64_t L, float scale, float* __restrict__ out, int64_t out_rs,
+                                  int64_t out_cs) {
+  const int64_t total = s * L;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / L, col = e - t * L;
+    const int64_t q = col >> 5;
+    const int r = (int)((col >> 3) & 3), c = (int)(col & 7);
+    float acc = 0.f;
+    for (int m = 0; m < maxl; ++m) {
+      const int ent = qtab[q * maxl + m];
+      if (ent < 0) break;
+      acc += part[(((size_t)ent * 4 + r) * SMAX + t) * W + c];
+    }
+    out[t * out_rs + col * out_cs] = acc * scale;
+  }
+}
+
+// mask[jh][g] bit e = (row 4096 jh + g + 64 e < n and its sign is -1).
+__global__ void srht_acc_masks(const int8_t* __restrict__ signs, int64_t n, int64_t jh_count,
+                               unsigned long long* __restrict__ mask) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= jh_count * 64) return;
+  const int64_t jh = i >> 6, g = i & 63;
+  unsigned long long m = 0;
+  for (int e = 0; e < 64; ++e) {
+    const int64_t row = jh * ROWS + g + 64 * e;
+    if (row < n && signs[row] < 0) m |= 1ull << e;
+  }
+  mask[i] = m;
+}
+
+}  // namespace
+
+bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
+                  int64_t out_rs, int64_t out_cs) {
+  if (std::getenv("RNLA_SRHT_NO_ACC") || plan.q < LO || plan.s > SMAX || L < 1 || !tma_encode_available()) return false;
+  if ((reinterpret_cast<uintptr_t>(in) & 15) || ((ld * 4) % 16) || plan.n > (int64_t)INT32_MAX) return false;
+  if (plan.n < 1 || ctx->num_sms < 4) return false;
+  const int64_t jh_count = plan.big_n >> LO;
+  if (!plan.acc_mask.p) {
+    plan.acc_mask = DevBuf(sizeof(unsigned long long) * (size_t)jh_count * 64, ctx->stream);
+    srht_acc_masks<<<(unsigned)((jh_count * 64 + 255) / 256), 256, 0, ctx->stream>>>(
+        plan.signs.as<int8_t>(), plan.n, jh_count, plan.acc_mask.as<unsigned long long>());
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+    std::vector<uint32_t> sp(SMAX, 0u);
+    for (int64_t t = 0; t < plan.s; ++t) {
+      const int64_t ix = plan.host_idx[(size_t)t];
+      sp[(size_t)t] = (uint32_t)(ix & (ROWS - 1)) | ((uint32_t)(ix >> LO) << LO);
+    }
+    plan.acc_samp = DevBuf(sizeof(uint32_t) * SMAX, ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(plan.acc_samp.p, sp.data(), sizeof(uint32_t) * SMAX, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // sp goes out of scope
+  }
+  // Runs: KQ groups of four CTAs split the Q * JH quad-tiles evenly, q-major.
+  const int64_t nquads = (L + 4 * W - 1) / (4 * W);
+  const int64_t qt = nquads * jh_count;
+  if (qt > (int64_t)1 << 30) return false;
+  const int kq = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms / 4, qt));
+  // qtab[q][m] = index (run k, segment of the run) of the m-th partial of quad q, -1 padded.
+  int segmax = 1;
+  std::vector<std::vector<std::pair<int, int>>> lists((size_t)nquads);
+  for (int k = 0; k < kq; ++k) {
+    const int64_t s0 = (int64_t)k * qt / kq, s1 = (int64_t)(k + 1) * qt / kq;
+    if (s1 <= s0) continue;
+    const int64_t qa = s0 / jh_count, qb = (s1 - 1) / jh_count;
+    segmax = std::max(segmax, (int)(qb - qa + 1));
+    for (int64_t qq = qa; qq <= qb; ++qq) lists[(size_t)qq].emplace_back(k, (int)(qq - qa));
+  }
+  int maxl = 1;
+  for (auto& l : lists) maxl = std::max(maxl, (int)l.size());
+  std::vector<int32_t> qtab((size_t)nquads * maxl, -1);
+  for (int64_t qq = 0; qq < nquads; ++qq)
+    for (size_t m = 0; m < lists[(size_t)qq].size(); ++m)
+      qtab[(size_t)qq * maxl + m] = lists[(size_t)qq][m].first * segmax + lists[(size_t)qq][m].second;
+  DevBuf dq(sizeof(int32_t) * qtab.size(), ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(dq.p, qtab.data(), sizeof(int32_t) * qtab.size(), cudaMemcpyHostToDevice, ctx->stream));
+  DevBuf part(sizeof(float) * (size_t)kq * segmax * 4 * SMAX * W, ctx->stream);
+
+  CUtensorMap amap;
+  tma_map_rows_f32(&amap, in, plan.n, L, ld, W, 256);
+  int jh_log = 0;
+  while (((int64_t)1 << jh_log) < jh_count) ++jh_log;
+  AccArgs args{plan.acc_mask.as<unsigned long long>(), plan.acc_samp.as<uint32_t>(), part.as<float>(), qt,
+               (int)jh_count, jh_log, kq, segmax};
+  ensure_dyn_smem((const void*)srht_acc_kernel, SMEM_BYTES);
+  srht_acc_kernel<<<4 * kq, NT, SMEM_BYTES, ctx->stream>>>(amap, args);
+  RNLA_CUDA(cudaGetLastError());
+  const float scale = (float)(1.0 / std::sqrt((double)plan.s));
+  srht_acc_finalize<<<grid_for(ctx, plan.s * L, 256), 256, 0, ctx->stream>>>(part.as<float>(), dq.as<int32_t>(), maxl,
+                                                                             plan.s, L, scale, out, out_rs, out_cs);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx, 2);
+  // dq's host vector is copied before return (pageable memcpy is synchronous
+  // with respect to the host buffer); the device buffers are stream-ordered.
+  return true;
+}
+
+}  // namespace rnla

@@ -299,6 +299,20 @@ void make_map(CUtensorMap* m, void* base, int rank, const cuuint64_t* dims, cons
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+}  // namespace
+
+bool tma_encode_available() { return encode_fn() != nullptr; }
+
+void tma_map_rows_f32(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols,
+                      uint32_t box_rows) {
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  make_map(m, const_cast<float*>(base), 2, dims, strides, box);
+}
+
+namespace {
+
 template <int LOGR, bool HI>
 void launch_pass(rnla_ctx* ctx, dim3 grid, const CUtensorMap& src, const CUtensorMap& dst, const SrhtPlan& plan,
                  int64_t L, int64_t c0, float scale, float* out, int64_t out_rs, int64_t out_cs) {

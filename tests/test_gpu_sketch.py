@@ -158,6 +158,35 @@ def test_srht_register_path_fp32(ctx):
     assert relf(got, orc.srht_rows(m.astype(np.float64), 4096, 17)) <= 1e-4
 
 
+@pytest.mark.parametrize("n,L,s,ld", [(4096, 8, 4096, 8), (5000, 1, 1, 4), (70000, 40, 300, 40), (1 << 16, 100, 4096, 104),
+                                      ((1 << 17) + 3, 33, 2048, 36), (1 << 18, 256, 4096, 256)])
+def test_srht_onepass_fp32(ctx, n, L, s, ld):
+    # srht_acc.cu: 4096-row tiles, sampled outputs accumulated in TMEM, runs that
+    # cross 32-column quads flushed to partials. Checked against the fp64 oracle
+    # and against the two-pass TMA kernels on the same operator.
+    rng = np.random.default_rng(n + L)
+    full = rng.standard_t(3, size=(n, ld)).astype(np.float32)
+    m = torch.from_numpy(full).cuda()[:, :L]
+    spec = rn.SketchSpec.srht(s, 900 + L)
+    got = rn.sketch_rows(m, spec, ctx=ctx).cpu().numpy()
+    ref = orc.srht_rows(full[:, :L].astype(np.float64), s, 900 + L)
+    assert relf(got, ref) <= 1e-4
+    os.environ["RNLA_SRHT_NO_ACC"] = "1"
+    try:
+        two = rn.sketch_rows(m, spec, ctx=ctx).cpu().numpy()
+    finally:
+        del os.environ["RNLA_SRHT_NO_ACC"]
+    assert relf(got, two) <= 1e-5
+
+
+def test_srht_onepass_many_runs(ctx):
+    # 2^20 x 72: 3 quads x 256 tiles over 37 runs -> runs span quad boundaries
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal(((1 << 20), 72)).astype(np.float32)
+    got = rn.sketch_rows(dev(m), rn.SketchSpec.srht(4096, 5), ctx=ctx).cpu().numpy()
+    assert relf(got, orc.srht_rows(m.astype(np.float64), 4096, 5)) <= 1e-4
+
+
 def test_srht_rows_fp32(ctx):
     rng = np.random.default_rng(12)
     m = rng.standard_t(3, size=(1 << 14, 96)).astype(np.float32)
