@@ -118,6 +118,9 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 // four row groups a warp touches in phase 2 (rows 64a + b, a = 4w..4w+3) sit in
 // different 8-bank groups; phase 1 (rows g + 64e) stays conflict-free too.
 __device__ __forceinline__ int swz(int r) { return r ^ ((r >> 6) & 3); }
+// Column c of physical row p sits at p * W + (c ^ (p & 4)): the two 16-B
+// halves of a row are swapped when bit 2 of p is set, so the gather's 16-B
+// loads of random rows spread over all eight 4-bank groups instead of four.
 
 __device__ __forceinline__ void butterfly64(float* v) {
 #pragma unroll
@@ -167,11 +170,14 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
   const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
 
   const int qt0 = (int)start;  // quad-tile indices fit in int (Q * JH <= 2^30 checked on the host)
-  // Producer (thread 0): chunk N lands in slot N % RING. After reading chunk G
-  // it waits until every warp has read chunk G - 1 (usually long done) and
-  // refills that slot with chunk G + RING - 1, so RING - 1 chunks stay in flight
-  // through phase 2 and the gather.
-  auto issue = [&](int N, int slot) {
+  // Producer (thread 0): chunk N lands in slot N % RING once chunk N - RING has
+  // been read by every warp. During phase 1 it keeps chunks up to G + RING - 2
+  // issued (G = the chunk just read; the wait is for G - 2, normally long
+  // done); after barrier A every chunk of the tile is read, so it tops the ring
+  // up to RING chunks for phase 2 and the gather. Its counter lives in smem.
+  __shared__ int nissue_s;
+  auto issue = [&](int N) {
+    const int slot = N % RING;
     const int qti = qt0 + (N >> 3), kk = N & (NCH - 1);
     const int q = qti >> a.jh_log, jh = qti & (jhn - 1);
     mbar_expect(su32(&bars[slot]), CH * W * 4);
@@ -180,8 +186,11 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
       tma_load_2d(su32(ring + ((size_t)slot * CH + b * 256) * W), &amap, (4 * q + r) * W, jh * ROWS + kk * CH + b * 256,
                   su32(&bars[slot]));
   };
-  if (tid == 0)
-    for (int N = 0; N < RING - 1 && N < total_chunks; ++N) issue(N, N);
+  if (tid == 0) {
+    int N = 0;
+    for (; N < RING && N < total_chunks; ++N) issue(N);
+    nissue_s = N;
+  }
 
   int cslot = 0;
   uint32_t cpar = 0;
@@ -207,11 +216,12 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
       __syncwarp();
       if (lane == 0) mbar_arrive(su32(&bars[RING + cslot]));
       if (tid == 0) {
-        const int G = i * NCH + kk, Gn = G + RING - 1;
-        if (Gn < total_chunks) {
-          const int pslot = cslot == 0 ? RING - 1 : cslot - 1;  // slot of chunk G - 1 = slot of Gn
-          if (G >= 1) mbar_wait(su32(&bars[RING + pslot]), cslot == 0 ? cpar ^ 1u : cpar);
-          issue(Gn, pslot);
+        const int G = i * NCH + kk, N = nissue_s;
+        if (N <= G + RING - 2 && N < total_chunks) {
+          const int P = N - RING;  // previous occupant of N's slot, <= G - 2
+          mbar_wait(su32(&bars[RING + P % RING]), (uint32_t)((P / RING) & 1));
+          issue(N);
+          nissue_s = N + 1;
         }
       }
       if (++cslot == RING) {
@@ -221,16 +231,21 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
     }
     msk = msk_next;
     butterfly64(v);
-    __syncthreads();  // A: the previous tile's gather has finished reading `tile`
+    __syncthreads();  // A: the previous tile's gather has finished reading `tile`; all chunks read
+    if (tid == 0) {
+      int N = nissue_s;
+      for (const int lim = min(total_chunks, (i + 1) * NCH + RING); N < lim; ++N) issue(N);
+      nissue_s = N;
+    }
 #pragma unroll
-    for (int e = 0; e < 64; ++e) tile[swz(g + 64 * e) * W + c] = v[e];
+    for (int e = 0; e < 64; ++e) tile[(64 * e + (g ^ (e & 3))) * W + (c ^ (g & 4))] = v[e];  // row g + 64 e
     __syncthreads();  // B
     // ---- phase 2: rows 64a + b (a = g), written back in place ----
 #pragma unroll
-    for (int b = 0; b < 64; ++b) v[b] = tile[swz(64 * g + b) * W + c];
+    for (int b = 0; b < 64; ++b) v[b] = tile[(64 * g + (b ^ (g & 3))) * W + (c ^ (b & 4))];  // row 64 g + b
     butterfly64(v);
 #pragma unroll
-    for (int b = 0; b < 64; ++b) tile[swz(64 * g + b) * W + c] = v[b];
+    for (int b = 0; b < 64; ++b) tile[(64 * g + (b ^ (g & 3))) * W + (c ^ (b & 4))] = v[b];
 
     // ---- gather: samples 8 tid .. 8 tid + 7, all W columns ----
     float acc[64];
@@ -251,8 +266,9 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
       const int tl = (int)(ws[k] & (ROWS - 1));
       const uint32_t th = ws[k] >> LO;
       const float sg = (__popc(th & (uint32_t)jh) & 1) ? -1.f : 1.f;
-      const float4* y = reinterpret_cast<const float4*>(tile + (size_t)swz(tl) * W);
-      const float4 y0 = y[0], y1 = y[1];
+      const int p = swz(tl);
+      const float4 y0 = *reinterpret_cast<const float4*>(tile + p * W + (p & 4));
+      const float4 y1 = *reinterpret_cast<const float4*>(tile + p * W + (4 ^ (p & 4)));
       acc[8 * k + 0] = fmaf(sg, y0.x, acc[8 * k + 0]);
       acc[8 * k + 1] = fmaf(sg, y0.y, acc[8 * k + 1]);
       acc[8 * k + 2] = fmaf(sg, y0.z, acc[8 * k + 2]);
