@@ -35,25 +35,31 @@ namespace rnla {
 namespace {
 
 constexpr int LO = 12, ROWS = 1 << LO;  // rows per tile
-constexpr int W = 8;                     // fp32 columns per CTA
-constexpr int NT = 512;                  // threads: 64 row groups x 8 columns
-constexpr int CH = 512;                  // rows per chunk (16 KB = two 256-row TMA boxes)
+constexpr int CH = 512;                  // rows per chunk (two 256-row TMA boxes)
 constexpr int NCH = ROWS / CH;           // 8 chunks per tile
 constexpr int EPC = CH / 64;             // values per thread per chunk
-constexpr int RING = 6;                  // chunk slots (96 KB in flight)
+constexpr int RING = 6;                  // chunk slots (3/4 of a tile in flight)
 constexpr int SMAX = 4096;               // sampled outputs held on chip
-constexpr int TMEM_COLS = 256;           // 128 lanes x 256 fp32 = 4096 samples x 8 columns
 static_assert(NCH == 8, "chunk N belongs to tile N >> 3");
 
-constexpr size_t RING_BYTES = (size_t)RING * CH * W * 4;
-constexpr size_t TILE_BYTES = (size_t)ROWS * W * 4;
-constexpr size_t SMEM_BYTES = RING_BYTES + TILE_BYTES + 2 * RING * 8 + 16;
+// W fp32 columns per CTA (W = 8: one 32-B sector per row, 512 threads, one CTA
+// per SM; W = 4: 16-B rows, 256 threads, two CTAs per SM).
+template <int W>
+struct Cfg {
+  static constexpr int NT = 64 * W;           // 64 row groups x W columns
+  static constexpr int GS = 32 / W;           // CTAs (slices) per 128-B line; also the swizzle span
+  static constexpr int TMEM_COLS = 32 * W;    // 128 lanes x 32W fp32 = 4096 samples x W columns
+  static constexpr int SPT = 64 / W;          // samples per thread in the gather
+  static constexpr size_t RING_BYTES = (size_t)RING * CH * W * 4;
+  static constexpr size_t TILE_BYTES = (size_t)ROWS * W * 4;
+  static constexpr size_t SMEM_BYTES = RING_BYTES + TILE_BYTES + 2 * RING * 8 + 16;
+};
 
 struct AccArgs {
   const unsigned long long* mask;  // [JH][64]: bit e of (jh, g) = sign of row 4096 jh + g + 64 e is -1
   const uint32_t* samp;            // [SMAX]: tl | th << 12
-  float* part;                     // [KQ * segmax][4][SMAX][W] running sums per (run segment, slice)
-  int64_t qt;                      // quad-tiles = Q * JH (quad = 4 slices = 32 columns)
+  float* part;                     // [KQ * segmax][GS][SMAX][W] running sums per (run segment, slice)
+  int64_t qt;                      // line-tiles = Q * JH (Q = 32-column lines of GS slices)
   int jh_count, jh_log, kq, segmax;
 };
 
@@ -117,10 +123,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 // Physical row of tile row r: the low two bits are XORed with bits 6-7, so the
 // four row groups a warp touches in phase 2 (rows 64a + b, a = 4w..4w+3) sit in
 // different 8-bank groups; phase 1 (rows g + 64e) stays conflict-free too.
-__device__ __forceinline__ int swz(int r) { return r ^ ((r >> 6) & 3); }
-// Column c of physical row p sits at p * W + (c ^ (p & 4)): the two 16-B
-// halves of a row are swapped when bit 2 of p is set, so the gather's 16-B
-// loads of random rows spread over all eight 4-bank groups instead of four.
+// Physical row of tile row r: r XOR ((r >> 6) mod GS), so the GS row groups a
+// warp touches in phase 2 (rows 64a + b) sit in different bank groups while
+// phase 1 (rows g + 64e) stays conflict-free. For W = 8, column c of physical
+// row p sits at p * 8 + (c ^ (p & 4)): the two 16-B halves of a row swap when
+// bit 2 of p is set, so the gather's 16-B loads spread over all eight 4-bank
+// groups.
+template <int GS>
+__device__ __forceinline__ int swz(int r) { return r ^ ((r >> 6) & (GS - 1)); }
 
 __device__ __forceinline__ void butterfly64(float* v) {
 #pragma unroll
@@ -134,16 +144,21 @@ __device__ __forceinline__ void butterfly64(float* v) {
       }
 }
 
-__global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__ CUtensorMap amap, AccArgs a) {
+template <int W>
+__global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __grid_constant__ CUtensorMap amap, AccArgs a) {
+  using C = Cfg<W>;
+  constexpr int NT = C::NT, GS = C::GS, TMEM_COLS = C::TMEM_COLS, SPT = C::SPT;
+  constexpr size_t RING_BYTES = C::RING_BYTES, TILE_BYTES = C::TILE_BYTES;
   extern __shared__ __align__(1024) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);               // [RING][CH][W]
   float* tile = reinterpret_cast<float*>(smem + RING_BYTES);  // [ROWS][W], swizzled rows
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + TILE_BYTES);  // full[RING], empty[RING]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RING);
+  int& nissue_s = *reinterpret_cast<int*>(tmem_slot + 1);  // producer's next chunk
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = tid >> 3, c = tid & 7;  // phase 1: row group g; phase 2: row group a = g
-  const int kq = blockIdx.x >> 2, r = blockIdx.x & 3;
+  const int g = tid / W, c = tid % W;  // phase 1: row group g; phase 2: row group a = g
+  const int kq = blockIdx.x / GS, r = blockIdx.x % GS;
   const int64_t start = (int64_t)kq * a.qt / a.kq, end = (int64_t)(kq + 1) * a.qt / a.kq;
   const int ntiles = (int)(end - start);
   const int jhn = a.jh_count;
@@ -166,7 +181,7 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = *tmem_slot;
-  // this warp's TMEM window: lanes 32 (warp % 4) .., columns 64 (warp / 4) ..
+  // this warp's TMEM window: lanes 32 (warp % 4) .., columns 64 (warp / 4) .. (64 per thread)
   const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
 
   const int qt0 = (int)start;  // quad-tile indices fit in int (Q * JH <= 2^30 checked on the host)
@@ -175,7 +190,6 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
   // issued (G = the chunk just read; the wait is for G - 2, normally long
   // done); after barrier A every chunk of the tile is read, so it tops the ring
   // up to RING chunks for phase 2 and the gather. Its counter lives in smem.
-  __shared__ int nissue_s;
   auto issue = [&](int N) {
     const int slot = N % RING;
     const int qti = qt0 + (N >> 3), kk = N & (NCH - 1);
@@ -183,7 +197,7 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
     mbar_expect(su32(&bars[slot]), CH * W * 4);
 #pragma unroll
     for (int b = 0; b < CH / 256; ++b)
-      tma_load_2d(su32(ring + ((size_t)slot * CH + b * 256) * W), &amap, (4 * q + r) * W, jh * ROWS + kk * CH + b * 256,
+      tma_load_2d(su32(ring + ((size_t)slot * CH + b * 256) * W), &amap, (GS * q + r) * W, jh * ROWS + kk * CH + b * 256,
                   su32(&bars[slot]));
   };
   if (tid == 0) {
@@ -238,19 +252,20 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
       nissue_s = N;
     }
 #pragma unroll
-    for (int e = 0; e < 64; ++e) tile[(64 * e + (g ^ (e & 3))) * W + (c ^ (g & 4))] = v[e];  // row g + 64 e
+    for (int e = 0; e < 64; ++e) tile[(64 * e + (g ^ (e & (GS - 1)))) * W + (W == 8 ? (c ^ (g & 4)) : c)] = v[e];
     __syncthreads();  // B
     // ---- phase 2: rows 64a + b (a = g), written back in place ----
 #pragma unroll
-    for (int b = 0; b < 64; ++b) v[b] = tile[(64 * g + (b ^ (g & 3))) * W + (c ^ (b & 4))];  // row 64 g + b
+    for (int b = 0; b < 64; ++b) v[b] = tile[(64 * g + (b ^ (g & (GS - 1)))) * W + (W == 8 ? (c ^ (b & 4)) : c)];
     butterfly64(v);
 #pragma unroll
-    for (int b = 0; b < 64; ++b) tile[(64 * g + (b ^ (g & 3))) * W + (c ^ (b & 4))] = v[b];
+    for (int b = 0; b < 64; ++b) tile[(64 * g + (b ^ (g & (GS - 1)))) * W + (W == 8 ? (c ^ (b & 4)) : c)] = v[b];
 
-    // ---- gather: samples 8 tid .. 8 tid + 7, all W columns ----
+    // ---- gather: samples SPT tid .. SPT tid + SPT - 1, all W columns ----
     float acc[64];
-    const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(a.samp) + 2 * tid);
-    const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(a.samp) + 2 * tid + 1);
+    uint4 wv[SPT / 4];
+#pragma unroll
+    for (int m = 0; m < SPT / 4; ++m) wv[m] = __ldg(reinterpret_cast<const uint4*>(a.samp) + (SPT / 4) * tid + m);
     __syncthreads();  // D: Y complete
     if (first) {
 #pragma unroll
@@ -260,28 +275,25 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
       for (int m = 0; m < 4; ++m) tmem_ld16(taddr + 16 * m, acc + 16 * m);
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     }
-    const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int tl = (int)(ws[k] & (ROWS - 1));
-      const uint32_t th = ws[k] >> LO;
-      const float sg = (__popc(th & (uint32_t)jh) & 1) ? -1.f : 1.f;
-      const int p = swz(tl);
-      const float4 y0 = *reinterpret_cast<const float4*>(tile + p * W + (p & 4));
-      const float4 y1 = *reinterpret_cast<const float4*>(tile + p * W + (4 ^ (p & 4)));
-      acc[8 * k + 0] = fmaf(sg, y0.x, acc[8 * k + 0]);
-      acc[8 * k + 1] = fmaf(sg, y0.y, acc[8 * k + 1]);
-      acc[8 * k + 2] = fmaf(sg, y0.z, acc[8 * k + 2]);
-      acc[8 * k + 3] = fmaf(sg, y0.w, acc[8 * k + 3]);
-      acc[8 * k + 4] = fmaf(sg, y1.x, acc[8 * k + 4]);
-      acc[8 * k + 5] = fmaf(sg, y1.y, acc[8 * k + 5]);
-      acc[8 * k + 6] = fmaf(sg, y1.z, acc[8 * k + 6]);
-      acc[8 * k + 7] = fmaf(sg, y1.w, acc[8 * k + 7]);
+    for (int k = 0; k < SPT; ++k) {
+      const uint32_t wk = k % 4 == 0 ? wv[k / 4].x : k % 4 == 1 ? wv[k / 4].y : k % 4 == 2 ? wv[k / 4].z : wv[k / 4].w;
+      const int p = swz<GS>((int)(wk & (ROWS - 1)));
+      const float sg = (__popc((wk >> LO) & (uint32_t)jh) & 1) ? -1.f : 1.f;
+#pragma unroll
+      for (int h = 0; h < W / 4; ++h) {
+        const float4 y = *reinterpret_cast<const float4*>(tile + p * W + (W == 8 ? ((4 * h) ^ (p & 4)) : 0));
+        float* o = acc + W * k + 4 * h;
+        o[0] = fmaf(sg, y.x, o[0]);
+        o[1] = fmaf(sg, y.y, o[1]);
+        o[2] = fmaf(sg, y.z, o[2]);
+        o[3] = fmaf(sg, y.w, o[3]);
+      }
     }
     if (last) {
       const int seg = q - q_first;
-      float4* dst = reinterpret_cast<float4*>(
-          a.part + ((((size_t)kq * a.segmax + seg) * 4 + r) * SMAX + (size_t)8 * tid) * W);
+      float4* dst = reinterpret_cast<float4*>(a.part + ((((size_t)kq * a.segmax + seg) * GS + r) * SMAX) * W +
+                                              (size_t)64 * tid);
 #pragma unroll
       for (int m = 0; m < 16; ++m) dst[m] = make_float4(acc[4 * m], acc[4 * m + 1], acc[4 * m + 2], acc[4 * m + 3]);
     } else {
@@ -300,18 +312,19 @@ __global__ void __launch_bounds__(NT, 1) srht_acc_kernel(const __grid_constant__
 
 // out[t][col] = scale * sum of the run partials of col's slice, in run order.
 __global__ void srht_acc_finalize(const float* __restrict__ part, const int32_t* __restrict__ qtab, int maxl,
-                                  int64_t s, int64_t L, float scale, float* __restrict__ out, int64_t out_rs,
+                                  int W, int64_t s, int64_t L, float scale, float* __restrict__ out, int64_t out_rs,
                                   int64_t out_cs) {
+  const int GS = 32 / W;
   const int64_t total = s * L;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / L, col = e - t * L;
     const int64_t q = col >> 5;
-    const int r = (int)((col >> 3) & 3), c = (int)(col & 7);
+    const int r = (int)((col & 31) / W), c = (int)(col % W);
     float acc = 0.f;
     for (int m = 0; m < maxl; ++m) {
       const int ent = qtab[q * maxl + m];
       if (ent < 0) break;
-      acc += part[(((size_t)ent * 4 + r) * SMAX + t) * W + c];
+      acc += part[(((size_t)ent * GS + r) * SMAX + t) * W + c];
     }
     out[t * out_rs + col * out_cs] = acc * scale;
   }
@@ -333,34 +346,17 @@ __global__ void srht_acc_masks(const int8_t* __restrict__ signs, int64_t n, int6
 
 }  // namespace
 
-bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
-                  int64_t out_rs, int64_t out_cs) {
-  if (std::getenv("RNLA_SRHT_NO_ACC") || plan.q < LO || plan.s > SMAX || L < 1 || !tma_encode_available()) return false;
-  if ((reinterpret_cast<uintptr_t>(in) & 15) || ((ld * 4) % 16) || plan.n > (int64_t)INT32_MAX) return false;
-  if (plan.n < 1 || ctx->num_sms < 4) return false;
-  const int64_t jh_count = plan.big_n >> LO;
-  if (!plan.acc_mask.p) {
-    plan.acc_mask = DevBuf(sizeof(unsigned long long) * (size_t)jh_count * 64, ctx->stream);
-    srht_acc_masks<<<(unsigned)((jh_count * 64 + 255) / 256), 256, 0, ctx->stream>>>(
-        plan.signs.as<int8_t>(), plan.n, jh_count, plan.acc_mask.as<unsigned long long>());
-    RNLA_CUDA(cudaGetLastError());
-    note_launch(ctx);
-    std::vector<uint32_t> sp(SMAX, 0u);
-    for (int64_t t = 0; t < plan.s; ++t) {
-      const int64_t ix = plan.host_idx[(size_t)t];
-      sp[(size_t)t] = (uint32_t)(ix & (ROWS - 1)) | ((uint32_t)(ix >> LO) << LO);
-    }
-    plan.acc_samp = DevBuf(sizeof(uint32_t) * SMAX, ctx->stream);
-    RNLA_CUDA(cudaMemcpyAsync(plan.acc_samp.p, sp.data(), sizeof(uint32_t) * SMAX, cudaMemcpyHostToDevice,
-                              ctx->stream));
-    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // sp goes out of scope
-  }
-  // Runs: KQ groups of four CTAs split the Q * JH quad-tiles evenly, q-major.
-  const int64_t nquads = (L + 4 * W - 1) / (4 * W);
-  const int64_t qt = nquads * jh_count;
-  if (qt > (int64_t)1 << 30) return false;
-  const int kq = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms / 4, qt));
-  // qtab[q][m] = index (run k, segment of the run) of the m-th partial of quad q, -1 padded.
+namespace {
+
+template <int W>
+void srht_acc_launch(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
+                     int64_t out_rs, int64_t out_cs, int64_t jh_count, int64_t qt) {
+  using C = Cfg<W>;
+  // Runs: KQ groups of GS CTAs (the slices of one 128-B line) split the Q * JH
+  // line-tiles evenly, q-major.
+  const int64_t nquads = qt / jh_count;
+  const int kq = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * (8 / W) / C::GS, qt));
+  // qtab[q][m] = index (run k, segment of the run) of the m-th partial of line q, -1 padded.
   int segmax = 1;
   std::vector<std::vector<std::pair<int, int>>> lists((size_t)nquads);
   for (int k = 0; k < kq; ++k) {
@@ -378,7 +374,7 @@ bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t 
       qtab[(size_t)qq * maxl + m] = lists[(size_t)qq][m].first * segmax + lists[(size_t)qq][m].second;
   DevBuf dq(sizeof(int32_t) * qtab.size(), ctx->stream);
   RNLA_CUDA(cudaMemcpyAsync(dq.p, qtab.data(), sizeof(int32_t) * qtab.size(), cudaMemcpyHostToDevice, ctx->stream));
-  DevBuf part(sizeof(float) * (size_t)kq * segmax * 4 * SMAX * W, ctx->stream);
+  DevBuf part(sizeof(float) * (size_t)kq * segmax * C::GS * SMAX * W, ctx->stream);
 
   CUtensorMap amap;
   tma_map_rows_f32(&amap, in, plan.n, L, ld, W, 256);
@@ -386,16 +382,48 @@ bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t 
   while (((int64_t)1 << jh_log) < jh_count) ++jh_log;
   AccArgs args{plan.acc_mask.as<unsigned long long>(), plan.acc_samp.as<uint32_t>(), part.as<float>(), qt,
                (int)jh_count, jh_log, kq, segmax};
-  ensure_dyn_smem((const void*)srht_acc_kernel, SMEM_BYTES);
-  srht_acc_kernel<<<4 * kq, NT, SMEM_BYTES, ctx->stream>>>(amap, args);
+  ensure_dyn_smem((const void*)srht_acc_kernel<W>, C::SMEM_BYTES);
+  srht_acc_kernel<W><<<C::GS * kq, C::NT, C::SMEM_BYTES, ctx->stream>>>(amap, args);
   RNLA_CUDA(cudaGetLastError());
   const float scale = (float)(1.0 / std::sqrt((double)plan.s));
-  srht_acc_finalize<<<grid_for(ctx, plan.s * L, 256), 256, 0, ctx->stream>>>(part.as<float>(), dq.as<int32_t>(), maxl,
-                                                                             plan.s, L, scale, out, out_rs, out_cs);
+  srht_acc_finalize<<<grid_for(ctx, plan.s * L, 256), 256, 0, ctx->stream>>>(
+      part.as<float>(), dq.as<int32_t>(), maxl, W, plan.s, L, scale, out, out_rs, out_cs);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx, 2);
-  // dq's host vector is copied before return (pageable memcpy is synchronous
-  // with respect to the host buffer); the device buffers are stream-ordered.
+  // qtab was staged by the pageable cudaMemcpyAsync before it returned; the
+  // device buffers are freed stream-ordered.
+}
+
+}  // namespace
+
+bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t ld, int64_t L, float* out,
+                  int64_t out_rs, int64_t out_cs) {
+  if (std::getenv("RNLA_SRHT_NO_ACC") || plan.q < LO || plan.s > SMAX || L < 1 || !tma_encode_available()) return false;
+  if ((reinterpret_cast<uintptr_t>(in) & 15) || ((ld * 4) % 16) || plan.n > (int64_t)INT32_MAX) return false;
+  if (plan.n < 1 || ctx->num_sms < 4) return false;
+  const int64_t jh_count = plan.big_n >> LO;
+  const int64_t qt = (L + 31) / 32 * jh_count;
+  if (qt > (int64_t)1 << 30) return false;
+  if (!plan.acc_mask.p) {
+    plan.acc_mask = DevBuf(sizeof(unsigned long long) * (size_t)jh_count * 64, ctx->stream);
+    srht_acc_masks<<<(unsigned)((jh_count * 64 + 255) / 256), 256, 0, ctx->stream>>>(
+        plan.signs.as<int8_t>(), plan.n, jh_count, plan.acc_mask.as<unsigned long long>());
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+    std::vector<uint32_t> sp(SMAX, 0u);
+    for (int64_t t = 0; t < plan.s; ++t) {
+      const int64_t ix = plan.host_idx[(size_t)t];
+      sp[(size_t)t] = (uint32_t)(ix & (ROWS - 1)) | ((uint32_t)(ix >> LO) << LO);
+    }
+    plan.acc_samp = DevBuf(sizeof(uint32_t) * SMAX, ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(plan.acc_samp.p, sp.data(), sizeof(uint32_t) * SMAX, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // sp goes out of scope
+  }
+  // RNLA_SRHT_ACC_W=4: 4-column slices, two CTAs per SM (default 8: one CTA per SM).
+  const char* w_env = std::getenv("RNLA_SRHT_ACC_W");
+  if (w_env && std::atoi(w_env) == 4) srht_acc_launch<4>(ctx, plan, in, ld, L, out, out_rs, out_cs, jh_count, qt);
+  else srht_acc_launch<8>(ctx, plan, in, ld, L, out, out_rs, out_cs, jh_count, qt);
   return true;
 }
 
