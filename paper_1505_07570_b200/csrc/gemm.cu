@@ -264,6 +264,20 @@ __global__ void splitk_reduce(int64_t m, int64_t n, int splits, const T* __restr
 
 }  // namespace
 
+// gemm_dmma.cu: the cp.async-pipelined DMMA kernel for K-major A and B.
+template <class TI>
+bool dmma_kk_applicable(const TI* A, int64_t a_rs, int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs);
+template <class TI>
+void dmma_kk_launch(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int64_t splits, double alpha,
+                    const TI* A, int64_t lda, const TI* B, int64_t ldb, double beta, double* C, int64_t c_rs,
+                    int64_t c_cs, double* ws, int sym);
+int dmma_kk_tiles(int64_t m, int64_t n, int sym);
+int dmma_kk_per_sm();
+template <class TI>
+static bool try_dmma_kk(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const TI* A, int64_t a_rs,
+                        int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
+                        int64_t c_cs, int max_splits, int sym);
+
 template <class T>
 void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
           const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs, int max_splits) {
@@ -273,6 +287,11 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
       gemm_f32_tc(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs);
       return;
     }
+  }
+  if constexpr (std::is_same<T, double>::value) {
+    if (m >= 64 && n >= 64 &&
+        try_dmma_kk<double>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs, max_splits, 0))
+      return;
   }
   // narrow outputs (n mod 64 in 1..32) use 32-wide tiles for the fp64 kernel
   const int nb = (std::is_same<T, double>::value && ((n % 64) != 0) && ((n % 64) <= 32)) ? 32 : BN;
@@ -332,12 +351,47 @@ static int64_t wave_splits(int64_t active, int64_t slots, int64_t k, int64_t cap
   return best;
 }
 
+// Split-K sized on the K-major DMMA kernel's tiles, fixed-order reduce, and
+// the lower-tile mirror for symmetric products. False when the layout does not
+// apply (the caller falls back to the generic kernel).
+template <class TI>
+static bool try_dmma_kk(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const TI* A, int64_t a_rs,
+                        int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
+                        int64_t c_cs, int max_splits, int sym) {
+  if (!dmma_kk_applicable<TI>(A, a_rs, a_cs, B, b_rs, b_cs)) return false;
+  const int64_t active = dmma_kk_tiles(m, n, sym);
+  int64_t splits = wave_splits(active, (int64_t)dmma_kk_per_sm() * ctx->num_sms, k, std::max(1, max_splits));
+  int64_t kchunk = ((k + splits - 1) / splits + BK - 1) / BK * BK;
+  if (k == 0) kchunk = BK;
+  splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
+  DevBuf ws;
+  double* wsp = nullptr;
+  if (splits > 1) {
+    ws = DevBuf(sizeof(double) * (size_t)(splits * m * n), ctx->stream);
+    wsp = ws.as<double>();
+  }
+  dmma_kk_launch<TI>(ctx, m, n, k, kchunk, splits, alpha, A, a_rs, B, b_cs, beta, C, c_rs, c_cs, wsp, sym);
+  if (splits > 1) {
+    const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, (int64_t)ctx->num_sms * 8);
+    splitk_reduce<double><<<blocks, 256, 0, ctx->stream>>>(m, n, (int)splits, wsp, alpha, beta, C, c_rs, c_cs);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+  if (sym) {
+    mirror_lower_tiles<<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, C, c_rs, c_cs);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
+  return true;
+}
+
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                      int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
                      int64_t c_cs) {
   if (m == 0 || n == 0) return;
   // Gram products (B = A') are symmetric: compute the upper tiles only.
   const int sym = (A == B && m == n && a_rs == b_cs && a_cs == b_rs) ? 1 : 0;
+  if (try_dmma_kk<float>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs, 64, sym)) return;
   const int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
   const int64_t active = sym ? tm * (tm + 1) / 2 : tm * tn;
   static const int per_sm = [] {
