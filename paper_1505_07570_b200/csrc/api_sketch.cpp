@@ -92,6 +92,13 @@ static rnla::GreenSplit* green_for(rnla_ctx* ctx) {
   }
   return ctx->green.get();
 }
+// Row pitch (elements) rounded up to 16 bytes.
+template <class T>
+static int64_t aligned_ld(int64_t L) {
+  const int64_t e = 16 / (int64_t)sizeof(T);
+  return (L + e - 1) / e * e;
+}
+
 template <class T>
 void gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s,
                     int64_t k0, bool first, T* out, int64_t out_rs, int64_t out_cs) {
@@ -104,6 +111,18 @@ template <class T>
 void gaussian_segments(rnla_ctx* ctx, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s, uint64_t seed, T* out,
                        int64_t out_rs, int64_t out_cs) {
   const DenseOperator& g = gaussian_operator(ctx, n, s, seed, std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32);
+  // fp64 segments whose rows are not 16-B aligned are first copied to padded
+  // rows, so every large Gaussian stage runs the cp.async DMMA kernel and a
+  // standalone call agrees bitwise with the combined sketch's stage
+  // (tests/test_sketch.cpp:88-98).
+  DevBuf padded;
+  if (std::is_same<T, double>::value && (ld * (int64_t)sizeof(T)) % 16 != 0 && n > 0 && L >= 64 && s >= 64) {
+    const int64_t ld2 = aligned_ld<T>(L);
+    padded = DevBuf(sizeof(T) * (size_t)(n * ld2), ctx->stream);
+    copy2d<T>(ctx, n, L, in, ld, 1, padded.as<T>(), ld2, 1);
+    in = padded.as<T>();
+    ld = ld2;
+  }
   if (n == 0) {  // empty sum
     DevBuf z(sizeof(T) * (size_t)std::max<int64_t>(s * L, 1), ctx->stream);
     RNLA_CUDA(cudaMemsetAsync(z.p, 0, sizeof(T) * (size_t)(s * L), ctx->stream));
@@ -128,7 +147,8 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
   const int64_t Lo = L + (extra ? 1 : 0), s = spec->s, s2 = spec->stage2_s;
   const DenseOperator& g = gaussian_operator(ctx, s, s2, spec->stage2_seed, dt);
   if (n > 0) count_sketch_plan(ctx, n, s, spec->seed, row_offset);
-  DevBuf mid(sizeof(T) * (size_t)(s * Lo), ctx->stream);
+  const int64_t ldm = aligned_ld<T>(Lo);
+  DevBuf mid(sizeof(T) * (size_t)(s * ldm), ctx->stream);
   DevBuf acc(sizeof(T) * (size_t)(s2 * Lo), ctx->stream);
   const int64_t KC = gauss_kc_for(ctx, s);
   const int64_t chunks = (s + KC - 1) / KC;
@@ -166,7 +186,7 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
       const int64_t b0 = c * KC, b1 = std::min(s, b0 + KC);
       {
         StreamScope on_gather(ctx, gather_st[c & 1]);
-        count_sketch_segments<T>(ctx, M, ld, extra, xs, n, L, s, spec->seed, row_offset, mid.as<T>(), Lo, false, b0,
+        count_sketch_segments<T>(ctx, M, ld, extra, xs, n, L, s, spec->seed, row_offset, mid.as<T>(), ldm, false, b0,
                                  b1);
         RNLA_CUDA(cudaEventRecord(ev[(size_t)c], ctx->stream));
       }
@@ -183,9 +203,9 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
       RNLA_CUDA(cudaStreamWaitEvent(gemm_st, ev[(size_t)c], 0));
       StreamScope on_aux(ctx, gemm_st);
       const int owner = (int)(c % ctx->world);
-      if (ctx->world > 1) reduce_to(ctx, mid.as<T>() + b0 * Lo, (size_t)((b1 - b0) * Lo), dt, owner);
+      if (ctx->world > 1) reduce_to(ctx, mid.as<T>() + b0 * ldm, (size_t)((b1 - b0) * ldm), dt, owner);
       if (owner == ctx->rank) {
-        gaussian_chunk<T>(ctx, g, mid.as<T>(), Lo, s, Lo, s2, b0, first, acc.as<T>(), Lo, 1);
+        gaussian_chunk<T>(ctx, g, mid.as<T>(), ldm, s, Lo, s2, b0, first, acc.as<T>(), Lo, 1);
         first = false;
       }
     }
@@ -254,17 +274,18 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
     T* mp = out;
     int64_t m_rs = o_rs;
     if (!direct) {
-      mid = DevBuf(sizeof(T) * (size_t)(s * Lo), ctx->stream);
+      // rows padded to 16 B so the Gaussian stage reads them with cp.async (gemm_dmma.cu)
+      m_rs = aligned_ld<T>(Lo);
+      mid = DevBuf(sizeof(T) * (size_t)(s * m_rs), ctx->stream);
       mp = mid.as<T>();
-      m_rs = Lo;
     }
     count_sketch_segments<T>(ctx, M, ld, extra, xs, n, L, s, spec->seed, row_offset, mp, m_rs, false);
-    if (sharded) allreduce_sum(ctx, mp, (size_t)(s * Lo), std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32);
+    if (sharded) allreduce_sum(ctx, mp, (size_t)(s * m_rs), std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32);
     if (kind == RNLA_SKETCH_COUNT) {
-      if (!direct) copy2d<T>(ctx, s, Lo, mp, Lo, 1, out, o_rs, o_cs);
+      if (!direct) copy2d<T>(ctx, s, Lo, mp, m_rs, 1, out, o_rs, o_cs);
       return;
     }
-    dense_stage<T>(ctx, spec->stage2_kind, mp, Lo, s, Lo, spec->stage2_s, spec->stage2_seed, out, o_rs, o_cs);
+    dense_stage<T>(ctx, spec->stage2_kind, mp, m_rs, s, Lo, spec->stage2_s, spec->stage2_seed, out, o_rs, o_cs);
     return;
   }
   if (kind == RNLA_SKETCH_SRHT && sharded) {

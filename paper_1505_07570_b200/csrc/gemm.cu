@@ -266,11 +266,11 @@ __global__ void splitk_reduce(int64_t m, int64_t n, int splits, const T* __restr
 
 // gemm_dmma.cu: the cp.async-pipelined DMMA kernel for K-major A and B.
 template <class TI>
-bool dmma_kk_applicable(const TI* A, int64_t a_rs, int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs);
+int dmma_kk_applicable(const TI* A, int64_t a_rs, int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs);
 template <class TI>
-void dmma_kk_launch(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int64_t splits, double alpha,
-                    const TI* A, int64_t lda, const TI* B, int64_t ldb, double beta, double* C, int64_t c_rs,
-                    int64_t c_cs, double* ws, int sym);
+void dmma_kk_launch(rnla_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, int64_t kchunk, int64_t splits,
+                    double alpha, const TI* A, int64_t lda, const TI* B, int64_t ldb, double beta, double* C,
+                    int64_t c_rs, int64_t c_cs, double* ws, int sym);
 int dmma_kk_tiles(int64_t m, int64_t n, int sym);
 int dmma_kk_per_sm();
 template <class TI>
@@ -358,7 +358,8 @@ template <class TI>
 static bool try_dmma_kk(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const TI* A, int64_t a_rs,
                         int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
                         int64_t c_cs, int max_splits, int sym) {
-  if (!dmma_kk_applicable<TI>(A, a_rs, a_cs, B, b_rs, b_cs)) return false;
+  const int layout = dmma_kk_applicable<TI>(A, a_rs, a_cs, B, b_rs, b_cs);
+  if (!layout) return false;
   const int64_t active = dmma_kk_tiles(m, n, sym);
   int64_t splits = wave_splits(active, (int64_t)dmma_kk_per_sm() * ctx->num_sms, k, std::max(1, max_splits));
   int64_t kchunk = ((k + splits - 1) / splits + BK - 1) / BK * BK;
@@ -370,7 +371,8 @@ static bool try_dmma_kk(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double a
     ws = DevBuf(sizeof(double) * (size_t)(splits * m * n), ctx->stream);
     wsp = ws.as<double>();
   }
-  dmma_kk_launch<TI>(ctx, m, n, k, kchunk, splits, alpha, A, a_rs, B, b_cs, beta, C, c_rs, c_cs, wsp, sym);
+  dmma_kk_launch<TI>(ctx, layout, m, n, k, kchunk, splits, alpha, A, a_rs, B, layout == 1 ? b_cs : b_rs, beta, C,
+                     c_rs, c_cs, wsp, sym);
   if (splits > 1) {
     const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, (int64_t)ctx->num_sms * 8);
     splitk_reduce<double><<<blocks, 256, 0, ctx->stream>>>(m, n, (int)splits, wsp, alpha, beta, C, c_rs, c_cs);

@@ -1,8 +1,9 @@
 // gemm_dmma.cu -- fp64-accumulating DMMA GEMM for K-major operands, fed by a
 // multi-stage cp.async pipeline.
 //
-// C[m x n] = alpha * A * B + beta * C with A(i, p) = A[i * lda + p] and
-// B(p, j) = B[j * ldb + p] (both K-major: the Gram C'C of a column-major block,
+// C[m x n] = alpha * A * B + beta * C with A(i, p) = A[i * lda + p] (K-major)
+// and B(p, j) = B[j * ldb + p] (K-major) or B[p * ldb + j] (N-major: the
+// config-1 Gaussian stage Omega' * S'[A, b]). K-major x K-major covers the Gram C'C of a column-major block,
 // the Nystrom C'C of config 4 (src/spsd.cpp:193-215 via the Gram route), Q'A
 // of a row-major A, ...). TI = double, or float widened exactly to fp64 when a
 // fragment is read (products of fp32 values are exact in fp64).
@@ -67,7 +68,34 @@ __device__ __forceinline__ void load_stage(TI* S, const TI* __restrict__ G, int6
   }
 }
 
+// One stage of an N-major operand B(p, j) = G[p * ld + j]: k rows [k0, k0 + BK)
+// clipped to kend, columns [n0, n0 + BN) clipped to ncols, into S[BK][LDS_N].
+// Row length of an N-major stage (elements): k rows stay 16-B aligned and the
+// four k rows of a fragment read land in distinct banks (fp64: 68, fp32: 72).
 template <class TI>
+constexpr int lds_n() { return sizeof(TI) == 8 ? BN + 4 : BN + 8; }
+template <class TI>
+__device__ __forceinline__ void load_stage_kn(TI* S, const TI* __restrict__ G, int64_t ld, int64_t ncols, int64_t n0,
+                                              int64_t k0, int64_t kend, int tid) {
+  constexpr int EPC = 16 / sizeof(TI);
+  constexpr int CPR = BN / EPC;
+  constexpr int TOTAL = BK * CPR;
+  constexpr int LDS_N = lds_n<TI>();
+#pragma unroll
+  for (int c = tid; c < TOTAL; c += NT) {
+    const int kr = c / CPR, nc = (c % CPR) * EPC;
+    const int64_t gk = k0 + kr, gj = n0 + nc;
+    int bytes = 0;
+    const TI* src = G;
+    if (gk < kend && gj < ncols) {
+      bytes = (int)((ncols - gj < EPC ? ncols - gj : (int64_t)EPC) * (int64_t)sizeof(TI));
+      src = G + gk * ld + gj;
+    }
+    cp_async16(S + kr * LDS_N + nc, src, bytes);
+  }
+}
+
+template <class TI, bool B_KM>
 __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int64_t kdim, int64_t kchunk, double alpha,
                                                      const TI* __restrict__ A, int64_t lda, const TI* __restrict__ B,
                                                      int64_t ldb, double beta, double* C, int64_t c_rs, int64_t c_cs,
@@ -79,7 +107,9 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int6
   if (sym_upper && n0 + BN <= m0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TI* As = reinterpret_cast<TI*>(smem_raw);     // [STAGES][BM][LDS_K]
-  TI* Bs = As + (size_t)STAGES * BM * LDS_K;    // [STAGES][BN][LDS_K]
+  TI* Bs = As + (size_t)STAGES * BM * LDS_K;    // [STAGES][BN][LDS_K] (K-major B) or [STAGES][BK][LDS_N]
+  constexpr int LDS_N = lds_n<TI>();
+  constexpr int BSTAGE = B_KM ? BN * LDS_K : BK * LDS_N;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t = lane & 3;
@@ -97,7 +127,8 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int6
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nsteps) {
       load_stage<TI, BM>(As + (size_t)s * BM * LDS_K, A, lda, m, m0, kbeg + (int64_t)s * BK, kend, tid);
-      load_stage<TI, BN>(Bs + (size_t)s * BN * LDS_K, B, ldb, n, n0, kbeg + (int64_t)s * BK, kend, tid);
+      if constexpr (B_KM) load_stage<TI, BN>(Bs + (size_t)s * BSTAGE, B, ldb, n, n0, kbeg + (int64_t)s * BK, kend, tid);
+      else load_stage_kn<TI>(Bs + (size_t)s * BSTAGE, B, ldb, n, n0, kbeg + (int64_t)s * BK, kend, tid);
     }
     cp_commit();
   }
@@ -108,18 +139,20 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int6
     if (nx < nsteps) {
       const int sl = nx % STAGES;
       load_stage<TI, BM>(As + (size_t)sl * BM * LDS_K, A, lda, m, m0, kbeg + (int64_t)nx * BK, kend, tid);
-      load_stage<TI, BN>(Bs + (size_t)sl * BN * LDS_K, B, ldb, n, n0, kbeg + (int64_t)nx * BK, kend, tid);
+      if constexpr (B_KM) load_stage<TI, BN>(Bs + (size_t)sl * BSTAGE, B, ldb, n, n0, kbeg + (int64_t)nx * BK, kend, tid);
+      else load_stage_kn<TI>(Bs + (size_t)sl * BSTAGE, B, ldb, n, n0, kbeg + (int64_t)nx * BK, kend, tid);
     }
     cp_commit();
     const TI* as = As + (size_t)(it % STAGES) * BM * LDS_K + (wm * 32 + g) * LDS_K + t;
-    const TI* bs = Bs + (size_t)(it % STAGES) * BN * LDS_K + (wn * 32 + g) * LDS_K + t;
+    const TI* bs = B_KM ? Bs + (size_t)(it % STAGES) * BSTAGE + (wn * 32 + g) * LDS_K + t
+                        : Bs + (size_t)(it % STAGES) * BSTAGE + t * LDS_N + wn * 32 + g;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[MI], bf[NI];
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) af[mi] = (double)as[mi * 8 * LDS_K + kk];
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) bf[ni] = (double)bs[ni * 8 * LDS_K + kk];
+      for (int ni = 0; ni < NI; ++ni) bf[ni] = (double)(B_KM ? bs[ni * 8 * LDS_K + kk] : bs[kk * LDS_N + ni * 8]);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -147,30 +180,40 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int6
       }
 }
 
-template <class TI>
+template <class TI, bool B_KM>
 constexpr size_t smem_bytes() {
-  return (size_t)stages<TI>() * (BM + BN) * LDS_K * sizeof(TI);
+  return (size_t)stages<TI>() * (BM * LDS_K + (B_KM ? BN * LDS_K : BK * lds_n<TI>())) * sizeof(TI);
 }
 
 }  // namespace
 
+// 1: K-major B, 2: N-major B, 0: not applicable (A must be K-major; 16-B aligned rows).
 template <class TI>
-bool dmma_kk_applicable(const TI* A, int64_t a_rs, int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs) {
-  if (std::getenv("RNLA_DMMA_GENERIC")) return false;
+int dmma_kk_applicable(const TI* A, int64_t a_rs, int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs) {
+  if (std::getenv("RNLA_DMMA_GENERIC")) return 0;
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  return a_cs == 1 && b_rs == 1 && al(A) && al(B) && (a_rs * (int64_t)sizeof(TI)) % 16 == 0 &&
-         (b_cs * (int64_t)sizeof(TI)) % 16 == 0;
+  if (a_cs != 1 || !al(A) || !al(B) || (a_rs * (int64_t)sizeof(TI)) % 16 != 0) return 0;
+  if (b_rs == 1 && (b_cs * (int64_t)sizeof(TI)) % 16 == 0) return 1;
+  if (b_cs == 1 && (b_rs * (int64_t)sizeof(TI)) % 16 == 0) return 2;
+  return 0;
 }
 
 template <class TI>
-void dmma_kk_launch(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int64_t splits, double alpha,
-                    const TI* A, int64_t lda, const TI* B, int64_t ldb, double beta, double* C, int64_t c_rs,
-                    int64_t c_cs, double* ws, int sym) {
-  constexpr size_t smem = smem_bytes<TI>();
-  ensure_dyn_smem((const void*)gemm_dmma_kk<TI>, smem);
+void dmma_kk_launch(rnla_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, int64_t kchunk, int64_t splits,
+                    double alpha, const TI* A, int64_t lda, const TI* B, int64_t ldb, double beta, double* C,
+                    int64_t c_rs, int64_t c_cs, double* ws, int sym) {
   dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)splits);
-  gemm_dmma_kk<TI><<<grid, NT, smem, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, c_rs, c_cs, ws,
-                                                   sym);
+  if (layout == 1) {
+    constexpr size_t smem = smem_bytes<TI, true>();
+    ensure_dyn_smem((const void*)gemm_dmma_kk<TI, true>, smem);
+    gemm_dmma_kk<TI, true><<<grid, NT, smem, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, c_rs,
+                                                            c_cs, ws, sym);
+  } else {
+    constexpr size_t smem = smem_bytes<TI, false>();
+    ensure_dyn_smem((const void*)gemm_dmma_kk<TI, false>, smem);
+    gemm_dmma_kk<TI, false><<<grid, NT, smem, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, c_rs,
+                                                             c_cs, ws, sym);
+  }
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
@@ -187,11 +230,12 @@ int dmma_kk_tiles(int64_t m, int64_t n, int sym) {
 
 int dmma_kk_per_sm() { return 2; }
 
-template bool dmma_kk_applicable<double>(const double*, int64_t, int64_t, const double*, int64_t, int64_t);
-template bool dmma_kk_applicable<float>(const float*, int64_t, int64_t, const float*, int64_t, int64_t);
-template void dmma_kk_launch<double>(rnla_ctx*, int64_t, int64_t, int64_t, int64_t, int64_t, double, const double*,
-                                     int64_t, const double*, int64_t, double, double*, int64_t, int64_t, double*, int);
-template void dmma_kk_launch<float>(rnla_ctx*, int64_t, int64_t, int64_t, int64_t, int64_t, double, const float*,
+template int dmma_kk_applicable<double>(const double*, int64_t, int64_t, const double*, int64_t, int64_t);
+template int dmma_kk_applicable<float>(const float*, int64_t, int64_t, const float*, int64_t, int64_t);
+template void dmma_kk_launch<double>(rnla_ctx*, int, int64_t, int64_t, int64_t, int64_t, int64_t, double,
+                                     const double*, int64_t, const double*, int64_t, double, double*, int64_t, int64_t,
+                                     double*, int);
+template void dmma_kk_launch<float>(rnla_ctx*, int, int64_t, int64_t, int64_t, int64_t, int64_t, double, const float*,
                                     int64_t, const float*, int64_t, double, double*, int64_t, int64_t, double*, int);
 
 }  // namespace rnla

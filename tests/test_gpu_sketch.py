@@ -220,6 +220,18 @@ def test_combined_is_exact_composition(ctx):
     assert relf(c, orc.combined_sketch(a, 64, 20, "gaussian", 16, 21)) <= 1e-10
 
 
+@pytest.mark.parametrize("m", [100, 101])
+def test_combined_is_exact_composition_large(ctx, m):
+    # Gaussian stage large enough for the cp.async DMMA kernel (gemm_dmma.cu);
+    # odd m makes the standalone call copy to 16-B aligned rows first.
+    a = orc.gaussian_matrix(m, 3000, 9)
+    spec = rn.SketchSpec.combined(512, rn.SketchSpec.gaussian(128, 33), 31)
+    c = rn.apply_sketch(a, spec, ctx=ctx)
+    mid = rn.count_sketch(a, 512, 31, ctx=ctx)
+    assert np.linalg.norm(c - rn.gaussian_sketch(mid, 128, 33, ctx=ctx)) == 0.0
+    assert relf(c, orc.combined_sketch(a, 512, 31, "gaussian", 128, 33)) <= 1e-10
+
+
 def test_combined_srht_stage(ctx):
     a = orc.gaussian_matrix(9, 300, 6)
     spec = rn.SketchSpec.combined(100, rn.SketchSpec.srht(32, 8), 7)
