@@ -149,8 +149,59 @@ struct KsvdWork {
       tsqr(ctx, rows, cols, Y);
       return;
     }
-    if (rows >= 4 * cols && cholqr2(ctx, rows, cols, Y, false)) return;
+    if (rows >= 4 * cols &&
+        (cols <= kSmallCholMax ? cholqr2_fast(ctx, rows, cols, Y) : cholqr2(ctx, rows, cols, Y, false)))
+      return;
     householder(ctx, rows, cols, Y);
+  }
+
+  // G = Y'Y (fp64) of a column-major rows x cols Y.
+  static void gram(rnla_ctx* ctx, int64_t rows, int64_t cols, const T* Y, double* G) {
+    if constexpr (std::is_same<T, double>::value) {
+      gemm<double>(ctx, cols, cols, rows, 1.0, Y, rows, 1, Y, 1, rows, 0.0, G, 1, cols);
+    } else {
+      DevBuf Gf(sizeof(float) * cols * cols, ctx->stream);
+      gemm<float>(ctx, cols, cols, rows, 1.f, Y, rows, 1, Y, 1, rows, 0.f, Gf.as<float>(), 1, cols);
+      copy2d_cast<float, double>(ctx, cols, cols, Gf.as<float>(), 1, cols, G, 1, cols);
+    }
+  }
+
+  // CholeskyQR2 with both small factorizations on the device (small_chol_inv)
+  // and one host round trip: pass 1 writes Q1 = Y R1^-1 to a scratch buffer,
+  // pass 2 factors Q1'Q1 with the sign rule folded into R2^-1, and only when
+  // both passes factored cleanly is Y overwritten by Q1 R2^-1. Otherwise Y is
+  // untouched and the caller falls back to Householder.
+  static bool cholqr2_fast(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
+    constexpr bool f64 = std::is_same<T, double>::value;
+    const double thresh = f64 ? 1e-5 : 1e-2;
+    DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream);
+    DevBuf st(2 * sizeof(int), ctx->stream), tmp(sizeof(T) * rows * cols, ctx->stream), Rt;
+    if constexpr (!f64) Rt = DevBuf(sizeof(float) * cols * cols, ctx->stream);
+    float* rt = f64 ? nullptr : Rt.as<float>();
+    auto apply = [&](const T* X, T* out) {  // out = X Rinv
+      if constexpr (f64)
+        gemm<double>(ctx, rows, cols, cols, 1.0, X, 1, rows, Rinv.as<double>(), 1, cols, 0.0, out, 1, rows);
+      else
+        gemm<float>(ctx, rows, cols, cols, 1.f, X, 1, rows, rt, 1, cols, 0.f, out, 1, rows);
+    };
+    gram(ctx, rows, cols, Y, G.as<double>());
+    trace_mark(ctx, "cholqr2: gram 1");
+    small_chol_inv<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, nullptr, 0, thresh, st.as<int>());
+    trace_mark(ctx, "cholqr2: chol+inv 1");
+    apply(Y, tmp.as<T>());
+    trace_mark(ctx, "cholqr2: Y R^-1");
+    gram(ctx, rows, cols, tmp.as<T>(), G.as<double>());
+    trace_mark(ctx, "cholqr2: gram 2");
+    small_chol_inv<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, tmp.as<T>(), rows, thresh, st.as<int>() + 1);
+    int hs[2] = {0, 0};
+    RNLA_CUDA(cudaMemcpyAsync(hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    trace_mark(ctx, "cholqr2: chol+inv 2");
+    if ((hs[0] & 3) || (hs[1] & 3)) return false;
+    apply(tmp.as<T>(), Y);
+    trace_mark(ctx, "cholqr2: Q1 R2^-1");
+    if (hs[1] & 4) sign_fix(ctx, rows, cols, Y);
+    return true;
   }
 
   static void tsqr(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
@@ -339,20 +390,26 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
     if (st != RNLA_OK) throw InvalidArgument(rnla_last_error());
     require(cols == s, "prototype_ksvd: sketch returned a different width");
   }
+  trace_mark(ctx, "ksvd: Y = A S");
   const int dt = std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32;
   DevBuf Z(sizeof(T) * n * s, ctx->stream);
   for (int32_t it = 0; it < q; ++it) {
     KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), sharded);
+    trace_mark(ctx, "ksvd: orth(Y)");
     // Z = orth(A' Q): n x s (a sum over row shards)
     gemm<T>(ctx, n, s, m, T(1), Ap, A.cs, A.rs, Y.as<T>(), 1, m, T(0), Z.as<T>(), 1, n);
     if (sharded) allreduce_sum(ctx, Z.p, (size_t)(n * s), dt);
     ++passes;
+    trace_mark(ctx, "ksvd: Z = A' Q");
     KsvdWork<T>::orth(ctx, n, s, Z.as<T>(), false);
+    trace_mark(ctx, "ksvd: orth(Z)");
     // Y = A Z
     gemm<T>(ctx, m, s, n, T(1), Ap, A.rs, A.cs, Z.as<T>(), 1, n, T(0), Y.as<T>(), 1, m);
     ++passes;
+    trace_mark(ctx, "ksvd: Y = A Z");
   }
   KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), sharded);  // Q = thin_qr(C).Q
+  trace_mark(ctx, "ksvd: orth(Y)");
   // pass 2: B = Q' A (s x n), column-major
   // computed as B' = A' Q (the streaming orientation of the A' Q power step),
   // written transposed: element (i, j) of B' lands at B[j + i*s].
@@ -369,8 +426,10 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
     copy2d_cast<float, double>(ctx, s, n, B.as<float>(), 1, s, B64.as<double>(), 1, s);
     Bp = B64.as<double>();
   }
+  trace_mark(ctx, "ksvd: B = Q' A");
   const int64_t kk = std::min(k, std::min(s, n));
   SvdDev small = topk_svd_wide(ctx, s, n, Bp, kk);
+  trace_mark(ctx, "ksvd: small SVD");
   const int64_t rk = std::min(kk, small.rank);
   // U = Q Ubar (m x rk)
   DevBuf U64(sizeof(double) * m * std::max<int64_t>(rk, 1), ctx->stream);
@@ -384,6 +443,7 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   }
   store_block(ctx, U64.as<double>(), m, rk, m, uo);
   store_block(ctx, small.V.as<double>(), n, rk, n, vo);
+  trace_mark(ctx, "ksvd: U = Q Ubar, stores");
   for (int64_t i = 0; i < rk; ++i) sv_out[i] = small.s[(size_t)i];
   *rank_out = rk;
   *passes_out = passes;

@@ -366,4 +366,139 @@ int64_t eig_sym_top(rnla_ctx* ctx, int64_t n, double* A, int64_t k, double* W) {
   return found;
 }
 
+// ---------------------------------------------------------------------------
+// One-CTA Cholesky + triangular inverse for the CholeskyQR2 passes of
+// tall-skinny orthonormalization (n <= kSmallCholMax): no cuSOLVER call and no
+// host round trip per pass (the potrf info read, the diagonal-ratio check and
+// the sign probe each synchronized the stream before).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kSmallCholThreads = 1024;
+
+// G (n x n, column-major, upper triangle read) = R'R; Rinv = R^-1 (column-major,
+// exact zeros below the diagonal), optionally also as fp32. status bits:
+// 1 = not positive definite / non-finite, 2 = min|r_ii| <= thresh * max|r_ii|,
+// 4 = sign of a column of Q = Y Rinv undecidable from row 0 (|q0| < 1e-6).
+// With y0 set, columns of Rinv are negated so that row 0 of Y Rinv is >= 0
+// (the reference's sign rule, src/core.cpp:15-33).
+template <class T>
+__global__ void __launch_bounds__(kSmallCholThreads) small_chol_inv_kernel(int n, const double* __restrict__ G,
+                                                                          double* __restrict__ Rinv, float* Rinv32,
+                                                                          const T* __restrict__ y0, int64_t y_cs,
+                                                                          double thresh, int* status) {
+  extern __shared__ double sm[];  // R / X: [n][n + 1], element (i, j) at i * (n + 1) + j
+  __shared__ double dmin, dmax;
+  __shared__ int bad;
+  const int ld = n + 1, tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e % n, j = e / n;
+    sm[i * ld + j] = i <= j ? G[e] : 0.0;
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  // right-looking upper Cholesky in the square-root-free form: step k updates
+  // the trailing upper triangle with row k unscaled, A(i, j) -= A(k, i) A(k, j) / A(k, k),
+  // so one barrier per step suffices; rows are scaled by 1/sqrt(A(k, k)) at the end.
+  // Threads form a 32 x (nt/32) grid over the trailing (i, j), i <= j.
+  const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
+  for (int k = 0; k < n; ++k) {
+    const double d = sm[k * ld + k];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) bad = 1;
+      break;  // uniform: every thread read the same d
+    }
+    const double inv = 1.0 / d;
+    for (int i = k + 1 + ty; i < n; i += nty) {
+      const double aki = sm[k * ld + i] * inv;
+      for (int j = i + tx; j < n; j += 32) sm[i * ld + j] -= aki * sm[k * ld + j];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) *status = 1;
+    return;
+  }
+  for (int k = ty; k < n; k += nty) {
+    const double dk = sqrt(sm[k * ld + k]), r = 1.0 / dk;
+    for (int j = k + 1 + tx; j < n; j += 32) sm[k * ld + j] *= r;
+    __syncwarp();
+    if (tx == 0) sm[k * ld + k] = dk;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double lo = INFINITY, hi = 0.0;
+    for (int k = 0; k < n; ++k) {
+      lo = fmin(lo, fabs(sm[k * ld + k]));
+      hi = fmax(hi, fabs(sm[k * ld + k]));
+    }
+    dmin = lo;
+    dmax = hi;
+  }
+  __syncthreads();
+  int st = (dmax > 0.0 && dmin > thresh * dmax) ? 0 : 2;
+  // in-place upper triangular inverse, column by column:
+  // X(0:j, j) = -X(j, j) * X(0:j, 0:j) R(0:j, j), X(j, j) = 1 / R(j, j).
+  // Warp w owns rows i = w, w + 32, ...; its lanes split the p-sum, then a
+  // shuffle reduction (fixed order) gives tmp[i].
+  double* tmp = sm + (size_t)n * ld;  // n scratch doubles
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int j = 0; j < n; ++j) {
+    const double xjj = 1.0 / sm[j * ld + j];
+    for (int i = wid; i < j; i += nw) {
+      double acc = 0.0;
+      for (int p = i + lane; p < j; p += 32) acc += sm[i * ld + p] * sm[p * ld + j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) tmp[i] = acc;
+    }
+    __syncthreads();
+    for (int i = tid; i < j; i += nt) sm[i * ld + j] = -xjj * tmp[i];
+    if (tid == 0) sm[j * ld + j] = xjj;
+    __syncthreads();
+  }
+  if (y0) {
+    for (int j = tid; j < n; j += nt) {
+      double q0 = 0.0;
+      for (int p = 0; p <= j; ++p) q0 += (double)y0[p * y_cs] * sm[p * ld + j];
+      tmp[j] = q0;
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += nt) {
+      const int i = e / n, j = e % n;
+      if (i <= j && tmp[j] < 0.0) sm[i * ld + j] = -sm[i * ld + j];
+    }
+    if (tid == 0)
+      for (int j = 0; j < n; ++j)
+        if (fabs(tmp[j]) < 1e-6) st |= 4;
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e % n, j = e / n;
+    const double v = i <= j ? sm[i * ld + j] : 0.0;
+    Rinv[e] = v;
+    if (Rinv32) Rinv32[e] = (float)v;
+  }
+  if (tid == 0) *status = st;
+}
+
+}  // namespace
+
+template <class T>
+void small_chol_inv(rnla_ctx* ctx, int64_t n, const double* G, double* Rinv, float* Rinv32, const T* y0, int64_t y_cs,
+                    double thresh, int* status) {
+  require(n >= 1 && n <= 160, "small_chol_inv: n out of range");
+  const size_t smem = sizeof(double) * ((size_t)n * (n + 1) + n);
+  ensure_dyn_smem((const void*)small_chol_inv_kernel<T>, smem);
+  small_chol_inv_kernel<T><<<1, kSmallCholThreads, smem, ctx->stream>>>((int)n, G, Rinv, Rinv32, y0, y_cs, thresh,
+                                                                        status);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+template void small_chol_inv<double>(rnla_ctx*, int64_t, const double*, double*, float*, const double*, int64_t,
+                                     double, int*);
+template void small_chol_inv<float>(rnla_ctx*, int64_t, const double*, double*, float*, const float*, int64_t, double,
+                                    int*);
+
 }  // namespace rnla
