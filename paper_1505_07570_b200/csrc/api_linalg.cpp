@@ -836,8 +836,13 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
                      T.as<double>(), d, 1);
         row_sqnorms<double>(ctx, rows, d, T.as<double>(), d, 1, sc.as<double>() + r0);
       } else {
-        gemm<float>(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
-                    T.as<float>(), d, 1);
+        // R^-1 is upper triangular: column tile j needs k < its last column only
+        if (tc_gemm_enabled())
+          gemm_f32_tc_tri_b(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
+                            T.as<float>(), d, 1);
+        else
+          gemm<float>(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
+                      T.as<float>(), d, 1);
         row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
       }
     }

@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   using OutT = typename std::conditional<DF, double, float>::type;
   // symmetric products (C = A'A): tiles strictly below the diagonal are skipped
   // (uniformly for the whole CTA, before any barrier) and mirrored afterwards
-  if (sym && (int64_t)blockIdx.x * TC_BM >= ((int64_t)blockIdx.y + 1) * BN) return;
+  // (sym bit 0). Bit 1: B is upper triangular (B(p, j) = 0 for p > j, the
+  // leverage-score product M R^-1), so this N tile needs k < n0 + BN only.
+  if ((sym & 1) && (int64_t)blockIdx.x * TC_BM >= ((int64_t)blockIdx.y + 1) * BN) return;
   constexpr int PKB = DF ? 256 / TC_BK : TC_PROMOTE_KB;
   // DF also splits three ways (BF16x6: hh, hm, mh, hl, lh, mm ~ fp32-faithful
   // products, 1.9e-7 rel-F per SURVEY §7 hard part 5); otherwise BF16x3.
@@ -426,7 +428,8 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m0 = (int64_t)blockIdx.x * TC_BM, n0 = (int64_t)blockIdx.y * BN;
-  const int64_t kbeg = (int64_t)blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t kend = (sym & 2) ? min(min(K, kbeg + kchunk), n0 + BN) : min(K, kbeg + kchunk);
   const int nkb = (int)((kend - kbeg + TC_BK - 1) / TC_BK);
 
   if (tid == 0) {
@@ -771,7 +774,8 @@ __global__ void mirror_skipped_tiles(int64_t n, int bm, int bn, OutT* C, int64_t
 template <bool DF>
 void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                   int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta,
-                  typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs) {
+                  typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
+                  bool tri_b = false) {
   using OutT = typename std::conditional<DF, double, float>::type;
   if (m == 0 || n == 0) return;
   // one N tile up to 160 columns (3 fp32 accumulators fit TMEM; 128 with the
@@ -816,9 +820,11 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
       if (eff >= 0.97) break;
     }
   }
+  if (tri_b) splits = 1;  // every CTA's clipped k range then starts at 0
   int64_t kchunk = ((k + splits - 1) / splits + TC_BK - 1) / TC_BK * TC_BK;
   if (k == 0) kchunk = TC_BK;
   splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
+  const int flags = sym | (tri_b && !sym ? 2 : 0);
   DevBuf wsb;
   OutT* ws = nullptr;
   if (splits > 1) {
@@ -829,10 +835,10 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   const bool tma = make_a_map(&amap, A, m, k, a_rs, a_cs);
   if (a_cs == 1)
     dispatch_bn<true, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
-                          c_rs, c_cs, ws, sym, tma ? &amap : nullptr);
+                          c_rs, c_cs, ws, flags, tma ? &amap : nullptr);
   else
     dispatch_bn<false, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
-                           c_rs, c_cs, ws, sym, tma ? &amap : nullptr);
+                           c_rs, c_cs, ws, flags, tma ? &amap : nullptr);
   if (splits > 1) {
     splitk_reduce_tc<OutT><<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, n, (int)splits, ws, alpha, beta, C,
                                                                                c_rs, c_cs);
@@ -870,6 +876,14 @@ void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, co
                  int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
                  int64_t c_cs) {
   gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs);
+}
+
+// Same with B upper triangular (B(p, j) = 0 for p > j): each N tile stops at
+// k = its last column, skipping the zero blocks.
+void gemm_f32_tc_tri_b(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
+                       int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
+                       int64_t c_cs) {
+  gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs, true);
 }
 
 // Same with double-float accumulation across 256-row chunks and fp64 output.

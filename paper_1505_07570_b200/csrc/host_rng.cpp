@@ -70,12 +70,23 @@ std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w
   require(total > 0.0, "sample_with_replacement: all weights zero");
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> unif(0.0, total);
+  std::vector<double> u(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) u[static_cast<size_t>(i)] = unif(rng);
+  // upper_bound(cum, u_i) for every draw, found by one sweep over cum in
+  // ascending u order instead of count binary searches over an n-element
+  // array (cache-missing at n = 2^20); cum is non-decreasing, so the sweep
+  // returns exactly the upper_bound positions.
+  std::vector<int64_t> order(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) order[static_cast<size_t>(i)] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t a, int64_t b) { return u[static_cast<size_t>(a)] < u[static_cast<size_t>(b)]; });
   std::vector<int64_t> out(static_cast<size_t>(count));
-  for (int64_t i = 0; i < count; ++i) {
-    const double u = unif(rng);
-    int64_t j = static_cast<int64_t>(std::upper_bound(cum.begin(), cum.end(), u) - cum.begin());
-    if (j >= n) j = n - 1;
-    out[static_cast<size_t>(i)] = j;
+  int64_t j = 0;
+  for (int64_t r = 0; r < count; ++r) {
+    const int64_t i = order[static_cast<size_t>(r)];
+    const double ui = u[static_cast<size_t>(i)];
+    while (j < n && cum[static_cast<size_t>(j)] <= ui) ++j;
+    out[static_cast<size_t>(i)] = j >= n ? n - 1 : j;
   }
   return out;
 }

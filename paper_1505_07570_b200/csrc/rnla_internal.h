@@ -173,6 +173,10 @@ bool tc_gemm_enabled();
 void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
                  int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
                  int64_t c_cs);
+// gemm_f32_tc with B upper triangular (zero blocks below the diagonal skipped).
+void gemm_f32_tc_tri_b(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
+                       int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
+                       int64_t c_cs);
 
 // Same on tcgen05 with double-float (~fp64) accumulation across 256-row chunks, fp64 output.
 void gemm_f32_tc_f64acc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,

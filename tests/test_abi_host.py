@@ -72,6 +72,13 @@ def test_host_sampling_matches_oracle(golden):
         assert np.array_equal(got, orc.sample_without_replacement(case["n"], case["count"], int(case["seed"])))
     w = np.random.default_rng(0).random(1000)
     assert np.array_equal(rn.sample_with_replacement(w, 300, 5), orc.sample_with_replacement(w, 300, 5))
+    # zero weights, repeated draws (count > n) and ties: the sorted sweep must
+    # return exactly upper_bound, in draw order
+    w2 = np.random.default_rng(1).random(5000) ** 4
+    w2[::7] = 0.0
+    w2[-50:] = 0.0
+    for seed, cnt in [(3, 1), (11, 4096), (12, 20000)]:
+        assert np.array_equal(rn.sample_with_replacement(w2, cnt, seed), orc.sample_with_replacement(w2, cnt, seed))
     for case in golden["srht"]:
         sg, idx = rn.srht_operator(case["n"], case["s"], int(case["seed"]))
         assert sg.tolist() == case["signs"] and idx.tolist() == case["idx"]
