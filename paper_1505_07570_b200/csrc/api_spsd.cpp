@@ -197,37 +197,43 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   // Otherwise the eigendecomposition route below runs.
   DevBuf Tm;  // s x kp: L = C Tm
   int64_t kp = 0;
-  if (kk >= s && !std::getenv("RNLA_NYSTROM_EIGW")) {
-    DevBuf Ws(sizeof(double) * s * s, ctx->stream), R(sizeof(double) * s * s, ctx->stream),
-        Ri(sizeof(double) * s * s, ctx->stream);
-    symmetrize(ctx, s, W.as<double>(), Ws.as<double>());
-    RNLA_CUDA(cudaMemcpyAsync(R.p, Ws.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (cholesky_upper(ctx, s, R.as<double>())) {
-      upper_inverse(ctx, s, R.as<double>(), Ri.as<double>());
-      const double inv_fro2 = sum_squares_dev(ctx, Ri.as<double>(), s * s);
-      const double w_fro = std::sqrt(sum_squares_dev(ctx, Ws.as<double>(), s * s));
-      const double floor_ub = std::numeric_limits<double>::epsilon() * w_fro * static_cast<double>(n);
-      if (std::isfinite(inv_fro2) && inv_fro2 > 0.0 && 1.0 / inv_fro2 > 4.0 * floor_ub) {
-        Tm = std::move(Ri);
-        kp = s;
-      }
-    }
-    trace_mark(ctx, "nystrom_eig: Cholesky route test");
-  }
-  // Otherwise eig(W) (cuSOLVER syevd, latency-bound) runs on the helper
-  // context from a second host thread while this thread accumulates C'C
-  // (DMMA-bound), its kernels dispatched first from the high-priority stream.
+  auto cholesky_route = [&](rnla_ctx* c) {
+    DevBuf Ws(sizeof(double) * s * s, c->stream), R(sizeof(double) * s * s, c->stream),
+        Ri(sizeof(double) * s * s, c->stream);
+    symmetrize(c, s, W.as<double>(), Ws.as<double>());
+    RNLA_CUDA(cudaMemcpyAsync(R.p, Ws.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, c->stream));
+    if (!cholesky_upper(c, s, R.as<double>())) return false;
+    upper_inverse(c, s, R.as<double>(), Ri.as<double>());
+    const double inv_fro2 = sum_squares_dev(c, Ri.as<double>(), s * s);
+    const double w_fro = std::sqrt(sum_squares_dev(c, Ws.as<double>(), s * s));
+    const double floor_ub = std::numeric_limits<double>::epsilon() * w_fro * static_cast<double>(n);
+    if (!(std::isfinite(inv_fro2) && inv_fro2 > 0.0 && 1.0 / inv_fro2 > 4.0 * floor_ub)) return false;
+    RNLA_CUDA(cudaStreamSynchronize(c->stream));
+    Tm = std::move(Ri);
+    kp = s;
+    return true;
+  };
+  const bool try_cholesky = kk >= s && !std::getenv("RNLA_NYSTROM_EIGW");
+  // The Cholesky route, and eig(W) when it does not apply (cuSOLVER syevd,
+  // latency-bound), run on the helper context from a second host thread
+  // while this thread accumulates C'C (DMMA-bound), their kernels dispatched
+  // from the high-priority stream.
   EigW e;
+  bool need_eig = false;
   std::exception_ptr eig_err;
-  const bool need_eig = kp == 0;
-  const bool overlap = need_eig && !std::getenv("RNLA_NYSTROM_SERIAL");
+  const bool overlap = !std::getenv("RNLA_NYSTROM_SERIAL");
   rnla_ctx* side = overlap ? side_ctx(ctx) : nullptr;
+  if (!overlap && try_cholesky) cholesky_route(ctx);
+  if (!overlap) need_eig = kp == 0;
   std::thread eig_thread;
   if (overlap)
     eig_thread = std::thread([&] {
       try {
         RNLA_CUDA(cudaSetDevice(side->device));
-        e = nystrom_core(side, W.as<double>(), s, n, kk);
+        if (!(try_cholesky && cholesky_route(side))) {
+          need_eig = true;
+          e = nystrom_core(side, W.as<double>(), s, n, kk);
+        }
       } catch (...) {
         eig_err = std::current_exception();
       }
@@ -264,8 +270,8 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   } else if (need_eig) {
     e = nystrom_core(ctx, W.as<double>(), s, n, kk);
   }
+  trace_mark(ctx, kp > 0 ? "nystrom_eig: Cholesky route (overlapped)" : "nystrom_eig: eig(W)");
   if (need_eig) {
-    trace_mark(ctx, "nystrom_eig: eig(W)");
     Tm = whitened(ctx, e, s);
     kp = e.kept;
   }
