@@ -149,9 +149,7 @@ struct KsvdWork {
       tsqr(ctx, rows, cols, Y);
       return;
     }
-    if (rows >= 4 * cols &&
-        (cols <= kSmallCholMax ? cholqr2_fast(ctx, rows, cols, Y) : cholqr2(ctx, rows, cols, Y, false)))
-      return;
+    if (rows >= 4 * cols && cholqr2_fast(ctx, rows, cols, Y)) return;
     householder(ctx, rows, cols, Y);
   }
 
@@ -184,15 +182,23 @@ struct KsvdWork {
       else
         gemm<float>(ctx, rows, cols, cols, 1.f, X, 1, rows, rt, 1, cols, 0.f, out, 1, rows);
     };
+    // one-CTA factorization for narrow blocks, cuSOLVER potrf + trsm above
+    auto factor = [&](const T* y0, int* status) {
+      if (cols <= kSmallCholMax)
+        small_chol_inv<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, y0, rows, thresh, status);
+      else
+        chol_inv_async<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, y0, rows, thresh, status);
+    };
+    RNLA_CUDA(cudaMemsetAsync(st.p, 0, 2 * sizeof(int), ctx->stream));
     gram(ctx, rows, cols, Y, G.as<double>());
     trace_mark(ctx, "cholqr2: gram 1");
-    small_chol_inv<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, nullptr, 0, thresh, st.as<int>());
+    factor(nullptr, st.as<int>());
     trace_mark(ctx, "cholqr2: chol+inv 1");
     apply(Y, tmp.as<T>());
     trace_mark(ctx, "cholqr2: Y R^-1");
     gram(ctx, rows, cols, tmp.as<T>(), G.as<double>());
     trace_mark(ctx, "cholqr2: gram 2");
-    small_chol_inv<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, tmp.as<T>(), rows, thresh, st.as<int>() + 1);
+    factor(tmp.as<T>(), st.as<int>() + 1);
     int hs[2] = {0, 0};
     RNLA_CUDA(cudaMemcpyAsync(hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));

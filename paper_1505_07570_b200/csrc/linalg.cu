@@ -93,6 +93,11 @@ void fix_column_signs(rnla_ctx* ctx, int64_t rows, int64_t cols, double* M, int6
 }
 
 namespace {
+// *status |= bit when *flag is set
+__global__ void or_flag_kernel(const int* flag, int bit, int* status) {
+  if (*flag) *status |= bit;
+}
+
 // q0_j = sum_p Y(0, p) Rinv(p, j) in fp64; negate column j of Rinv when
 // q0_j < 0 so that Q = Y Rinv comes out with the reference's sign rule
 // (first entry with |q| > 1e-12 non-negative, src/core.cpp:15-33). Entries
@@ -500,6 +505,88 @@ void small_chol_inv(rnla_ctx* ctx, int64_t n, const double* G, double* Rinv, flo
 template void small_chol_inv<double>(rnla_ctx*, int64_t, const double*, double*, float*, const double*, int64_t,
                                      double, int*);
 template void small_chol_inv<float>(rnla_ctx*, int64_t, const double*, double*, float*, const float*, int64_t, double,
+                                    int*);
+
+// ---------------------------------------------------------------------------
+// The same CholeskyQR2 factorization step for wider blocks (n > kSmallCholMax)
+// on cuSOLVER/cuBLAS, without host round trips: potrf's info, the diagonal
+// ratio and the sign probe all land in a device status word.
+// ---------------------------------------------------------------------------
+namespace {
+// status |= 1 (potrf info != 0 or a non-finite diagonal), |= 2 (min |r_ii| <= thresh * max |r_ii|)
+__global__ void chol_status_kernel(int64_t n, const double* __restrict__ R, const int* __restrict__ info,
+                                   double thresh, int* status) {
+  __shared__ double lo_s[32], hi_s[32];
+  __shared__ int bad_s;
+  if (threadIdx.x == 0) bad_s = 0;
+  __syncthreads();
+  double lo = INFINITY, hi = 0.0;
+  int bad = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = fabs(R[i * (n + 1)]);
+    if (!isfinite(v)) bad = 1;
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (bad) atomicOr(&bad_s, 1);
+  if ((threadIdx.x & 31) == 0) {
+    lo_s[threadIdx.x >> 5] = lo;
+    hi_s[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = fmin(lo, lo_s[w]);
+      hi = fmax(hi, hi_s[w]);
+    }
+    int st = 0;
+    if (*info != 0 || bad_s) st |= 1;
+    else if (!(hi > 0.0 && lo > thresh * hi)) st |= 2;
+    *status |= st;
+  }
+}
+}  // namespace
+
+template <class T>
+void chol_inv_async(rnla_ctx* ctx, int64_t n, double* G, double* Rinv, float* Rinv32, const T* y0, int64_t y_cs,
+                    double thresh, int* status) {
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0;
+  cusolver_check(cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, (int)n, G, (int)n, &lwork),
+                 "potrf_bufferSize");
+  DevBuf work(sizeof(double) * std::max(lwork, 1), ctx->stream), info(sizeof(int), ctx->stream);
+  cusolver_check(cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, (int)n, G, (int)n, work.as<double>(), lwork,
+                                  info.as<int>()),
+                 "potrf");
+  chol_status_kernel<<<1, 256, 0, ctx->stream>>>(n, G, info.as<int>(), thresh, status);
+  RNLA_CUDA(cudaGetLastError());
+  identity_kernel<<<grid_for(ctx, n * n, 256), 256, 0, ctx->stream>>>(n, Rinv);
+  RNLA_CUDA(cudaGetLastError());
+  const double one = 1.0;
+  if (cublasDtrsm(static_cast<cublasHandle_t>(ctx->cublas), CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                  CUBLAS_DIAG_NON_UNIT, (int)n, (int)n, &one, G, (int)n, Rinv, (int)n) != CUBLAS_STATUS_SUCCESS)
+    throw CudaError("cublasDtrsm failed");
+  note_launch(ctx, 4);
+  if (y0) {
+    DevBuf amb(sizeof(int), ctx->stream);
+    RNLA_CUDA(cudaMemsetAsync(amb.p, 0, sizeof(int), ctx->stream));
+    presign_kernel<T><<<1, 256, 0, ctx->stream>>>(n, y0, y_cs, Rinv, amb.as<int>());
+    RNLA_CUDA(cudaGetLastError());
+    or_flag_kernel<<<1, 1, 0, ctx->stream>>>(amb.as<int>(), 4, status);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx, 2);
+  }
+  if (Rinv32) {
+    copy2d_cast<double, float>(ctx, n, n, Rinv, 1, n, Rinv32, 1, n);
+  }
+}
+template void chol_inv_async<double>(rnla_ctx*, int64_t, double*, double*, float*, const double*, int64_t, double,
+                                     int*);
+template void chol_inv_async<float>(rnla_ctx*, int64_t, double*, double*, float*, const float*, int64_t, double,
                                     int*);
 
 }  // namespace rnla

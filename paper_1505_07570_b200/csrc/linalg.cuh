@@ -45,6 +45,11 @@ bool diag_ratio_ok(rnla_ctx* ctx, int64_t n, const double* R, double thresh);
 // Above 64 columns the per-column barriers of the one-CTA inverse cost more
 // than cuSOLVER potrf + trsm (measured 0.39 ms vs ~0.25 ms at n = 150).
 constexpr int64_t kSmallCholMax = 64;
+// Same contract for any n on cuSOLVER potrf + cuBLAS trsm (G is overwritten by
+// R), with no host round trip. Rinv32 (nullable) gets an fp32 copy.
+template <class T>
+void chol_inv_async(rnla_ctx* ctx, int64_t n, double* G, double* Rinv, float* Rinv32, const T* y0, int64_t y_cs,
+                    double thresh, int* status);
 template <class T>
 void small_chol_inv(rnla_ctx* ctx, int64_t n, const double* G, double* Rinv, float* Rinv32, const T* y0, int64_t y_cs,
                     double thresh, int* status);
