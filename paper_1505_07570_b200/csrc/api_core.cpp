@@ -270,6 +270,9 @@ static void ctx_release(rnla_ctx* ctx) {
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   ctx->nccl = ctx->cusolver = ctx->cublas = nullptr;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  ctx->pinned = nullptr;
+  ctx->pinned_bytes = 0;
   cudaStreamDestroy(ctx->copy_stream);
   cudaStreamDestroy(ctx->aux_stream);
   cudaStreamDestroy(ctx->stream);
@@ -278,6 +281,18 @@ static void ctx_release(rnla_ctx* ctx) {
 }  // extern "C"
 
 namespace rnla {
+void* pinned_scratch(rnla_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->pinned_bytes) {
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // the old buffer may still be a copy target
+    if (ctx->pinned) RNLA_CUDA(cudaFreeHost(ctx->pinned));
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    RNLA_CUDA(cudaHostAlloc(&ctx->pinned, bytes, cudaHostAllocDefault));
+    ctx->pinned_bytes = bytes;
+  }
+  return ctx->pinned;
+}
+
 rnla_ctx* side_ctx(rnla_ctx* ctx) {
   std::lock_guard<std::mutex> lk(ctx->mu);
   if (!ctx->side) {

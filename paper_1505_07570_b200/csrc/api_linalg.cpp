@@ -835,43 +835,88 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
       Rf = DevBuf(sizeof(float) * d * d, ctx->stream);
       copy2d_cast<double, float>(ctx, d, d, Rinv.as<double>(), 1, d, Rf.as<float>(), 1, d);
     }
-    for (int64_t r0 = 0; r0 < n; r0 += blk) {
-      const int64_t rows = std::min(blk, n - r0);
-      if (M.dtype == RNLA_F64) {
-        gemm<double>(ctx, rows, d, d, 1.0, M.as<double>() + r0 * M.rs, M.rs, M.cs, Rinv.as<double>(), 1, d, 0.0,
-                     T.as<double>(), d, 1);
-        row_sqnorms<double>(ctx, rows, d, T.as<double>(), d, 1, sc.as<double>() + r0);
-      } else {
-        // R^-1 is upper triangular: column tile j needs k < its last column only
-        if (tc_gemm_enabled())
-          gemm_f32_tc_tri_b(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
-                            T.as<float>(), d, 1);
-        else
-          gemm<float>(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
-                      T.as<float>(), d, 1);
-        row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
+    // One GPU: each block's scores go to pinned host memory as soon as they
+    // are computed, and the host extends the sequential fp64 prefix sums of
+    // the draw (src/rng.cpp:42-65) while the device computes the next blocks.
+    const bool stream_draw = indices != nullptr && ctx->world == 1 && n > 0;
+    double* hs = stream_draw ? static_cast<double*>(pinned_scratch(ctx, sizeof(double) * n)) : nullptr;
+    const int64_t nblk = (n + blk - 1) / blk;
+    std::vector<cudaEvent_t> ev;
+    WeightPrefix prefix;
+    int64_t done = 0;  // blocks folded into prefix
+    auto fold = [&](int64_t upto) {
+      for (; done < upto; ++done) {
+        const int64_t r0 = done * blk, rows = std::min(blk, n - r0);
+        RNLA_CUDA(cudaEventSynchronize(ev[(size_t)done]));
+        prefix.extend(hs + r0, rows);
       }
+    };
+    if (stream_draw) {
+      ev.resize((size_t)nblk);
+      for (auto& e : ev) RNLA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      prefix.cum.reserve((size_t)n);
     }
+    try {
+      for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int64_t r0 = bi * blk, rows = std::min(blk, n - r0);
+        if (M.dtype == RNLA_F64) {
+          gemm<double>(ctx, rows, d, d, 1.0, M.as<double>() + r0 * M.rs, M.rs, M.cs, Rinv.as<double>(), 1, d, 0.0,
+                       T.as<double>(), d, 1);
+          row_sqnorms<double>(ctx, rows, d, T.as<double>(), d, 1, sc.as<double>() + r0);
+        } else {
+          // R^-1 is upper triangular: column tile j needs k < its last column only
+          if (tc_gemm_enabled())
+            gemm_f32_tc_tri_b(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
+                              T.as<float>(), d, 1);
+          else
+            gemm<float>(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
+                        T.as<float>(), d, 1);
+          row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
+        }
+        if (stream_draw) {
+          RNLA_CUDA(cudaMemcpyAsync(hs + r0, sc.as<double>() + r0, sizeof(double) * rows, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+          RNLA_CUDA(cudaEventRecord(ev[(size_t)bi], ctx->stream));
+          fold(bi);  // blocks before this one, while the device works on it
+        }
+      }
+      if (stream_draw) fold(nblk);
+    } catch (...) {
+      cudaStreamSynchronize(ctx->stream);
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto& e : ev) RNLA_CUDA(cudaEventDestroy(e));
     trace_mark(ctx, "leverage_rows: scores");
-    if (n > 0) RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (stream_draw) {
+      std::copy(hs, hs + n, scores);
+    } else {
+      if (n > 0) RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     trace_mark(ctx, "leverage_rows: d2h");
     if (indices) {
-      std::vector<double> all_scores;
-      const double* w = scores;
-      if (ctx->world > 1) {
-        DevBuf g(sizeof(double) * n_total, ctx->stream);
-        RNLA_CUDA(cudaMemsetAsync(g.p, 0, sizeof(double) * n_total, ctx->stream));
-        if (n > 0)
-          RNLA_CUDA(cudaMemcpyAsync(g.as<double>() + r_off, sc.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+      std::vector<int64_t> draws;
+      if (stream_draw) {
+        draws = prefix.draw(seed, p);
+      } else {
+        std::vector<double> all_scores;
+        const double* w = scores;
+        if (ctx->world > 1) {
+          DevBuf g(sizeof(double) * n_total, ctx->stream);
+          RNLA_CUDA(cudaMemsetAsync(g.p, 0, sizeof(double) * n_total, ctx->stream));
+          if (n > 0)
+            RNLA_CUDA(cudaMemcpyAsync(g.as<double>() + r_off, sc.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                      ctx->stream));
+          allreduce_sum(ctx, g.p, (size_t)n_total, RNLA_F64);
+          all_scores.resize((size_t)n_total);
+          RNLA_CUDA(cudaMemcpyAsync(all_scores.data(), g.p, sizeof(double) * n_total, cudaMemcpyDeviceToHost,
                                     ctx->stream));
-        allreduce_sum(ctx, g.p, (size_t)n_total, RNLA_F64);
-        all_scores.resize((size_t)n_total);
-        RNLA_CUDA(cudaMemcpyAsync(all_scores.data(), g.p, sizeof(double) * n_total, cudaMemcpyDeviceToHost, ctx->stream));
-        RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
-        w = all_scores.data();
+          RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+          w = all_scores.data();
+        }
+        draws = sample_with_replacement_host(seed, w, n_total, p);
       }
-      std::vector<int64_t> draws = sample_with_replacement_host(seed, w, n_total, p);
       std::sort(draws.begin(), draws.end());
       draws.erase(std::unique(draws.begin(), draws.end()), draws.end());
       std::copy(draws.begin(), draws.end(), indices);

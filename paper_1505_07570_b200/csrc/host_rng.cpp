@@ -58,16 +58,18 @@ std::vector<int64_t> sample_without_replacement_host(uint64_t seed, int64_t n, i
   return swor(rng, n, count);
 }
 
-std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w, int64_t n, int64_t count) {
-  require(count >= 1, "sample_with_replacement: count < 1");
-  std::vector<double> cum(static_cast<size_t>(n));
-  double total = 0.0;
-  for (int64_t i = 0; i < n; ++i) {
+void WeightPrefix::extend(const double* w, int64_t m) {
+  for (int64_t i = 0; i < m; ++i) {
     require(w[i] >= 0.0, "sample_with_replacement: negative weight");
     total += w[i];
-    cum[static_cast<size_t>(i)] = total;
+    cum.push_back(total);
   }
+}
+
+std::vector<int64_t> WeightPrefix::draw(uint64_t seed, int64_t count) const {
+  require(count >= 1, "sample_with_replacement: count < 1");
   require(total > 0.0, "sample_with_replacement: all weights zero");
+  const int64_t n = (int64_t)cum.size();
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> unif(0.0, total);
   std::vector<double> u(static_cast<size_t>(count));
@@ -89,6 +91,17 @@ std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w
     out[static_cast<size_t>(i)] = j >= n ? n - 1 : j;
   }
   return out;
+}
+
+// Sequential fp64 prefix sums (the reference's std::partial_sum order), one
+// engine, uniform_real_distribution(0, total), upper_bound, clamp
+// (src/rng.cpp:42-65).
+std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w, int64_t n, int64_t count) {
+  require(count >= 1, "sample_with_replacement: count < 1");
+  WeightPrefix p;
+  p.cum.reserve(static_cast<size_t>(n));
+  p.extend(w, n);
+  return p.draw(seed, count);
 }
 
 // Signs first, then the index sample, from one engine (src/sketch.cpp:61-65).

@@ -125,9 +125,16 @@ struct rnla_ctx {
   // handles) for independent work run from a second host thread, e.g. eig(W)
   // under the Nystrom C'C Gram; created lazily by side_ctx().
   std::unique_ptr<rnla_ctx> side;
+  // Pinned host staging (grown on demand, freed with the context): device
+  // results streamed to the host while later blocks still compute.
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
 
 namespace rnla {
+
+// Pinned host buffer of at least `bytes` owned by the context.
+void* pinned_scratch(rnla_ctx* ctx, size_t bytes);
 
 // ---- host operator generation (host_rng.cpp; libstdc++ like the reference) ----
 uint64_t splitmix64(uint64_t& state);
@@ -135,6 +142,15 @@ uint64_t derive_seed(uint64_t seed, uint64_t stream);
 void gaussian_matrix_host(uint64_t seed, int64_t rows, int64_t cols, double* out_colmajor);
 std::vector<int64_t> sample_without_replacement_host(uint64_t seed, int64_t n, int64_t count);
 std::vector<int64_t> sample_with_replacement_host(uint64_t seed, const double* w, int64_t n, int64_t count);
+// The same draw with the prefix sums built incrementally (blocks of weights in
+// row order, e.g. as they arrive from the device): extend() appends, draw()
+// samples once all n weights are in.
+struct WeightPrefix {
+  std::vector<double> cum;
+  double total = 0.0;
+  void extend(const double* w, int64_t m);
+  std::vector<int64_t> draw(uint64_t seed, int64_t count) const;
+};
 void srht_operator_host(uint64_t seed, int64_t n, int64_t s, int8_t* signs, int64_t* idx);
 int64_t next_pow2(int64_t n);
 
