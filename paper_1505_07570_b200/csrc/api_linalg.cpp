@@ -325,14 +325,17 @@ bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, doub
       KsvdWork<double>::orth(ctx, n, b, Q.as<double>(), false);
     }
     gemm<double>(ctx, n, b, n, 1.0, A, 1, n, Q.as<double>(), 1, n, 0.0, Y.as<double>(), 1, n);
+    trace_mark(ctx, rr ? "eig_top_subspace: orth + A Q (RR step)" : "eig_top_subspace: cholqr + A Q");
     if (!rr) continue;
     ++rr_count;
     // Rayleigh-Ritz: H = Q'AQ = (Z, theta); top-k Ritz vectors Q Z_k, images Y Z_k
     gemm<double>(ctx, b, b, n, 1.0, Q.as<double>(), n, 1, Y.as<double>(), 1, n, 0.0, H.as<double>(), 1, b);
     symmetrize(ctx, b, H.as<double>(), Hs.as<double>());
+    trace_mark(ctx, "eig_top_subspace: H = Q'AQ");
     eig_sym(ctx, b, Hs.as<double>(), th.as<double>());  // ascending
     RNLA_CUDA(cudaMemcpyAsync(ht.data(), th.p, sizeof(double) * b, cudaMemcpyDeviceToHost, ctx->stream));
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    trace_mark(ctx, "eig_top_subspace: eig(H)");
     for (int64_t t = 0; t < k; ++t) td[(size_t)t] = ht[(size_t)(b - 1 - t)];
     copy2d<double>(ctx, b, k, Hs.as<double>() + (b - 1) * b, 1, -b, Zk.as<double>(), 1, b);
     gemm<double>(ctx, n, k, b, 1.0, Q.as<double>(), 1, n, Zk.as<double>(), 1, b, 0.0, VZ.as<double>(), 1, n);
