@@ -232,6 +232,24 @@ def test_combined_is_exact_composition_large(ctx, m):
     assert relf(c, orc.combined_sketch(a, 512, 31, "gaussian", 128, 33)) <= 1e-10
 
 
+@pytest.mark.parametrize("n,L,s_cs,s2", [(9000, 77, 1000, 100), (20000, 130, 4500, 70), (5000, 64, 4096, 64)])
+def test_combined_rows_dmma_edges(ctx, n, L, s_cs, s2):
+    # row-form combined sketch: K = s_cs not a multiple of the 16-k step, odd and
+    # even L (16-B row padding of the intermediate), K split into 2048-bucket
+    # chunks when s_cs >= 4096; bitwise equal to the two-step composition
+    rng = np.random.default_rng(n + L)
+    m = rng.standard_normal((n, L))
+    b = rng.standard_normal(n)
+    spec = rn.SketchSpec.combined(s_cs, rn.SketchSpec.gaussian(s2, 5), 4)
+    got = rn.sketch_rows(dev(m), spec, extra=dev(b), ctx=ctx).cpu().numpy()
+    mid = rn.sketch_rows(dev(m), rn.SketchSpec.count_sketch(s_cs, 4), extra=dev(b), ctx=ctx)
+    two = rn.sketch_rows(mid, rn.SketchSpec.gaussian(s2, 5), ctx=ctx).cpu().numpy()
+    assert np.array_equal(got, two)
+    mid_ref = orc.count_sketch_rows(m, s_cs, 4, extra=b)
+    ref = orc.gaussian_sketch(mid_ref.T, s2, 5).T
+    assert relf(got, ref) <= 1e-10
+
+
 def test_combined_srht_stage(ctx):
     a = orc.gaussian_matrix(9, 300, 6)
     spec = rn.SketchSpec.combined(100, rn.SketchSpec.srht(32, 8), 7)
