@@ -42,9 +42,9 @@ bool diag_ratio_ok(rnla_ctx* ctx, int64_t n, const double* R, double thresh);
 // device: status (device int) bit 1 = breakdown, 2 = diag ratio below thresh,
 // 4 = row-0 sign probe undecidable; with y0 the columns of Rinv are negated
 // so that row 0 of Y Rinv is non-negative. Rinv32 (nullable) gets an fp32 copy.
-// Above 64 columns the per-column barriers of the one-CTA inverse cost more
-// than cuSOLVER potrf + trsm (measured 0.39 ms vs ~0.25 ms at n = 150).
-constexpr int64_t kSmallCholMax = 64;
+// n <= 152: the factor, the blocked inverse and their scratch fit 227 KB of
+// shared memory.
+constexpr int64_t kSmallCholMax = 152;
 // Same contract for any n on cuSOLVER potrf + cuBLAS trsm (G is overwritten by
 // R), with no host round trip. Rinv32 (nullable) gets an fp32 copy.
 template <class T>
