@@ -800,6 +800,17 @@ rnla_status rnla_leverage_sample_columns(rnla_ctx* ctx, const rnla_mat* a, int64
 // R = chol(G), l_i = ||m_i R^-1||^2 = ||Q_i,:||^2 (basis invariance, paper
 // Fact 6; tests/test_facts.cpp:86-97); then the reference's weighted draw +
 // sort + unique (src/spsd.cpp:150-154).
+namespace {
+// out[i] = sum_t part[t * rows + i], t ascending
+__global__ void sum_tiles_kernel(int64_t rows, int nt, const double* __restrict__ part, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < nt; ++t) acc += part[(int64_t)t * rows + i];
+    out[i] = acc;
+  }
+}
+}  // namespace
+
 rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t p, uint64_t seed, double* scores,
                                       int64_t* indices, int64_t* count_out) {
   return guard([&] {
@@ -867,14 +878,21 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
                        T.as<double>(), d, 1);
           row_sqnorms<double>(ctx, rows, d, T.as<double>(), d, 1, sc.as<double>() + r0);
         } else {
-          // R^-1 is upper triangular: column tile j needs k < its last column only
-          if (tc_gemm_enabled())
-            gemm_f32_tc_tri_b(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
-                              T.as<float>(), d, 1);
-          else
+          // R^-1 is upper triangular: column tile j needs k < its last column only.
+          // The GEMM epilogue sums the squares of each N tile of a row (M R^-1 is
+          // never stored); the tiles are added in order.
+          if (tc_gemm_enabled()) {
+            const int nt = gemm_f32_tc_tri_b_rownorm(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs,
+                                                     Rf.as<float>(), 1, d, T.as<double>());
+            sum_tiles_kernel<<<grid_for(ctx, rows, 256), 256, 0, ctx->stream>>>(rows, nt, T.as<double>(),
+                                                                              sc.as<double>() + r0);
+            RNLA_CUDA(cudaGetLastError());
+            note_launch(ctx);
+          } else {
             gemm<float>(ctx, rows, d, d, 1.f, M.as<float>() + r0 * M.rs, M.rs, M.cs, Rf.as<float>(), 1, d, 0.f,
                         T.as<float>(), d, 1);
-          row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
+            row_sqnorms<float>(ctx, rows, d, T.as<float>(), d, 1, sc.as<double>() + r0);
+          }
         }
         if (stream_draw) {
           RNLA_CUDA(cudaMemcpyAsync(hs + r0, sc.as<double>() + r0, sizeof(double) * rows, cudaMemcpyDeviceToHost,

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
                        int64_t a_cs, const uint8_t* __restrict__ bimg, int64_t nkb_total, double alpha,
                        double beta, typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
                        typename std::conditional<DF, double, float>::type* ws, int sym,
-                       const __grid_constant__ CUtensorMap amap) {
+                       const __grid_constant__ CUtensorMap amap, double* rownorm) {
   using OutT = typename std::conditional<DF, double, float>::type;
   // symmetric products (C = A'A): tiles strictly below the diagonal are skipped
   // (uniformly for the whole CTA, before any barrier) and mirrored afterwards
@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
       mbar_wait(smem_u32(&bars[2 * STAGES + (last & 1)]), (uint32_t)((last / 2) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n");
     }
+    double rsq = 0.0;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
       uint32_t v[16], y[16], yl[16];
@@ -628,7 +629,14 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = OutT(0);  // empty K range: the sum is zero
       }
-      if (row < M) {
+      if (rownorm) {  // row-norm mode: sum of squares of this tile's columns, C not written
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (n0 + c0 + j < N) {
+            const double v = alpha * (double)acc[j];
+            rsq += v * v;
+          }
+      } else if (row < M) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int64_t col = n0 + c0 + j;
@@ -643,6 +651,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         }
       }
     }
+    if (rownorm && row < M) rownorm[(int64_t)blockIdx.y * M + row] = rsq;  // [N tile][row]
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
@@ -656,7 +665,8 @@ template <bool A_KC, int BN, int STAGES, bool DF, bool TMA_A>
 void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
                typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-               typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap) {
+               typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap,
+               double* rownorm) {
   constexpr int NS = DF ? 3 : 2;
   constexpr size_t STAGE = NS * (TC_BM * ROWB + BN * ROWB);
   const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
@@ -672,7 +682,7 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
   CUtensorMap dummy{};
   kern<<<grid, TMA_A ? TC_THREADS + 32 : TC_THREADS, smem, ctx->stream>>>(
       m, n, k, kchunk, A, a_rs, a_cs, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs, ws, sym,
-      amap ? *amap : dummy);
+      amap ? *amap : dummy, rownorm);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
@@ -681,7 +691,8 @@ template <bool A_KC, bool DF>
 void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                  int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
                  typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-                 typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap) {
+                 typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap,
+                 double* rownorm) {
   // as many stages as fit in ~220 KB of shared memory (at most TC_STAGES_MAX)
 #define RNLA_ST(BNV) \
   std::min(TC_STAGES_MAX, (220 * 1024) / ((DF ? 3 : 2) * (TC_BM * ROWB + (BNV) * ROWB)))
@@ -689,10 +700,11 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
   do {                                                                                                         \
     if (amap)                                                                                                  \
       launch_tc<A_KC, BNV, RNLA_ST(BNV), DF, true>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs, b_cs, \
-                                                   alpha, beta, C, c_rs, c_cs, ws, sym, amap);                 \
+                                                   alpha, beta, C, c_rs, c_cs, ws, sym, amap, rownorm);        \
     else                                                                                                       \
       launch_tc<A_KC, BNV, RNLA_ST(BNV), DF, false>(ctx, m, n, k, kchunk, splits, A, a_rs, a_cs, B, b_rs,      \
-                                                    b_cs, alpha, beta, C, c_rs, c_cs, ws, sym, nullptr);       \
+                                                    b_cs, alpha, beta, C, c_rs, c_cs, ws, sym, nullptr,        \
+                                                    rownorm);                                                  \
   } while (0)
   if (bn <= 32) RNLA_TC(32);
   else if (bn <= 64) RNLA_TC(64);
@@ -775,7 +787,7 @@ template <bool DF>
 void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                   int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta,
                   typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-                  bool tri_b = false) {
+                  bool tri_b = false, double* rownorm = nullptr) {
   using OutT = typename std::conditional<DF, double, float>::type;
   if (m == 0 || n == 0) return;
   // one N tile up to 160 columns (3 fp32 accumulators fit TMEM; 128 with the
@@ -820,7 +832,7 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
       if (eff >= 0.97) break;
     }
   }
-  if (tri_b) splits = 1;  // every CTA's clipped k range then starts at 0
+  if (tri_b || rownorm) splits = 1;  // clipped k ranges start at 0; row norms need whole sums
   int64_t kchunk = ((k + splits - 1) / splits + TC_BK - 1) / TC_BK * TC_BK;
   if (k == 0) kchunk = TC_BK;
   splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
@@ -835,17 +847,17 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   const bool tma = make_a_map(&amap, A, m, k, a_rs, a_cs);
   if (a_cs == 1)
     dispatch_bn<true, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
-                          c_rs, c_cs, ws, flags, tma ? &amap : nullptr);
+                          c_rs, c_cs, ws, flags, tma ? &amap : nullptr, rownorm);
   else
     dispatch_bn<false, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
-                           c_rs, c_cs, ws, flags, tma ? &amap : nullptr);
+                           c_rs, c_cs, ws, flags, tma ? &amap : nullptr, rownorm);
   if (splits > 1) {
     splitk_reduce_tc<OutT><<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, n, (int)splits, ws, alpha, beta, C,
                                                                                c_rs, c_cs);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
   }
-  if (sym) {
+  if (sym && !rownorm) {
     mirror_skipped_tiles<OutT><<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, TC_BM, bn_eff, C, c_rs, c_cs);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
@@ -884,6 +896,17 @@ void gemm_f32_tc_tri_b(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alp
                        int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
                        int64_t c_cs) {
   gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs, true);
+}
+
+// Row norms of C = A B with B upper triangular, C never stored:
+// rownorm[t * m + i] = sum over the columns of N tile t of (alpha C(i, j))^2,
+// t < ntiles (returned). The caller adds the tiles in order.
+int gemm_f32_tc_tri_b_rownorm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
+                              int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double* rownorm) {
+  gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, 0.f, nullptr, 0, 0, true, rownorm);
+  const int bn = n <= 160 ? (int)(((n + 15) / 16) * 16) : 128;
+  const int bn_eff = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 96 ? 96 : bn <= 128 ? 128 : 160;
+  return (int)((n + bn_eff - 1) / bn_eff);
 }
 
 // Same with double-float accumulation across 256-row chunks and fp64 output.

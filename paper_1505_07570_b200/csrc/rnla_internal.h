@@ -189,6 +189,10 @@ bool tc_gemm_enabled();
 void gemm_f32_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
                  int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
                  int64_t c_cs);
+// Row sums of squares of C = alpha A B (B upper triangular) per N tile, C not
+// stored: rownorm[t * m + i], t < the returned tile count (gemm_tc.cu).
+int gemm_f32_tc_tri_b_rownorm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
+                              int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double* rownorm);
 // gemm_f32_tc with B upper triangular (zero blocks below the diagonal skipped).
 void gemm_f32_tc_tri_b(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t a_rs,
                        int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, float beta, float* C, int64_t c_rs,
