@@ -467,6 +467,9 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
       if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
       mbar_wait(smem_u32(&tfull[st]), (uint32_t)((kb / STAGES) & 1));
       convert_tile_inplace<A_KC, NS>(smem + st * STAGE, gtid, grp);
+      // Gram with B = A' (sym bit 3, BN == TC_BM): the B tile is the A operand's
+      // tile at column block n0, landed by TMA and split the same way.
+      if (BN == TC_BM && (sym & 8)) convert_tile_inplace<A_KC, NS>(smem + st * STAGE + NS * A_TILE, gtid, grp);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive(smem_u32(&bars[st]));
     }
@@ -480,7 +483,8 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
         uint8_t* base = smem + st * STAGE;
         const uint32_t bar = smem_u32(&tfull[st]);
-        mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 + NS * B_TILE));
+        const bool b_from_a = BN == TC_BM && (sym & 8);
+        mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 + (b_from_a ? TC_BM * TC_BK * 4 : NS * B_TILE)));
         const int k0 = (int)(kbeg + (int64_t)kb * TC_BK);
         if (A_KC) {  // one 128-row x 32-fp32 SWIZZLE_128B box per 32 k
 #pragma unroll
@@ -489,7 +493,17 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         } else {
           tma_load_2d_g2s(smem_u32(base), &amap, (int)m0, k0, bar);
         }
-        bulk_copy_g2s(smem_u32(base + NS * A_TILE), bsrc + (int64_t)kb * (NS * B_TILE), NS * B_TILE, bar);
+        if (b_from_a) {
+          if (A_KC) {
+#pragma unroll
+            for (int b = 0; b < TC_BK / 32; ++b)
+              tma_load_2d_g2s(smem_u32(base + NS * A_TILE + b * TC_BM * 128), &amap, k0 + 32 * b, (int)n0, bar);
+          } else {
+            tma_load_2d_g2s(smem_u32(base + NS * A_TILE), &amap, (int)n0, k0, bar);
+          }
+        } else {
+          bulk_copy_g2s(smem_u32(base + NS * A_TILE), bsrc + (int64_t)kb * (NS * B_TILE), NS * B_TILE, bar);
+        }
       }
     }
     __syncwarp();
@@ -670,11 +684,14 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
   constexpr int NS = DF ? 3 : 2;
   constexpr size_t STAGE = NS * (TC_BM * ROWB + BN * ROWB);
   const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
-  DevBuf img(NS * (size_t)BN * ROWB * (size_t)(nkb * nblk), ctx->stream);
-  split_b_image<NS><<<grid_for(ctx, nblk * nkb * BN * QPR, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb,
-                                                                                       nblk, img.as<uint8_t>());
-  RNLA_CUDA(cudaGetLastError());
-  note_launch(ctx);
+  DevBuf img;
+  if (!(sym & 8)) {  // B pre-split into bf16 images (a Gram with B = A' splits its B tiles in the kernel)
+    img = DevBuf(NS * (size_t)BN * ROWB * (size_t)(nkb * nblk), ctx->stream);
+    split_b_image<NS><<<grid_for(ctx, nblk * nkb * BN * QPR, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN,
+                                                                                         nkb, nblk, img.as<uint8_t>());
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+  }
   const size_t smem = STAGES * STAGE + 1024 + 8 * (3 * STAGES + 5);
   auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES, DF, TMA_A>;
   ensure_dyn_smem((const void*)kern, smem);
@@ -836,7 +853,6 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   int64_t kchunk = ((k + splits - 1) / splits + TC_BK - 1) / TC_BK * TC_BK;
   if (k == 0) kchunk = TC_BK;
   splits = std::max<int64_t>(1, (k + kchunk - 1) / kchunk);
-  const int flags = sym | (tri_b && !sym ? 2 : 0);
   DevBuf wsb;
   OutT* ws = nullptr;
   if (splits > 1) {
@@ -845,6 +861,11 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   }
   CUtensorMap amap;
   const bool tma = make_a_map(&amap, A, m, k, a_rs, a_cs);
+  // Gram via the TMA path with 128-wide tiles: B tiles come from the same
+  // tensor map (RNLA_TC_B_IMAGE=1 keeps the pre-split B image).
+  static const bool b_image = std::getenv("RNLA_TC_B_IMAGE") != nullptr;
+  const bool b_from_a = sym && tma && bn_full == TC_BM && !b_image;
+  const int flags = sym | (tri_b && !sym ? 2 : 0) | (b_from_a ? 8 : 0);
   if (a_cs == 1)
     dispatch_bn<true, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
                           c_rs, c_cs, ws, flags, tma ? &amap : nullptr, rownorm);
