@@ -35,12 +35,15 @@ namespace rnla {
 namespace {
 
 constexpr int LO = 12, ROWS = 1 << LO;  // rows per tile
-constexpr int CH = 512;                  // rows per chunk (two 256-row TMA boxes)
+#ifndef RNLA_SRHT_ACC_CH
+#define RNLA_SRHT_ACC_CH 512
+#endif
+constexpr int CH = RNLA_SRHT_ACC_CH;     // rows per chunk (256-row TMA boxes)
 constexpr int NCH = ROWS / CH;           // 8 chunks per tile
 constexpr int EPC = CH / 64;             // values per thread per chunk
-constexpr int RING = 6;                  // chunk slots (3/4 of a tile in flight)
+constexpr int RING = (96 * 1024) / (CH * 32);  // chunk slots: 96 KB (3/4 of a tile) in flight
 constexpr int SMAX = 4096;               // sampled outputs held on chip
-static_assert(NCH == 8, "chunk N belongs to tile N >> 3");
+static_assert((NCH & (NCH - 1)) == 0 && CH % 256 == 0, "power-of-two chunks per tile, whole TMA boxes");
 
 // W fp32 columns per CTA (W = 8: one 32-B sector per row, 512 threads, one CTA
 // per SM; W = 4: 16-B rows, 256 threads, two CTAs per SM).
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __gri
   // up to RING chunks for phase 2 and the gather. Its counter lives in smem.
   auto issue = [&](int N) {
     const int slot = N % RING;
-    const int qti = qt0 + (N >> 3), kk = N & (NCH - 1);
+    const int qti = qt0 + N / NCH, kk = N & (NCH - 1);
     const int q = qti >> a.jh_log, jh = qti & (jhn - 1);
     mbar_expect(su32(&bars[slot]), CH * W * 4);
 #pragma unroll
