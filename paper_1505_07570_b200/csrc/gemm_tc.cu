@@ -400,7 +400,10 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   // (uniformly for the whole CTA, before any barrier) and mirrored afterwards
   // (sym bit 0). Bit 1: B is upper triangular (B(p, j) = 0 for p > j, the
   // leverage-score product M R^-1), so this N tile needs k < n0 + BN only.
-  if ((sym & 1) && (int64_t)blockIdx.x * TC_BM >= ((int64_t)blockIdx.y + 1) * BN) return;
+  // Bit 4: the grid is (N tiles, M tiles), so the N tiles of one M tile run
+  // together and share its A rows through L2.
+  const int64_t mblk = (sym & 16) ? blockIdx.y : blockIdx.x, nblk_i = (sym & 16) ? blockIdx.x : blockIdx.y;
+  if ((sym & 1) && mblk * TC_BM >= (nblk_i + 1) * BN) return;
   constexpr int PKB = DF ? 256 / TC_BK : TC_PROMOTE_KB;
   // DF also splits three ways (BF16x6: hh, hm, mh, hl, lh, mm ~ fp32-faithful
   // products, 1.9e-7 rel-F per SURVEY §7 hard part 5); otherwise BF16x3.
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * TC_BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t m0 = mblk * TC_BM, n0 = nblk_i * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = (sym & 2) ? min(min(K, kbeg + kchunk), n0 + BN) : min(K, kbeg + kchunk);
   const int nkb = (int)((kend - kbeg + TC_BK - 1) / TC_BK);
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
     // ---------------- TMA issuer: A boxes + the B image of each stage ----------------
     if (lane == 0) {
       const int64_t kb0 = kbeg / TC_BK;
-      const uint8_t* bsrc = bimg + ((int64_t)blockIdx.y * nkb_total + kb0) * (int64_t)(NS * B_TILE);
+      const uint8_t* bsrc = bimg + (nblk_i * nkb_total + kb0) * (int64_t)(NS * B_TILE);
       for (int kb = 0; kb < nkb; ++kb) {
         const int st = kb % STAGES;
         if (kb >= STAGES) mbar_wait(smem_u32(&bars[STAGES + st]), (uint32_t)(((kb / STAGES) - 1) & 1));
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
     // so two k-blocks of A loads are in flight per SM ----------------
     const int grp = warp >> 2, gtid = tid & (TC_GROUP - 1);
     const int64_t kb0 = kbeg / TC_BK;
-    const uint8_t* bsrc = bimg + ((int64_t)blockIdx.y * nkb_total + kb0) * (int64_t)(NS * B_TILE);
+    const uint8_t* bsrc = bimg + (nblk_i * nkb_total + kb0) * (int64_t)(NS * B_TILE);
     for (int kb = grp; kb < nkb; kb += TC_NGROUPS) {
       const int st = kb % STAGES;
 #if RNLA_TC_PF > 0
@@ -665,7 +668,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         }
       }
     }
-    if (rownorm && row < M) rownorm[(int64_t)blockIdx.y * M + row] = rsq;  // [N tile][row]
+    if (rownorm && row < M) rownorm[nblk_i * M + row] = rsq;  // [N tile][row]
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
@@ -695,7 +698,11 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
   const size_t smem = STAGES * STAGE + 1024 + 8 * (3 * STAGES + 5);
   auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES, DF, TMA_A>;
   ensure_dyn_smem((const void*)kern, smem);
-  dim3 grid((unsigned)((m + TC_BM - 1) / TC_BM), (unsigned)nblk, (unsigned)splits);
+  static const bool n_major_grid_off = std::getenv("RNLA_TC_M_FAST") != nullptr;
+  const bool nfast = nblk > 1 && !n_major_grid_off && (m + TC_BM - 1) / TC_BM <= 65535;
+  if (nfast) sym |= 16;
+  dim3 grid(nfast ? (unsigned)nblk : (unsigned)((m + TC_BM - 1) / TC_BM),
+            nfast ? (unsigned)((m + TC_BM - 1) / TC_BM) : (unsigned)nblk, (unsigned)splits);
   CUtensorMap dummy{};
   kern<<<grid, TMA_A ? TC_THREADS + 32 : TC_THREADS, smem, ctx->stream>>>(
       m, n, k, kchunk, A, a_rs, a_cs, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs, ws, sym,
