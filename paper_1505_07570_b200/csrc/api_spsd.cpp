@@ -197,6 +197,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   // Otherwise the eigendecomposition route below runs.
   DevBuf Tm;  // s x kp: L = C Tm
   int64_t kp = 0;
+  bool cholesky_T = false;  // Tm = R^-1 from the Cholesky route (upper triangular)
   auto cholesky_route = [&](rnla_ctx* c) {
     DevBuf Ws(sizeof(double) * s * s, c->stream), R(sizeof(double) * s * s, c->stream),
         Ri(sizeof(double) * s * s, c->stream);
@@ -211,6 +212,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
     RNLA_CUDA(cudaStreamSynchronize(c->stream));
     Tm = std::move(Ri);
     kp = s;
+    cholesky_T = true;
     return true;
   };
   const bool try_cholesky = kk >= s && !std::getenv("RNLA_NYSTROM_EIGW");
@@ -279,8 +281,17 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   // M = T' G T (kp x kp), symmetric
   DevBuf GT(sizeof(double) * s * kp, ctx->stream), M(sizeof(double) * kp * kp, ctx->stream),
       Ms(sizeof(double) * kp * kp, ctx->stream), ev(sizeof(double) * kp, ctx->stream);
-  gemm<double>(ctx, s, kp, s, 1.0, G.as<double>(), 1, s, Tm.as<double>(), 1, s, 0.0, GT.as<double>(), 1, s);
-  gemm<double>(ctx, kp, kp, s, 1.0, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, 0.0, M.as<double>(), 1, kp);
+  // Cholesky route: T = R^-1 is upper triangular, so G T skips k > column and
+  // M = T'(G T) (symmetric) skips k > row; G is read through its symmetry as
+  // K-major. Otherwise plain GEMMs.
+  const bool tri = kp == s && cholesky_T;
+  if (!(tri && gemm_f64_structured(ctx, s, kp, s, G.as<double>(), s, 1, Tm.as<double>(), 1, s, GT.as<double>(), 1, s,
+                                   2) &&
+        gemm_f64_structured(ctx, kp, kp, s, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, M.as<double>(), 1, kp,
+                            1 | 4))) {
+    gemm<double>(ctx, s, kp, s, 1.0, G.as<double>(), 1, s, Tm.as<double>(), 1, s, 0.0, GT.as<double>(), 1, s);
+    gemm<double>(ctx, kp, kp, s, 1.0, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, 0.0, M.as<double>(), 1, kp);
+  }
   symmetrize(ctx, kp, M.as<double>(), Ms.as<double>());
   trace_mark(ctx, "nystrom_eig: M = T'GT");
   // Only the top k eigenpairs are needed: block subspace iteration (a few

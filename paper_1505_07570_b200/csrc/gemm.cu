@@ -379,12 +379,20 @@ static bool try_dmma_kk(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double a
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
   }
-  if (sym) {
+  if (sym & 1) {
     mirror_lower_tiles<<<grid_for(ctx, m * n, 256), 256, 0, ctx->stream>>>(m, C, c_rs, c_cs);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
   }
   return true;
+}
+
+bool gemm_f64_structured(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t a_rs, int64_t a_cs,
+                         const double* B, int64_t b_rs, int64_t b_cs, double* C, int64_t c_rs, int64_t c_cs,
+                         int flags) {
+  if (m == 0 || n == 0) return true;
+  if ((flags & 1) && m != n) return false;
+  return try_dmma_kk<double>(ctx, m, n, k, 1.0, A, a_rs, a_cs, B, b_rs, b_cs, 0.0, C, c_rs, c_cs, 64, flags);
 }
 
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,

@@ -102,9 +102,10 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int6
                                                      double* ws, int sym_upper) {
   constexpr int MI = 4, NI = 4, STAGES = stages<TI>();
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-  // sym_upper (C = A A', A == B): skip tiles strictly below the diagonal; the
-  // caller mirrors the lower 64 x 64 tiles afterwards.
-  if (sym_upper && n0 + BN <= m0) return;
+  // sym_upper bit 0 (symmetric C): skip tiles strictly below the diagonal; the
+  // caller mirrors the lower 64 x 64 tiles afterwards. Bit 1: B upper triangular
+  // (k < n0 + BN only); bit 2: A lower triangular (k < m0 + BM only).
+  if ((sym_upper & 1) && n0 + BN <= m0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TI* As = reinterpret_cast<TI*>(smem_raw);     // [STAGES][BM][LDS_K]
   TI* Bs = As + (size_t)STAGES * BM * LDS_K;    // [STAGES][BN][LDS_K] (K-major B) or [STAGES][BK][LDS_N]
@@ -114,7 +115,9 @@ __global__ void __launch_bounds__(NT, 2) gemm_dmma_kk(int64_t m, int64_t n, int6
   const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t = lane & 3;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  const int64_t kend = min(kdim, kbeg + kchunk);
+  int64_t kend = min(kdim, kbeg + kchunk);
+  if (sym_upper & 2) kend = min(kend, n0 + BN);
+  if (sym_upper & 4) kend = min(kend, m0 + BM);
   const int nsteps = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
   double acc[MI][NI][2];
@@ -220,7 +223,7 @@ void dmma_kk_launch(rnla_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, 
 
 int dmma_kk_tiles(int64_t m, int64_t n, int sym) {
   const int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
-  if (!sym) return (int)(tm * tn);
+  if (!(sym & 1)) return (int)(tm * tn);
   int64_t live = 0;
   for (int64_t a = 0; a < tm; ++a)
     for (int64_t b = 0; b < tn; ++b)

@@ -205,6 +205,12 @@ void gemm_f32_tc_f64acc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double a
 
 // Gram-type fp32 products with fp64-grade accumulation: tcgen05 double-float
 // when enabled, else the DMMA widening kernel below.
+// C = A B (fp64, DMMA) with structure: flags bit 0 C symmetric (upper tiles,
+// mirrored), bit 1 B upper triangular, bit 2 A lower triangular -- the zero
+// k-blocks are skipped. False when the K-major cp.async kernel does not apply.
+bool gemm_f64_structured(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t a_rs, int64_t a_cs,
+                         const double* B, int64_t b_rs, int64_t b_cs, double* C, int64_t c_rs, int64_t c_cs,
+                         int flags);
 void gemm_f32_in_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                      int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
                      int64_t c_cs);
