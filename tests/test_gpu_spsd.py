@@ -86,7 +86,7 @@ def test_nystrom_eig_gram_route_matches_oracle(ctx):
     assert np.max(np.abs(np.abs(u[:, :4]) - np.abs(uo[:, :4]))) <= 1e-6
 
 
-@pytest.mark.parametrize("n,s,k,sigma", [(3000, 200, 12, 3.0), (6000, 400, 40, 4.0)])
+@pytest.mark.parametrize("n,s,k,sigma", [(3000, 200, 12, 3.0), (6000, 400, 40, 4.0), (2500, 257, 10, 3.0)])
 def test_nystrom_eig_full_rank_route(ctx, n, s, k, sigma):
     # target_k = s with a well-conditioned W: the Cholesky route (L' = C R^-1)
     # replaces eig(W); approx_eig outputs must match the reference's eig route.
