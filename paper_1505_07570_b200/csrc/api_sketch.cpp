@@ -79,8 +79,9 @@ static constexpr int64_t kGreenChunks = 16;
 
 // One GPU, K >= 2 kOneGpuKC: chunks of kOneGpuKC, so the pipelined combined
 // sketch can multiply chunk c while the gather produces chunk c + 1 (measured
-// on config 1: 3.29 -> 3.24 ms per step with 2048, 3.34 ms with 4096).
-static constexpr int64_t kOneGpuKC = 2048;
+// on config 1 with split-K per chunk: 3.29 -> 3.24 ms per step at 2048, 3.34 ms
+// at 4096; without split-K: 3.17 ms at 2048, 3.16 ms at 1024).
+static constexpr int64_t kOneGpuKC = 1024;
 static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k) {
   if (const char* e = std::getenv("RNLA_GAUSS_KC")) return std::max<int64_t>(16, std::atoll(e));
   const int64_t w = std::max(1, ctx->world);
@@ -108,8 +109,15 @@ template <class T>
 void gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s,
                     int64_t k0, bool first, T* out, int64_t out_rs, int64_t out_cs) {
   const int64_t kc = std::min(gauss_kc_for(ctx, n), n - k0);
+  // Chunked stages run each chunk without split-K (one CTA per output tile):
+  // under the gather that interferes least (config 1: 3.24 -> 3.16 ms). The
+  // standalone and the combined stage chunk identically, so the composition
+  // stays bitwise. RNLA_GAUSS_CHUNK_SPLITS overrides the cap.
+  static const int env_splits =
+      std::getenv("RNLA_GAUSS_CHUNK_SPLITS") ? std::atoi(std::getenv("RNLA_GAUSS_CHUNK_SPLITS")) : 0;
+  const int max_splits = env_splits > 0 ? env_splits : (gauss_kc_for(ctx, n) < n ? 1 : 64);
   gemm<T>(ctx, s, L, kc, T(1), g.data.as<T>() + k0, n, 1, in + k0 * ld, ld, 1, first ? T(0) : T(1), out, out_rs,
-          out_cs);
+          out_cs, max_splits);
 }
 
 template <class T>
