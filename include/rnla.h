@@ -27,6 +27,13 @@
  *    RNLA_ENUMERIC to std::runtime_error (e.g. src/spsd.cpp:200-207).
  *    "Flagged" fallbacks are reported through an int out-parameter, as the
  *    reference's LsrSolution::flagged (regression.hpp:17).
+ *  - Ordering: every call runs on the context's own stream and returns only
+ *    when its outputs are complete (host-synchronous results). Device INPUTS
+ *    written asynchronously by the caller (another stream, e.g. torch's
+ *    current stream) must be ordered first: either synchronize that stream or
+ *    call rnla_ctx_wait_stream(ctx, stream) before the call.
+ *  - Strides must be non-negative (a zero stride is allowed only along an
+ *    extent of 1); anything else returns RNLA_EINVAL.
  *  - There is no CPU fallback: compute entry points need a CUDA device and
  *    return RNLA_ECUDA without one. Host-only helpers (seeds, hashes and the
  *    libstdc++ operator draws) run anywhere.
@@ -112,6 +119,10 @@ void rnla_group_destroy(rnla_group* group);
 rnla_status rnla_ctx_create_grouped(int device, rnla_group* group, int rank, rnla_ctx** out);
 void rnla_ctx_destroy(rnla_ctx* ctx);
 rnla_status rnla_ctx_synchronize(rnla_ctx* ctx);
+/* Make the context's stream wait for all work enqueued so far on the caller's
+ * `stream` (a cudaStream_t on the context's device; NULL = the legacy default
+ * stream) without blocking the host: event record + cudaStreamWaitEvent. */
+rnla_status rnla_ctx_wait_stream(rnla_ctx* ctx, void* stream);
 /* The context's CUDA stream (a cudaStream_t), for callers that time with events. */
 void* rnla_ctx_stream(rnla_ctx* ctx);
 /* Kernel launches issued by this context since creation (instrumentation). */

@@ -179,21 +179,41 @@ def _dtype_code(x) -> int:
 
 
 def _mat(x) -> _abi.RnlaMat:
-    """rnla_mat view of a 1-D (n x 1) or 2-D numpy array / torch tensor."""
+    """rnla_mat view of a 1-D (n x 1) or 2-D numpy array / torch tensor.
+    Strides must be positive (inputs pass through _as2d, which copies views
+    with negative or zero strides; an output with such strides is rejected)."""
     if _is_torch(x):
         if x.dim() == 1:
             rows, cols, rs, cs = x.shape[0], 1, x.stride(0), 1
         else:
             rows, cols = x.shape
             rs, cs = x.stride()
+        rs = rs if rows > 1 else max(rs, 1)
+        cs = cs if cols > 1 else max(cs, 1)
+        if rs <= 0 or cs <= 0:
+            raise ValueError("matrix view with a zero stride: pass a contiguous tensor")
         return _abi.RnlaMat(x.data_ptr(), rows, cols, rs, cs, _dtype_code(x), 1 if x.is_cuda else 0)
     a = x
     if a.ndim == 1:
-        rows, cols, rs, cs = a.shape[0], 1, a.strides[0] // a.itemsize, 1
+        rows, cols = a.shape[0], 1
+        rs, cs = a.strides[0], a.itemsize
     else:
         rows, cols = a.shape
-        rs, cs = a.strides[0] // a.itemsize, a.strides[1] // a.itemsize
-    return _abi.RnlaMat(a.ctypes.data, rows, cols, max(rs, 1) if rows > 1 else max(rs, 1), cs, _dtype_code(a), 0)
+        rs, cs = a.strides
+    if rows <= 1:
+        rs = max(rs, a.itemsize)
+    if cols <= 1:
+        cs = max(cs, a.itemsize)
+    if rs <= 0 or cs <= 0 or rs % a.itemsize or cs % a.itemsize:
+        raise ValueError("matrix view with a negative, zero or unaligned stride: pass a contiguous array")
+    return _abi.RnlaMat(a.ctypes.data, rows, cols, rs // a.itemsize, cs // a.itemsize, _dtype_code(a), 0)
+
+
+def _bad_strides(x) -> bool:
+    if _is_torch(x):
+        st, sh = x.stride(), x.shape
+        return any(t <= 0 and e > 1 for t, e in zip(st, sh))
+    return any((t <= 0 and e > 1) or t % x.itemsize for t, e in zip(x.strides, x.shape))
 
 
 def _empty_like(x, rows: int, cols: int, order: str = "F", dtype=None):
@@ -207,16 +227,30 @@ def _empty_like(x, rows: int, cols: int, order: str = "F", dtype=None):
 
 
 def _as2d(x):
+    """2-D input operand; views with negative / zero / unaligned strides (e.g.
+    a[::-1], np.flipud, broadcasts) are copied to a contiguous array first."""
     if _is_torch(x):
-        return x if x.dim() == 2 else x.reshape(-1, 1)
+        x = x if x.dim() == 2 else x.reshape(-1, 1)
+        return x.contiguous() if _bad_strides(x) else x
     x = np.asarray(x)
     if x.dtype not in (np.float32, np.float64):
         x = x.astype(np.float64)
-    return x if x.ndim == 2 else x.reshape(-1, 1)
+    x = x if x.ndim == 2 else x.reshape(-1, 1)
+    return np.ascontiguousarray(x) if _bad_strides(x) else x
 
 
 def _ctx(ctx):
-    return ctx or default_context()
+    """The context for a call, ordered after the caller's torch CUDA stream:
+    device inputs written asynchronously by torch (e.g. torch.randn on the
+    device right before the call) are complete before the library's stream
+    reads them (rnla_ctx_wait_stream; no host synchronization)."""
+    c = ctx or default_context()
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        st = torch.cuda.current_stream(c.device).cuda_stream
+        _check(_abi.lib().rnla_ctx_wait_stream(c.handle, C.c_void_p(st)))
+    return c
 
 
 # --------------------------------------------------------------------------

@@ -63,6 +63,7 @@ SIGNATURES = {
     "rnla_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "rnla_ctx_destroy": (None, [_P]),
     "rnla_ctx_synchronize": (C.c_int, [_P]),
+    "rnla_ctx_wait_stream": (C.c_int, [_P, C.c_void_p]),
     "rnla_ctx_stream": (C.c_void_p, [_P]),
     "rnla_ctx_launch_count": (C.c_int64, [_P]),
     "rnla_ctx_clear_cache": (None, [_P]),

@@ -97,6 +97,9 @@ void check_mat(const rnla_mat* m, const char* name) {
   require(m->rows >= 0 && m->cols >= 0, std::string(name) + ": negative shape");
   require(m->dtype == RNLA_F64 || m->dtype == RNLA_F32, std::string(name) + ": unknown dtype");
   require(m->data != nullptr || m->rows == 0 || m->cols == 0, std::string(name) + ": null data");
+  require(m->row_stride >= 0 && m->col_stride >= 0, std::string(name) + ": negative stride");
+  require((m->row_stride > 0 || m->rows <= 1) && (m->col_stride > 0 || m->cols <= 1),
+          std::string(name) + ": zero stride along an extent > 1");
 }
 
 static bool dense_col(const rnla_mat* m) { return m->row_stride == 1 && (m->col_stride >= m->rows || m->cols <= 1); }
@@ -262,10 +265,6 @@ static void ctx_release(rnla_ctx* ctx) {
   ctx->gauss_ops.clear();
   ctx->srht_plans.clear();
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->green) {
-    for (auto s : {ctx->green->gather[0], ctx->green->gather[1], ctx->green->gemm}) cudaStreamSynchronize(s);
-    ctx->green.reset();
-  }
   if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
@@ -273,6 +272,7 @@ static void ctx_release(rnla_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   ctx->pinned = nullptr;
   ctx->pinned_bytes = 0;
+  if (ctx->caller_ev) cudaEventDestroy(ctx->caller_ev);
   cudaStreamDestroy(ctx->copy_stream);
   cudaStreamDestroy(ctx->aux_stream);
   cudaStreamDestroy(ctx->stream);
@@ -382,6 +382,15 @@ rnla_status rnla_ctx_synchronize(rnla_ctx* ctx) {
   return guard([&] {
     enter(ctx);
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+rnla_status rnla_ctx_wait_stream(rnla_ctx* ctx, void* stream) {
+  return guard([&] {
+    enter(ctx);
+    if (!ctx->caller_ev) RNLA_CUDA(cudaEventCreateWithFlags(&ctx->caller_ev, cudaEventDisableTiming));
+    RNLA_CUDA(cudaEventRecord(ctx->caller_ev, static_cast<cudaStream_t>(stream)));
+    RNLA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->caller_ev, 0));
   });
 }
 

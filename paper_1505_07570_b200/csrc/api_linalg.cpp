@@ -234,17 +234,22 @@ struct KsvdWork {
     fix_column_signs_sharded<T>(ctx, rows, cols, Y, 1, rows, nullptr, 0, 0, 0, false);
   }
 
+  // Y is overwritten only after both passes factored cleanly: pass 0 writes
+  // Q1 to a scratch buffer and pass 1 reads it, so a breakdown in either pass
+  // leaves the original Y for the TSQR / Householder fallback.
   static bool cholqr2(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, bool sharded) {
     DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream);
-    DevBuf tmp(sizeof(T) * rows * cols, ctx->stream), Rt;
+    DevBuf tmp(sizeof(T) * rows * cols, ctx->stream), q1(sizeof(T) * rows * cols, ctx->stream), Rt;
     if constexpr (!std::is_same<T, double>::value) Rt = DevBuf(sizeof(T) * cols * cols, ctx->stream);
     bool signed_ok = false;
     for (int pass = 0; pass < 2; ++pass) {
+      const T* X = pass == 0 ? Y : q1.as<T>();
+      T* out = pass == 0 ? q1.as<T>() : tmp.as<T>();
       if constexpr (std::is_same<T, double>::value) {
-        gemm<double>(ctx, cols, cols, rows, 1.0, Y, rows, 1, Y, 1, rows, 0.0, G.as<double>(), 1, cols);
+        gemm<double>(ctx, cols, cols, rows, 1.0, X, rows, 1, X, 1, rows, 0.0, G.as<double>(), 1, cols);
       } else {
         DevBuf Gf(sizeof(float) * cols * cols, ctx->stream);
-        gemm<float>(ctx, cols, cols, rows, 1.f, Y, rows, 1, Y, 1, rows, 0.f, Gf.as<float>(), 1, cols);
+        gemm<float>(ctx, cols, cols, rows, 1.f, X, rows, 1, X, 1, rows, 0.f, Gf.as<float>(), 1, cols);
         copy2d_cast<float, double>(ctx, cols, cols, Gf.as<float>(), 1, cols, G.as<double>(), 1, cols);
       }
       if (sharded) allreduce_sum(ctx, G.p, (size_t)(cols * cols), RNLA_F64);
@@ -252,16 +257,15 @@ struct KsvdWork {
       if (!diag_ratio_ok(ctx, cols, G.as<double>(), std::is_same<T, double>::value ? 1e-5 : 1e-2)) return false;
       upper_inverse(ctx, cols, G.as<double>(), Rinv.as<double>());
       // sign rule folded into the last R^-1: no extra pass over Q
-      if (pass == 1 && !sharded) signed_ok = presign_upper_inverse<T>(ctx, cols, Y, rows, Rinv.as<double>());
+      if (pass == 1 && !sharded) signed_ok = presign_upper_inverse<T>(ctx, cols, X, rows, Rinv.as<double>());
       if constexpr (std::is_same<T, double>::value) {
-        gemm<double>(ctx, rows, cols, cols, 1.0, Y, 1, rows, Rinv.as<double>(), 1, cols, 0.0, tmp.as<double>(), 1,
-                     rows);
+        gemm<double>(ctx, rows, cols, cols, 1.0, X, 1, rows, Rinv.as<double>(), 1, cols, 0.0, out, 1, rows);
       } else {
         copy2d_cast<double, float>(ctx, cols, cols, Rinv.as<double>(), 1, cols, Rt.as<float>(), 1, cols);
-        gemm<float>(ctx, rows, cols, cols, 1.f, Y, 1, rows, Rt.as<float>(), 1, cols, 0.f, tmp.as<float>(), 1, rows);
+        gemm<float>(ctx, rows, cols, cols, 1.f, X, 1, rows, Rt.as<float>(), 1, cols, 0.f, out, 1, rows);
       }
-      RNLA_CUDA(cudaMemcpyAsync(Y, tmp.p, sizeof(T) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
     }
+    RNLA_CUDA(cudaMemcpyAsync(Y, tmp.p, sizeof(T) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
     if (sharded)
       fix_column_signs_sharded<T>(ctx, rows, cols, Y, 1, rows, nullptr, 0, 0, 0, false);
     else if (!signed_ok)

@@ -70,13 +70,6 @@ std::shared_ptr<SrhtPlan> srht_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_
 // Gaussian stage under the count sketch does not overlap, the gather kernel
 // holds the register file), s / world on a row-sharded job so each rank
 // multiplies the chunks it owns after a per-chunk ncclReduce.
-// SM count for the GEMM side of a green-context split on one GPU (RNLA_GREEN_SMS, 0 = off).
-static int green_gemm_sms() {
-  static const int v = std::getenv("RNLA_GREEN_SMS") ? std::atoi(std::getenv("RNLA_GREEN_SMS")) : 0;
-  return v;
-}
-static constexpr int64_t kGreenChunks = 16;
-
 // One GPU, K >= 2 kOneGpuKC: chunks of kOneGpuKC, so the pipelined combined
 // sketch can multiply chunk c while the gather produces chunk c + 1 (measured
 // on config 1 with split-K per chunk: 3.29 -> 3.24 ms per step at 2048, 3.34 ms
@@ -85,19 +78,10 @@ static constexpr int64_t kOneGpuKC = 1024;
 static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k) {
   if (const char* e = std::getenv("RNLA_GAUSS_KC")) return std::max<int64_t>(16, std::atoll(e));
   const int64_t w = std::max(1, ctx->world);
-  if (w == 1 && green_gemm_sms() > 0) return std::max<int64_t>(16, (k + kGreenChunks - 1) / kGreenChunks);
   if (w == 1 && k >= 2 * kOneGpuKC) return kOneGpuKC;
   return std::max<int64_t>(16, (k + w - 1) / w);
 }
 
-static rnla::GreenSplit* green_for(rnla_ctx* ctx) {
-  if (ctx->world != 1 || green_gemm_sms() <= 0) return nullptr;
-  if (!ctx->green_tried) {
-    ctx->green_tried = true;
-    ctx->green = make_green_split(ctx->device, green_gemm_sms());
-  }
-  return ctx->green.get();
-}
 // Row pitch (elements) rounded up to 16 bytes.
 template <class T>
 static int64_t aligned_ld(int64_t L) {
@@ -169,25 +153,8 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
   for (auto& e : ev) RNLA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cudaEvent_t start = ev[(size_t)chunks], done = ev[(size_t)chunks + 1];
   RNLA_CUDA(cudaEventRecord(start, ctx->stream));
-  // One GPU with a green-context split: gather chunks on the gather SMs, the
-  // first n_b GEMM chunks on the GEMM SMs under the gather, the rest on the
-  // whole GPU once the gather is done (same chunk order -> same bits).
-  rnla::GreenSplit* green = green_for(ctx);
-  int64_t n_b = chunks;
   cudaStream_t gemm_st = ctx->aux_stream;
   cudaStream_t gather_st[2] = {ctx->stream, ctx->copy_stream};
-  if (green) {
-    gather_st[0] = green->gather[0];
-    gather_st[1] = green->gather[1];
-    gemm_st = green->gemm;
-    // chunks the GEMM SMs finish while the gather runs: gather time ~ bytes / HBM,
-    // GEMM time ~ flops / DMMA rate scaled by the SM share
-    const double ts = (double)n * (double)Lo * sizeof(T) / 6.4e12;
-    const double tg = 2.0 * (double)s * (double)s2 * (double)Lo / (sizeof(T) == 8 ? 25e12 : 400e12);
-    const double f = (double)green->gemm_sms / (double)(green->gemm_sms + green->gather_sms);
-    n_b = std::max<int64_t>(0, std::min<int64_t>(chunks, (int64_t)((double)chunks * f * ts / std::max(tg, 1e-12))));
-    if (const char* e = std::getenv("RNLA_GREEN_CHUNKS_B")) n_b = std::min<int64_t>(chunks, std::atoll(e));
-  }
   RNLA_CUDA(cudaStreamWaitEvent(gemm_st, start, 0));
   RNLA_CUDA(cudaStreamWaitEvent(gather_st[0], start, 0));
   RNLA_CUDA(cudaStreamWaitEvent(gather_st[1], start, 0));
@@ -206,13 +173,6 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
     }
     for (int64_t c = 0; c < chunks; ++c) {
       const int64_t b0 = c * KC, b1 = std::min(s, b0 + KC);
-      if (green && c == n_b) {
-        // hand the remaining chunks to the whole GPU after the gather and the GEMM SMs' last chunk
-        RNLA_CUDA(cudaEventRecord(done, gemm_st));
-        RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, done, 0));
-        for (int64_t q = 0; q < chunks; ++q) RNLA_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ev[(size_t)q], 0));
-        gemm_st = ctx->aux_stream;
-      }
       RNLA_CUDA(cudaStreamWaitEvent(gemm_st, ev[(size_t)c], 0));
       StreamScope on_aux(ctx, gemm_st);
       const int owner = (int)(c % ctx->world);
@@ -275,10 +235,9 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
   const int64_t Lo = L + (extra ? 1 : 0);
   const int kind = spec->kind;
   const bool sharded = ctx->world > 1;
-  static const bool force_pipeline = std::getenv("RNLA_PIPELINE") != nullptr;  // tuning knob
   const bool chunked = spec->kind == RNLA_SKETCH_COMBINED && gauss_kc_for(ctx, spec->s) < spec->s;
   if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN &&
-      (sharded || force_pipeline || chunked || green_gemm_sms() > 0)) {
+      (sharded || chunked)) {
     combined_gaussian_pipelined<T>(ctx, M, ld, extra, xs, n, L, spec, row_offset, out, o_rs, o_cs);
     return;
   }
@@ -539,7 +498,29 @@ namespace rnla {
 // (full rank) or pinv(R) Q' b with the 1e-12 pseudo_inverse cut (flagged).
 static void solve_sketched(rnla_ctx* ctx, int64_t s, int64_t d, double* a_sk, const double* b_sk, double* x_dev,
                            int32_t* flagged) {
-  require(s >= d, "lsr_sketched: s < d");
+  if (s < d) {
+    // The final sketch has fewer rows than d (a combined spec with stage2.s < d
+    // passes the reference's spec.s >= d check, src/regression.cpp:73): rank <= s < d,
+    // so the reference takes its flagged pinv(a_sk) b_sk route (:84-89).
+    *flagged = 1;
+    DevBuf u(sizeof(double) * s * s, ctx->stream), v(sizeof(double) * d * s, ctx->stream),
+        sv(sizeof(double) * std::max<int64_t>(s, 1), ctx->stream), w(sizeof(double) * std::max<int64_t>(s, 1), ctx->stream);
+    if (s == 0) {
+      RNLA_CUDA(cudaMemsetAsync(x_dev, 0, sizeof(double) * d, ctx->stream));
+      return;
+    }
+    svd_thin(ctx, s, d, a_sk, 1, s, u.as<double>(), sv.as<double>(), v.as<double>());  // a_sk = U S V'
+    gemm<double>(ctx, s, 1, s, 1.0, u.as<double>(), s, 1, b_sk, 1, 1, 0.0, w.as<double>(), 1, 1);  // U' b
+    std::vector<double> hs(s), hw(s);
+    RNLA_CUDA(cudaMemcpyAsync(hs.data(), sv.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaMemcpyAsync(hw.data(), w.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < s; ++i) hw[i] = hs[i] > 1e-12 * hs[0] ? hw[i] / hs[i] : 0.0;
+    RNLA_CUDA(cudaMemcpyAsync(w.p, hw.data(), sizeof(double) * s, cudaMemcpyHostToDevice, ctx->stream));
+    gemm<double>(ctx, d, 1, s, 1.0, v.as<double>(), 1, d, w.as<double>(), 1, 1, 0.0, x_dev, 1, 1);  // V (S^-1 U' b)
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   DevBuf r(sizeof(double) * d * d, ctx->stream);
   qr_householder(ctx, s, d, a_sk, r.as<double>(), 1, d);  // a_sk <- Q (s x d), r col-major
   DevBuf qtb(sizeof(double) * d, ctx->stream);

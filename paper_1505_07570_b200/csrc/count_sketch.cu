@@ -119,14 +119,7 @@ void launch_gather(rnla_ctx* ctx, const T* in, int64_t ld, const T* extra, int64
   constexpr int kTeams = 128 / TEAM;
   if (b1 <= b0) return;
   dim3 grid((unsigned)((b1 - b0 + kTeams - 1) / kTeams), (unsigned)((Lo + TEAM * CPT - 1) / (TEAM * CPT)));
-  // Optional dynamic-smem reservation caps gather CTAs per SM so a concurrent
-  // kernel (the pipelined Gaussian stage) can co-reside (tuning knob).
-  static const size_t pad = [] {
-    const char* e = std::getenv("RNLA_CS_SMEM_KB");
-    return e ? (size_t)std::atoi(e) * 1024 : (size_t)0;
-  }();
-  if (pad) ensure_dyn_smem((const void*)cs_gather_kernel<T, TEAM, CPT, U>, pad);
-  cs_gather_kernel<T, TEAM, CPT, U><<<grid, 128, pad, ctx->stream>>>(
+  cs_gather_kernel<T, TEAM, CPT, U><<<grid, 128, 0, ctx->stream>>>(
       in, ld, extra, xs, L, Lo, plan.offsets.as<uint32_t>(), plan.rows.as<uint32_t>(), b0, b1, out, ldo, acc ? 1 : 0);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);

@@ -553,10 +553,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
           const uint32_t base = smem_u32(smem + st * STAGE);
           const uint32_t a0 = base, b0 = base + NS * A_TILE;
           // products (i, j) of pieces: (0,0) (0,1) (1,0) [+ (0,2) (2,0) (1,1) for NS = 3]
-#ifndef RNLA_TC_NPMAX
-#define RNLA_TC_NPMAX 6
-#endif
-          constexpr int NP = (NS == 3 ? 6 : 3) < RNLA_TC_NPMAX ? (NS == 3 ? 6 : 3) : RNLA_TC_NPMAX;  // NPMAX: timing experiments only
+          constexpr int NP = NS == 3 ? 6 : 3;
           constexpr int PI[6] = {0, 0, 1, 0, 2, 1}, PJ[6] = {0, 1, 0, 2, 0, 1};
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
@@ -890,18 +887,7 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
   }
-  if (std::getenv("RNLA_TC_DEBUG")) {  // debugging aid: report non-finite outputs per call
-    const int64_t span = (m - 1) * c_rs + (n - 1) * c_cs + 1;
-    std::vector<OutT> h((size_t)span);
-    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
-    RNLA_CUDA(cudaMemcpy(h.data(), C, sizeof(OutT) * span, cudaMemcpyDeviceToHost));
-    int64_t bad = 0;
-    for (int64_t i = 0; i < m; ++i)
-      for (int64_t j = 0; j < n; ++j) bad += !std::isfinite((double)h[(size_t)(i * c_rs + j * c_cs)]);
-    std::fprintf(stderr, "tc gemm m=%lld n=%lld k=%lld a_rs=%lld a_cs=%lld tma=%d splits=%lld sym=%d nonfinite=%lld\n",
-                 (long long)m, (long long)n, (long long)k, (long long)a_rs, (long long)a_cs, (int)tma,
-                 (long long)splits, sym, (long long)bad);
-  }
+
 }
 
 }  // namespace

@@ -90,16 +90,6 @@ struct DenseOperator {  // G / sqrt(s) as the reference forms it, device fp64/fp
   int dtype = RNLA_F64;
 };
 
-// SM-partitioned streams from two CUDA green contexts (green.cpp).
-struct GreenSplit {
-  void* ctx_gather = nullptr;  // CUgreenCtx
-  void* ctx_gemm = nullptr;
-  cudaStream_t gather[2] = {nullptr, nullptr};
-  cudaStream_t gemm = nullptr;
-  int gather_sms = 0, gemm_sms = 0;
-  ~GreenSplit();
-};
-std::unique_ptr<GreenSplit> make_green_split(int device, int gemm_sms);
 
 }  // namespace rnla
 
@@ -108,7 +98,8 @@ struct rnla_ctx {
   int world = 1, rank = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
-  cudaStream_t aux_stream = nullptr;  // concurrent compute (e.g. Gaussian stage under the count sketch)
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t caller_ev = nullptr;  // rnla_ctx_wait_stream  // concurrent compute (e.g. Gaussian stage under the count sketch)
   void* nccl = nullptr;      // ncclComm_t
   rnla_group* group = nullptr;  // in-process host-staged group (dist.cpp), else NCCL
   void* cusolver = nullptr;  // cusolverDnHandle_t
@@ -119,8 +110,6 @@ struct rnla_ctx {
   std::map<std::tuple<int64_t, int64_t, int64_t, uint64_t>, std::unique_ptr<rnla::CountSketchPlan>> cs_plans;
   std::map<std::tuple<int64_t, int64_t, uint64_t, int>, std::unique_ptr<rnla::DenseOperator>> gauss_ops;
   std::map<std::tuple<int64_t, int64_t, uint64_t>, std::shared_ptr<rnla::SrhtPlan>> srht_plans;
-  std::unique_ptr<rnla::GreenSplit> green;  // lazily created (combined sketch pipelining)
-  bool green_tried = false;
   // Helper context on the same device (own high-priority stream and library
   // handles) for independent work run from a second host thread, e.g. eig(W)
   // under the Nystrom C'C Gram; created lazily by side_ctx().

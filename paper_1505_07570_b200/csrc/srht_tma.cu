@@ -222,58 +222,6 @@ __global__ void __launch_bounds__((1 << LOGR) / 2, LOGR == 10 ? 3 : 6) fwht_tma_
                       out_cs);
 }
 
-// Persistent, double-buffered form: each CTA walks tasks blockIdx.x, +gridDim.x, ...
-// (task = x + gx * y; LO: x = column tile, y = row block; HI: x = il, y = tile) and
-// lands the NEXT task's tile by TMA while it transforms the current one.
-template <int LOGR, bool HI>
-__global__ void __launch_bounds__((1 << LOGR) / 2, 1) fwht_tma_persist(
-    const __grid_constant__ CUtensorMap src_map, const __grid_constant__ CUtensorMap dst_map,
-    const int8_t* __restrict__ signs, int64_t n, int qlo, int64_t big_n, int64_t L, int64_t c0,
-    const int32_t* __restrict__ grp_off, const int32_t* __restrict__ grp_t, const int32_t* __restrict__ grp_hi,
-    float scale, float* __restrict__ out, int64_t out_rs, int64_t out_cs, int gx, int gy) {
-  constexpr int R = 1 << LOGR;
-  extern __shared__ __align__(128) float smem[];  // two [R][TW] tile buffers
-  __shared__ __align__(8) uint64_t bars[2];
-  const int tasks = gx * gy;
-  auto live = [&](int task) {
-    if (!HI) return true;
-    const int il = task % gx;
-    return grp_off[il] != grp_off[il + 1];
-  };
-  auto next_live = [&](int task) {
-    while (task < tasks && !live(task)) task += gridDim.x;
-    return task;
-  };
-  if (threadIdx.x == 0) {
-    mbar_init1(su32(&bars[0]));
-    mbar_init1(su32(&bars[1]));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int task, int b) {
-    const int x = task % gx, y = task / gx;
-    const int bx = HI ? x : y, tile = HI ? y : x;
-    fwht_issue<LOGR, HI>(smem + b * R * TW, &bars[b], &src_map, bx, tile, qlo, big_n, c0);
-  };
-  int cur = next_live((int)blockIdx.x);
-  if (cur < tasks && threadIdx.x == 0) issue(cur, 0);
-  uint32_t phase = 0;  // bit b: parity of the next completion of bars[b]
-  int b = 0;
-  while (cur < tasks) {
-    const int nxt = next_live(cur + (int)gridDim.x);
-    if (nxt < tasks && threadIdx.x == 0) issue(nxt, b ^ 1);  // buffer b^1 was released at the end of the last task
-    mbar_wait_parity(su32(&bars[b]), (phase >> b) & 1u);
-    phase ^= 1u << b;
-    const int x = cur % gx, y = cur / gx;
-    const int bx = HI ? x : y, tile = HI ? y : x;
-    const int g0 = HI ? grp_off[bx] : 0, g1 = HI ? grp_off[bx + 1] : 0;
-    fwht_tile<LOGR, HI>(smem + b * R * TW, bx, tile, g0, g1, &dst_map, signs, n, big_n, L, c0, grp_t, grp_hi, scale,
-                        out, out_rs, out_cs);
-    cur = nxt;
-    b ^= 1;
-  }
-}
-
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -317,31 +265,12 @@ template <int LOGR, bool HI>
 void launch_pass(rnla_ctx* ctx, dim3 grid, const CUtensorMap& src, const CUtensorMap& dst, const SrhtPlan& plan,
                  int64_t L, int64_t c0, float scale, float* out, int64_t out_rs, int64_t out_cs) {
   constexpr int R = 1 << LOGR;
-  // The persistent double-buffered form (RNLA_SRHT_PERSIST=1) measured slower on config 2
-  // (3.25 vs 2.60 ms): one 512-thread CTA per SM keeps fewer tiles in flight than three
-  // one-shot CTAs, so one tile per CTA stays the default.
-  static const bool one_shot = std::getenv("RNLA_SRHT_PERSIST") == nullptr;
-  if (one_shot) {
-    const size_t smem = (size_t)R * TW * sizeof(float);
-    auto k = fwht_tma_kernel<LOGR, HI>;
-    ensure_dyn_smem((const void*)k, smem);
-    k<<<grid, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
-                                          plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
-                                          plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs);
-  } else {
-    // persistent, double-buffered: two tiles per CTA, as many CTAs as fit
-    const size_t smem = 2 * (size_t)R * TW * sizeof(float);
-    auto k = fwht_tma_persist<LOGR, HI>;
-    ensure_dyn_smem((const void*)k, smem);
-    int per_sm = 1;
-    RNLA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, R / 2, smem));
-    const int64_t tasks = (int64_t)grid.x * grid.y;
-    const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(tasks, (int64_t)ctx->num_sms * std::max(1, per_sm)));
-    k<<<ctas, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
-                                          plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
-                                          plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs, (int)grid.x,
-                                          (int)grid.y);
-  }
+  const size_t smem = (size_t)R * TW * sizeof(float);
+  auto k = fwht_tma_kernel<LOGR, HI>;
+  ensure_dyn_smem((const void*)k, smem);
+  k<<<grid, R / 2, smem, ctx->stream>>>(src, dst, plan.signs.as<int8_t>(), plan.n, plan.qlo, plan.big_n, L, c0,
+                                        plan.grp_off.as<int32_t>(), plan.grp_t.as<int32_t>(),
+                                        plan.grp_hi.as<int32_t>(), scale, out, out_rs, out_cs);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }

@@ -113,3 +113,27 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(rn.CudaError):
         rn.Context(0)
+
+
+def test_operand_views_with_negative_or_zero_strides_are_copied():
+    """Inputs with negative / zero strides (a[::-1], np.flipud, broadcasts) are
+    copied to a contiguous array before their rnla_mat is built; an rnla_mat is
+    never described with a clamped stride (it would read the wrong elements)."""
+    a = np.arange(12.0).reshape(4, 3)
+    for view in (a[::-1], np.flipud(a), a[:, ::-1], np.broadcast_to(a[:1], (4, 3)), a[::2, ::-1]):
+        v2 = rn._as2d(view)
+        m = rn._mat(v2)
+        got = np.array([[np.frombuffer((np.ctypeslib.as_array(
+            (np.ctypeslib.ctypes.c_double * 1).from_address(m.data + 8 * (i * m.row_stride + j * m.col_stride))))
+        )[0] for j in range(m.cols)] for i in range(m.rows)])
+        assert np.array_equal(got, view)
+        assert m.row_stride > 0 and m.col_stride > 0
+    with pytest.raises(ValueError):
+        rn._mat(a[::-1])
+
+
+def test_wait_stream_without_gpu_fails_loudly():
+    if rn._abi.lib() is None:  # pragma: no cover
+        pytest.skip("library missing")
+    import ctypes as C
+    assert rn._abi.lib().rnla_ctx_wait_stream(None, C.c_void_p(0)) == _abi.RNLA_EINVAL
