@@ -1,31 +1,43 @@
 #!/usr/bin/env python
-"""bench.py -- headline benchmark: BASELINE config 1 sketch of [A, b].
+"""bench.py -- headline benchmark: BASELINE config 1 sketch of [A, b], plus a
+per-config block for configs 0, 2, 3 and 4.
 
 Workload (BASELINE.json configs[1]): dense fp64 A, n = 4,194,304 x d = 512,
 b = A x* + 0.01 N(0,1); CountSketch to s = 8192 rows (hash buckets / signs
 from seed) followed by the Gaussian projection 8192 -> 2048, i.e. the
 reference's combined sketch of lsr_sketched's stacked [A, b]
-(src/regression.cpp:76-79, src/sketch.cpp:108-123). Rows are sharded across
-ranks (one GPU each); the count stage is local, its 8192 x 513 partial is
-summed with NCCL allreduce inside the library, the Gaussian stage follows.
+(src/regression.cpp:76-79, src/sketch.cpp:108-123). The data is generated on
+the host (workloads.cfg1_host: fixed 65536-row blocks, identical bytes in both
+arms and for any rank count). Rows are sharded across ranks (one GPU each):
+each rank sketches its own rows (hashed by global row index), the 1024-bucket
+chunks are ncclReduce'd to an owner rank that multiplies them by its slice of
+Omega, and one allreduce of the 2048 x 513 result finishes.
 
 A "step" = one sketch_rows call over the whole (sharded) [A, b].
-  value  : GB/s of [A, b] read, whole job, inputs resident in HBM
-  e2e    : same metric through the public API with pinned HOST buffers
-           (H2D of every row + D2H of the 2048 x 513 result inside the timing)
+  value  : GB/s of [A, b] read, whole job, inputs resident in HBM (17.2 GB >> L2)
+  e2e    : same metric through the public API with pinned HOST buffers: every
+           rank copies its own rows over its own PCIe link inside the timing,
+           and the 2048 x 513 result comes back to the host
   roofline: the dominant kernel (count-sketch gather-reduce) vs measured HBM
-  cpu_baseline: the oracle's reference-faithful single-thread count sketch
-           loop + single-thread fp64 Gaussian stage on a bounded row sample.
+  cpu_baseline: the oracle's reference-faithful single-thread count-sketch
+           loop + single-thread fp64 Gaussian stage on a bounded row sample
+  per_config: configs 0, 2 (SRHT + leverage rows), 3, 4 -- device time,
+           binding roofline (burst and sustained peaks) and a CPU baseline
+           (the oracle port on the box's cores, bounded sample, extrapolated)
 
-`--impl reference` times the reference's CPU path (the oracle port: the
-reference itself cannot be built here, Eigen3 is absent) with all host
-threads, rank 0 only.
+`--gpus N` with no WORLD_SIZE in the environment relaunches itself under
+torch.distributed.run with N ranks (NCCL, 127.0.0.1). `--impl reference`
+times the reference's CPU path (the oracle port: the reference itself cannot
+be built here, Eigen3 is absent) on the FULL workload and the identical input
+bytes, with all host threads, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,55 +48,73 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_ROWS, D_COLS, S_CS, S_FINAL = 4_194_304, 512, 8192, 2048
-MASTER_SEED = 42
+import workloads as wl  # noqa: E402
 
-
-def derive_seed(seed: int, stream: int) -> int:
-    m = (1 << 64) - 1
-    s = seed ^ ((0x6A09E667F3BCC909 + stream * 0x9E3779B97F4A7C15) & m)
-    z = (s + 0x9E3779B97F4A7C15) & m
-    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
-    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
-    return z ^ (z >> 31)
-
-
-DATA_SEED = derive_seed(MASTER_SEED, 101)
-OP_SEED = derive_seed(MASTER_SEED, 201)
-STAGE2_SEED = derive_seed(OP_SEED, 1)
+N_ROWS, D_COLS, S_CS, S_FINAL = wl.CFG1["n"], wl.CFG1["d"], wl.CFG1["s_cs"], wl.CFG1["s"]
+OP_SEED = wl.op_seed(1)
+STAGE2_SEED = wl.derive_seed(OP_SEED, 1)
+METRIC = "sketch GB/s of [A,b] read (CountSketch 8192 -> Gaussian 2048)"
+DATA_DESC = "synthetic (seeded host N(0,1) A in 65536-row blocks, b = A x* + 0.01 N(0,1); identical bytes in both arms)"
 
 
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {"hbm_gbs": 6550.4, "bf16_tflops": 1671.1, "bf16_tflops_sustained": 1408.3, "kind": "fallback"}
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained"):
+            if k in d:
+                peaks[k] = float(d[k])
+        peaks["kind"] = "measured (MEASURED_PEAKS.json)"
+    # fp64 DMMA peak: cuBLAS DGEMM 8192^3 calibrated on this pool (profiles/peaks_r01.json)
+    peaks["fp64_tflops"] = 35.48
+    return peaks
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML every 2 ms during the
+    timed region (nvidia-smi as a fallback)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+             "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
-        self.index, self.samples, self._stop = index, [], threading.Event()
+        self.index, self.sm, self.mx, self.reasons = index, [], [], set()
+        self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            self.sm.append(float(n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)))
+            self.mx.append(float(n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)))
+            r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            for name, bit in self.NAMES.items():
+                if r & bit:
+                    self.reasons.add(name)
+            return
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        a, b = [float(x) for x in out.strip().split(",")[:2]]
+        self.sm.append(a)
+        self.mx.append(b)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         self._t.start()
@@ -93,17 +123,16 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        try:
+            self._sample()  # at least one sample even for a very short region
+        except Exception:
+            pass
 
     def summary(self):
-        if not self.samples:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
-                          "Active" in s[3 + i] and "Not" not in s[3 + i]})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": max(self.mx), "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -113,65 +142,435 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_baseline_run(sample_rows: int, threads: int, reps: int = 1):
-    """Reference CPU path on a bounded sample: count sketch of [A, b] (oracle C
-    loop, sequential order) + the fp64 Gaussian stage 8192 -> 2048 (BLAS).
-    Returns (GB/s of [A, b] read for the FULL workload extrapolated from the
-    sample, seconds per sample step, description)."""
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 without a launcher: start N ranks with torch.distributed.run."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+# ------------------------------------------------------------------ CPU arms
+def cpu_count_gauss_step(a, b, g, threads):
+    """One reference-path step on host rows: count sketch of [A, b] (the
+    oracle's C restatement of src/sketch.cpp:83-92, j ascending) + the fp64
+    Gaussian stage (src/sketch.cpp:41) through BLAS. Returns (total s, count s,
+    Gaussian-stage s)."""
     from oracle import oracle as orc
     from threadpoolctl import threadpool_limits
+    t0 = time.perf_counter()
+    mid = orc.count_sketch_rows(a, S_CS, OP_SEED, extra=b, threads=threads)
+    t1 = time.perf_counter()
+    with threadpool_limits(limits=threads):
+        out = g.T @ mid
+    t2 = time.perf_counter()
+    assert out.shape == (S_FINAL, D_COLS + 1)
+    return t2 - t0, t1 - t0, t2 - t1
 
-    rng = np.random.default_rng(DATA_SEED & 0xFFFFFFFF)
-    a = rng.standard_normal((sample_rows, D_COLS))
-    xs = rng.standard_normal(D_COLS)
-    b = a @ xs + 0.01 * rng.standard_normal(sample_rows)
-    g = orc.gaussian_matrix(S_CS, S_FINAL, STAGE2_SEED) / np.sqrt(S_FINAL)  # operator draw: not timed
-    t_count, t_gauss = [], []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        mid = orc.count_sketch_rows(a, S_CS, OP_SEED, extra=b, threads=threads)
-        t1 = time.perf_counter()
-        with threadpool_limits(limits=threads):
-            out = g.T @ mid
-        t2 = time.perf_counter()
-        t_count.append(t1 - t0)
-        t_gauss.append(t2 - t1)
-        assert out.shape == (S_FINAL, D_COLS + 1)
-    tc, tg = min(t_count), min(t_gauss)
-    full_bytes = N_ROWS * (D_COLS + 1) * 8
-    full_time = tc * (N_ROWS / sample_rows) + tg
-    desc = (f"{sample_rows} of {N_ROWS} rows of [A,b] fp64 ({sample_rows * (D_COLS + 1) * 8 / 1e9:.2f} GB): "
-            f"count sketch {tc:.3f} s (oracle C loop, {threads} thread(s)) + Gaussian stage {tg:.3f} s "
-            f"(numpy/OpenBLAS, {threads} thread(s)); full-size time extrapolated linearly in rows")
-    return full_bytes / full_time / 1e9, tc + tg, desc
+
+def gaussian_operator_host():
+    from oracle import oracle as orc
+    return orc.gaussian_matrix(S_CS, S_FINAL, STAGE2_SEED) / math.sqrt(S_FINAL)
 
 
 def run_reference(args):
+    """The reference CPU path on the full config-1 workload, identical bytes."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    threads = os.cpu_count() or 1
-    sample = args.cpu_sample_rows
+    threads = wl.host_threads()
+    n = args.rows
+    t0 = time.perf_counter()
+    a, b, _ = wl.cfg1_host(n=n)
+    t_gen = time.perf_counter() - t0
+    g = gaussian_operator_host()  # operator draw: not timed (as in the GPU arm)
     for _ in range(args.warmup):
-        cpu_baseline_run(min(sample, 65536), threads)
-    vals, secs = [], []
-    desc = ""
-    for _ in range(args.steps):
-        v, s, desc = cpu_baseline_run(sample, threads)
-        vals.append(v)
-        secs.append(s)
-    value = float(np.median(vals))
+        cpu_count_gauss_step(a, b, g, threads)
+    secs = [cpu_count_gauss_step(a, b, g, threads)[0] for _ in range(args.steps)]
+    ms = float(np.median(secs)) * 1e3
+    value = n * (D_COLS + 1) * 8 / (ms * 1e-3) / 1e9
     line = {
-        "impl": "reference", "metric": "sketch GB/s of [A,b] read (CountSketch 8192 -> Gaussian 2048)",
-        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), b = A x* + 0.01 N(0,1))",
-        "config": {"workload": "cfg1: combined sketch of [A,b], n=4194304, d=512, s=8192 -> 2048", "n": N_ROWS,
-                   "d": D_COLS, "s_cs": S_CS, "s": S_FINAL},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": desc},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": DATA_DESC,
+        "config": {"workload": "cfg1: combined sketch of [A,b], n=4194304, d=512, s=8192 -> 2048", "n": n,
+                   "d": D_COLS, "s_cs": S_CS, "s": S_FINAL, "data_gen_s": round(t_gen, 2)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"full workload ({n} rows of [A,b] fp64, {n * (D_COLS + 1) * 8 / 1e9:.2f} GB) per "
+                                   f"step: oracle C count-sketch loop ({threads} threads, column ranges, per-bucket "
+                                   f"order j ascending) + numpy/OpenBLAS Gaussian stage ({threads} threads)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ per-config block (rank 0, N = 1)
+def _events_time(torch, ctx, fn, warmup, reps):
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(warmup):
+        out = fn()
+    ctx.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts)), float(np.min(ts)), out
+
+
+def _roof(bytes_, flops, peaks, tflops_key_scale):
+    """Binding roofline time (ms) with burst and sustained compute peaks."""
+    hbm = bytes_ / (peaks["hbm_gbs"] * 1e9) * 1e3 if bytes_ else 0.0
+    out = {"hbm_ms": hbm}
+    for tag, key in (("burst", "bf16_tflops"), ("sustained", "bf16_tflops_sustained")):
+        if flops:
+            peak = tflops_key_scale(peaks, key)
+            out[f"compute_ms_{tag}"] = flops / (peak * 1e12) * 1e3
+    return out
+
+
+def per_config(torch, rn, peaks, args):
+    from oracle import oracle as orc
+    from threadpoolctl import threadpool_limits
+    threads = wl.host_threads()
+    ctx = rn.Context(0)
+    res = {}
+    W, R = 2, max(3, min(10, args.steps))
+
+    def finish(name, d, t_ms, roof, binding):
+        burst = max(v for k, v in roof.items() if "sustained" not in k)
+        sust = max(v for k, v in roof.items() if "burst" not in k)
+        d.update({"ms_median": t_ms, "roofline": dict(roof, binding=binding, frac=burst / t_ms,
+                                                        frac_sustained=sust / t_ms)})
+        res[name] = d
+
+    # ---- cfg0: prototype_ksvd fp64 8192 x 2048, k = 20, s = 30, q = 1 (1 GPU per BASELINE)
+    c = wl.CFG0
+    a0 = wl.cfg0_host()
+    A0 = torch.from_numpy(a0).cuda()
+    med, best, r = _events_time(torch, ctx, lambda: rn.prototype_ksvd(A0, c["k"], c["s"], wl.op_seed(0),
+                                                                      power_iters=c["q"], ctx=ctx), W, R)
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        _, so, _, _ = orc.prototype_ksvd(a0, c["k"], c["s"], wl.op_seed(0), q=c["q"])
+        tc = time.perf_counter() - t0
+    B, F = 4 * c["m"] * c["n"] * 8, 4 * 2 * c["m"] * c["n"] * c["s"]
+    roof = {"hbm_ms": B / (peaks["hbm_gbs"] * 1e9) * 1e3, "compute_ms_fp64_dmma": F / (peaks["fp64_tflops"] * 1e12) * 1e3}
+    finish("cfg0", {"workload": "prototype_ksvd fp64 8192x2048 k=20 s=30 q=1", "ms_best": best, "alg_bytes": B,
+                    "alg_flops": F, "passes": r.passes_over_a,
+                    "parity_sigma_rel_err_vs_oracle": float(np.max(np.abs(r.factors.singular_values - so) / so)),
+                    "cpu_baseline": {"value_ms": tc * 1e3, "cores": threads, "kind": "port",
+                                     "sample": "full config (oracle numpy/OpenBLAS fp64, same A and Omega)"}},
+           med, roof, "hbm~dmma")
+    del A0, r
+
+    # ---- cfg2: SRHT fp32 2^20 x 1024 -> 4096, and leverage-score rows (4096 draws)
+    c = wl.CFG2
+    A2 = wl.cfg2_device()
+    spec = rn.SketchSpec.srht(c["s"], wl.op_seed(2))
+    out2 = torch.empty(c["s"], c["d"], dtype=torch.float32, device="cuda")
+    med, best, _ = _events_time(torch, ctx, lambda: rn.sketch_rows(A2, spec, out=out2, ctx=ctx), W, R)
+    ncols = 16
+    sub = A2[:, :ncols].double().cpu().numpy()
+    t0 = time.perf_counter()
+    ref = orc.srht_rows(sub, c["s"], wl.op_seed(2), threads=min(threads, ncols))
+    tc = (time.perf_counter() - t0) * (c["d"] / ncols)
+    err = float(np.linalg.norm(out2[:, :ncols].double().cpu().numpy() - ref) / np.linalg.norm(ref))
+    B = c["n"] * c["d"] * 4 + c["s"] * c["d"] * 4
+    finish("cfg2_srht", {"workload": "SRHT fp32 2^20x1024 -> 4096 rows", "ms_best": best, "alg_bytes": B,
+                         "achieved_gbs": B / (med * 1e-3) / 1e9,
+                         "parity_rel_fro_err_first16cols": err,
+                         "cpu_baseline": {"value_ms": tc * 1e3, "cores": min(threads, ncols), "kind": "port",
+                                          "sample": f"{ncols} of {c['d']} columns at full n (oracle C sign/FWHT/"
+                                                    f"sample loop, fp64), time x {c['d'] // ncols}"}},
+           med, {"hbm_ms": B / (peaks["hbm_gbs"] * 1e9) * 1e3}, "hbm")
+    lseed = wl.derive_seed(wl.op_seed(2), 2)
+    med, best, lv = _events_time(torch, ctx, lambda: rn.leverage_sample_rows(A2, c["s"], lseed, ctx=ctx), 1,
+                                 max(3, R // 2))
+    rows = 65536
+    asub = A2[:rows].double().cpu().numpy()
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        sc = orc.row_leverage(asub)
+        orc.sample_with_replacement(sc, c["s"], lseed)
+        tc = (time.perf_counter() - t0) * (c["n"] / rows)
+    F = 2 * c["n"] * c["d"] * c["d"] * 2  # Gram + row-norm solve
+    bf3 = lambda p, k: p[k] / 3.0  # BF16x3 effective peak  # noqa: E731
+    roof = _roof(0, F, peaks, bf3)
+    finish("cfg2_leverage", {"workload": "row leverage scores (Gram + Cholesky + ||a_i R^-1||^2) + 4096 draws, fp32 "
+                                         "2^20x1024", "ms_best": best, "alg_flops": F,
+                             "scores_sum": float(lv[0].sum()), "indices": int(lv[1].size),
+                             "cpu_baseline": {"value_ms": tc * 1e3, "cores": threads, "kind": "port",
+                                              "sample": f"{rows} of {c['n']} rows (oracle thin_qr row norms + "
+                                                        f"libstdc++ draw), time x {c['n'] // rows}"}},
+           med, roof, "tensor (BF16x3)")
+    del A2, out2, lv
+    torch.cuda.empty_cache()
+
+    # ---- cfg3: prototype_ksvd fp32 262144 x 16384, k = 100, s = 150, q = 2
+    c = wl.CFG3
+    A3 = wl.cfg3_device()
+    med, best, r = _events_time(torch, ctx, lambda: rn.prototype_ksvd(A3, c["k"], c["s"], wl.op_seed(3),
+                                                                      power_iters=c["q"], ctx=ctx), 1, max(3, R // 2))
+    rows = 8192
+    asub = A3[:rows].double().cpu().numpy()
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        orc.prototype_ksvd(asub, c["k"], c["s"], wl.op_seed(3), q=c["q"])
+        tc = (time.perf_counter() - t0) * (c["m"] / rows)
+    B, F = 6 * c["m"] * c["n"] * 4, 6 * 2 * c["m"] * c["n"] * c["s"]
+    roof = _roof(B, F, peaks, bf3)
+    finish("cfg3", {"workload": "prototype_ksvd fp32 262144x16384 k=100 s=150 q=2", "ms_best": best, "alg_bytes": B,
+                    "alg_flops": F, "passes": r.passes_over_a, "sigma_top3": [float(x) for x in
+                                                                              r.factors.singular_values[:3]],
+                    "cpu_baseline": {"value_ms": tc * 1e3, "cores": threads, "kind": "port",
+                                     "sample": f"{rows} of {c['m']} rows (oracle numpy fp64, same Omega), time x "
+                                               f"{c['m'] // rows}"}},
+           med, roof, "hbm (75 flop/B vs BF16x3 ridge ~85)")
+    del A3, r
+    torch.cuda.empty_cache()
+
+    # ---- cfg4: Nystrom + top-64 eigenpairs, fp32 n = 131072, d = 64, c = 2048
+    c = wl.CFG4
+    X, sigma = wl.cfg4_device()
+    view = rn.KernelView(X, rn.KernelSpec(sigma))
+    med, best, out = _events_time(torch, ctx, lambda: rn.nystrom_eig(view, c["c"], wl.op_seed(4), c["c"], c["k"],
+                                                                     want_vectors=False, ctx=ctx), W, R)
+    pts = 8192
+    xs = X[:pts].double().cpu().numpy()
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        wl.nystrom_oracle_lambda(xs, sigma, c["c"], wl.op_seed(4), c["k"])
+        tc = (time.perf_counter() - t0) * (c["n"] / pts)
+    F = 2 * c["n"] * c["c"] * c["d"] + 2 * c["n"] * c["c"] ** 2 + 2 * c["n"] * c["c"] * c["k"]
+    roof = _roof(0, F, peaks, bf3)
+    finish("cfg4", {"workload": "Nystrom RBF n=131072 d=64 c=2048 (W+ at the reference floor) + top-64 eig, fp32",
+                    "ms_best": best, "alg_flops": F, "sigma": sigma, "kept": int(out[3]),
+                    "lambda_top3": [float(x) for x in out[1][:3]],
+                    "cpu_baseline": {"value_ms": tc * 1e3, "cores": threads, "kind": "port",
+                                     "sample": f"{pts} of {c['n']} points (oracle nystrom + approx_eig singular "
+                                               f"values, fp64), time x {c['n'] // pts} (upper bound: eig(W) is "
+                                               f"n-independent)"}},
+           med, roof, "tensor (BF16x3 equivalent)")
+    del X
+    ctx.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1505_07570_b200 as rn
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if os.environ.get("NCCL_DEBUG"):
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout to the one JSON line
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", world_size=world, rank=rank,
+                                device_id=torch.device("cuda", local))
+        idl = [rn.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idl, src=0)
+        ctx = rn.Context(local, world, rank, idl[0])
+    else:
+        ctx = rn.Context(local)
+
+    n_total = args.rows
+    r0, r1 = rn.shard_rows(n_total, world, rank)
+    n_loc = r1 - r0
+    d = D_COLS
+    # host data of this rank's rows, generated straight into pinned memory
+    t0 = time.perf_counter()
+    Ah = torch.empty(n_loc, d, dtype=torch.float64, pin_memory=True)
+    bh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    wl.cfg1_host(n=n_total, r0=r0, r1=r1, out_a=Ah.numpy(), out_b=bh.numpy(),
+                 threads=max(1, wl.host_threads() // world))
+    t_gen = time.perf_counter() - t0
+    A = Ah.to("cuda")
+    b = bh.to("cuda")
+    out = torch.empty(S_FINAL, d + 1, dtype=torch.float64, device="cuda")
+    spec = rn.SketchSpec.combined(S_CS, rn.SketchSpec.gaussian(S_FINAL, STAGE2_SEED), OP_SEED)
+    count_spec = rn.SketchSpec.count_sketch(S_CS, OP_SEED)
+    mid = torch.empty(S_CS, d + 1, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    torch.cuda.synchronize()
+
+    def step():
+        rn.sketch_rows(A, spec, extra=b, row_offset=r0, out=out, ctx=ctx)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world > 1:
+            t = torch.tensor([v], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return v
+
+    # operator builds, reported on their own (not in ms_per_step): the count-sketch
+    # plan (device hash + bucket sort, cached per (n, s, seed, row offset)) and the
+    # Gaussian operator (libstdc++ draw on the host + H2D, cached per (n, s, seed))
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    first = []
+    for i in range(4):  # fresh operator seeds: every call builds its plan (the first also warms the pool)
+        sp = rn.SketchSpec.count_sketch(S_CS, OP_SEED + 1 + i)
+        p0, p1 = ev(), ev()
+        ctx.synchronize()
+        p0.record(stream)
+        rn.sketch_rows(A, sp, extra=b, row_offset=r0, out=mid, ctx=ctx)  # plan + gather
+        p1.record(stream)
+        p1.synchronize()
+        first.append(p0.elapsed_time(p1))
+    first_count_ms = float(np.median(first[1:]))
+    ctx.clear_cache()
+    t_op = time.perf_counter()
+    step()  # + Gaussian operator draw
+    ctx.synchronize()
+    t_op = time.perf_counter() - t_op
+    for _ in range(max(args.warmup, 1)):
+        step()
+    ctx.synchronize()
+
+    # ---- timed region: K steps, device events on the library stream ----
+    barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    e0, e1 = ev(), ev()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - l0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    total_bytes = n_total * (d + 1) * 8
+    value = total_bytes / (ms * 1e-3) / 1e9
+
+    # ---- dominant kernel: count-sketch gather-reduce timed alone (count-only call) ----
+    for _ in range(2):
+        rn.sketch_rows(A, count_spec, extra=b, row_offset=r0, out=mid, ctx=ctx)
+    ctx.synchronize()
+    k0, k1 = ev(), ev()
+    kreps = max(3, args.steps)
+    k0.record(stream)
+    for _ in range(kreps):
+        rn.sketch_rows(A, count_spec, extra=b, row_offset=r0, out=mid, ctx=ctx)
+    k1.record(stream)
+    k1.synchronize()
+    k_ms = k0.elapsed_time(k1) / kreps
+    alg_bytes = n_loc * (d + 1) * 8 + S_CS * (d + 1) * 8
+    peaks = load_peaks()
+    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    plan_ms = max(0.0, first_count_ms - k_ms)
+
+    # ---- e2e through the public API with pinned host buffers (host-sharded: own rows, own PCIe link) ----
+    e2e = None
+    if not args.no_e2e:
+        outh = np.empty((S_FINAL, d + 1), dtype=np.float64)
+        rn.sketch_rows(Ah, spec, extra=bh, row_offset=r0, out=outh, ctx=ctx)  # warm
+        barrier()
+        e_steps = max(1, args.e2e_steps)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            rn.sketch_rows(Ah, spec, extra=bh, row_offset=r0, out=outh, ctx=ctx)
+        barrier()
+        es = max_over_ranks((time.perf_counter() - t0) / e_steps)
+        same = np.array_equal(outh, out.cpu().numpy())
+        e2e = {"value": total_bytes / es / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(n_total * (d + 1) * 8),
+               "d2h_bytes_per_step": int(S_FINAL * (d + 1) * 8 * world), "ms_per_step": es * 1e3,
+               "h2d_path": f"{world} rank(s), each copies its own {n_loc} rows over its own PCIe link",
+               "matches_device_result_bitwise": bool(same)}
+
+    # ---- one-GPU NCCL transport check: the same step through a world-1 NCCL context ----
+    nccl1 = None
+    if world == 1 and not args.no_nccl_check:
+        nctx = rn.Context(local, 1, 0, rn.Context.nccl_unique_id())
+        o2 = torch.empty_like(out)
+        for _ in range(2):
+            rn.sketch_rows(A, spec, extra=b, out=o2, ctx=nctx)
+        nctx.synchronize()
+        ns = torch.cuda.ExternalStream(nctx.stream)
+        n0, n1 = ev(), ev()
+        n0.record(ns)
+        for _ in range(5):
+            rn.sketch_rows(A, spec, extra=b, out=o2, ctx=nctx)
+        n1.record(ns)
+        n1.synchronize()
+        nccl1 = {"ms_per_step": n0.elapsed_time(n1) / 5,
+                 "rel_diff_vs_single_gpu_path": float(((o2 - out).norm() / out.norm()).item()),
+                 "note": "sharded code path (ncclReduce per 1024-bucket chunk + ncclAllReduce) on a 1-rank communicator"}
+        nctx.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rows = min(args.cpu_sample_rows, n_loc)
+        g = gaussian_operator_host()
+        _, tcount, tg = cpu_count_gauss_step(Ah.numpy()[:rows], bh.numpy()[:rows], g, 1)
+        full = tcount * (N_ROWS / rows) + tg
+        cpu = {"value": total_bytes / full / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": f"first {rows} of {N_ROWS} rows of the same [A,b] (fp64): oracle C count-sketch loop "
+                         f"(1 thread, j ascending) + numpy/OpenBLAS Gaussian stage (1 thread); count time "
+                         f"extrapolated linearly in rows"}
+
+    pc = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        del Ah, bh
+        del A, b
+        torch.cuda.empty_cache()
+        pc = per_config(torch, rn, peaks, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": DATA_DESC,
+            "config": {"workload": "cfg1: combined sketch of [A,b], n=4194304, d=512, s=8192 -> 2048",
+                       "n": n_total, "d": d, "s_cs": S_CS, "s": S_FINAL,
+                       "parallelism": f"rows sharded x{world}" + (" (NCCL)" if world > 1 else ""),
+                       "l2": "inputs (17.2 GB) larger than L2; no flush needed",
+                       "data_gen_s": round(t_gen, 2)},
+            "operator_build": {"count_sketch_plan_ms": plan_ms, "gaussian_operator_s": round(t_op, 3),
+                               "note": "cached per operator; excluded from ms_per_step (SURVEY §8(d))"},
+            "roofline": {"bound": "hbm", "kernel": "cs_gather_kernel (count sketch gather-reduce)",
+                         "achieved": achieved, "peak": peaks["hbm_gbs"], "peak_kind": peaks["kind"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic_from_profiles(),
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
+                         "step_roofline_frac": alg_bytes / (peaks["hbm_gbs"] * 1e9) / (ms * 1e-3),
+                         "frac_of_8TBs_nominal": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "nccl_world1": nccl1,
+            "per_config": pc,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -188,155 +587,10 @@ def ncu_traffic_from_profiles():
     return None
 
 
-def run_gpu(args):
-    import torch
-    import torch.distributed as dist
-
-    import paper_1505_07570_b200 as rn
-
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://", world_size=world, rank=rank,
-                                device_id=torch.device("cuda", local))
-        idl = [rn.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idl, src=0)
-        ctx = rn.Context(local, world, rank, idl[0])
-    else:
-        ctx = rn.Context(local)
-
-    n_total = args.rows
-    r0, r1 = rn.shard_rows(n_total, world, rank)
-    n_loc = r1 - r0
-    d = D_COLS
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed((DATA_SEED + rank) & 0x7FFFFFFFFFFFFFFF)
-    A = torch.randn(n_loc, d, dtype=torch.float64, device="cuda", generator=gen)
-    xg = torch.Generator(device="cuda")
-    xg.manual_seed(DATA_SEED & 0x7FFFFFFF)
-    xstar = torch.randn(d, dtype=torch.float64, device="cuda", generator=xg)
-    b = A @ xstar + 0.01 * torch.randn(n_loc, dtype=torch.float64, device="cuda", generator=gen)
-    out = torch.empty(S_FINAL, d + 1, dtype=torch.float64, device="cuda")
-    spec = rn.SketchSpec.combined(S_CS, rn.SketchSpec.gaussian(S_FINAL, STAGE2_SEED), OP_SEED)
-    count_spec = rn.SketchSpec.count_sketch(S_CS, OP_SEED)
-    mid = torch.empty(S_CS, d + 1, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.ExternalStream(ctx.stream)
-    torch.cuda.synchronize()
-
-    def step():
-        rn.sketch_rows(A, spec, extra=b, row_offset=r0, out=out, ctx=ctx)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # warm-up (plans + Gaussian operator are built and cached here: operator generation is not timed)
-    t_op = time.perf_counter()
-    for _ in range(max(args.warmup, 1)):
-        step()
-    ctx.synchronize()
-    t_op = time.perf_counter() - t_op
-
-    # ---- timed region: K steps, device events on the library stream ----
-    barrier()
-    torch.cuda.synchronize()
-    l0 = ctx.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        ev1.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    launches = ctx.launch_count() - l0
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_bytes = n_total * (d + 1) * 8
-    value = total_bytes / (ms * 1e-3) / 1e9
-
-    # ---- dominant kernel: count-sketch gather-reduce timed alone (count-only call) ----
-    for _ in range(2):
-        rn.sketch_rows(A, count_spec, extra=b, row_offset=r0, out=mid, ctx=ctx)
-    ctx.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kreps = max(3, args.steps)
-    k0.record(stream)
-    for _ in range(kreps):
-        rn.sketch_rows(A, count_spec, extra=b, row_offset=r0, out=mid, ctx=ctx)
-    k1.record(stream)
-    k1.synchronize()
-    k_ms = k0.elapsed_time(k1) / kreps
-    alg_bytes = n_loc * (d + 1) * 8 + S_CS * (d + 1) * 8
-    peak, peak_kind = load_peaks()
-    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
-
-    # ---- e2e through the public API with pinned host buffers ----
-    e2e = None
-    if not args.no_e2e:
-        Ah = torch.empty(n_loc, d, dtype=torch.float64).pin_memory()
-        bh = torch.empty(n_loc, dtype=torch.float64).pin_memory()
-        Ah.copy_(A)
-        bh.copy_(b)
-        outh = np.empty((S_FINAL, d + 1), dtype=np.float64)
-        rn.sketch_rows(Ah, spec, extra=bh, row_offset=r0, out=outh, ctx=ctx)  # warm
-        barrier()
-        e_steps = max(1, args.e2e_steps)
-        t0 = time.perf_counter()
-        for _ in range(e_steps):
-            rn.sketch_rows(Ah, spec, extra=bh, row_offset=r0, out=outh, ctx=ctx)
-        barrier()
-        es = (time.perf_counter() - t0) / e_steps
-        if world > 1:
-            t = torch.tensor([es], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            es = float(t.item())
-        same = np.array_equal(outh, out.cpu().numpy())
-        e2e = {"value": total_bytes / es / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(n_total * (d + 1) * 8),
-               "d2h_bytes_per_step": int(S_FINAL * (d + 1) * 8), "ms_per_step": es * 1e3,
-               "matches_device_result_bitwise": bool(same)}
-        del Ah, bh
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        v, s, desc = cpu_baseline_run(args.cpu_sample_rows, 1)
-        cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "port", "sample": desc}
-
-    if rank == 0:
-        line = {
-            "metric": "sketch GB/s of [A,b] read (CountSketch 8192 -> Gaussian 2048)",
-            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded N(0,1) A on device, b = A x* + 0.01 N(0,1))",
-            "config": {"workload": "cfg1: combined sketch of [A,b], n=4194304, d=512, s=8192 -> 2048",
-                       "n": n_total, "d": d, "s_cs": S_CS, "s": S_FINAL, "parallelism": f"rows sharded x{world}",
-                       "l2": "inputs (17.2 GB) larger than L2; no flush needed",
-                       "operator_build_s": round(t_op, 3)},
-            "roofline": {"bound": "hbm", "kernel": "cs_gather_kernel (count sketch gather-reduce)",
-                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic_from_profiles(),
-                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
-                         "frac_of_8TBs_nominal": achieved / 8000.0},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    ctx.close()
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", type=int, default=N_ROWS)
@@ -344,11 +598,15 @@ def main():
     ap.add_argument("--cpu-sample-rows", type=int, default=1 << 20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-nccl-check", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_gpu(args)
 
 

@@ -104,7 +104,9 @@ const char* rnla_last_error(void);
 rnla_status rnla_ctx_create(int device, rnla_ctx** out);
 /* Row-sharded context: rank `rank` of `world` processes, one GPU each, joined
  * through NCCL with a 128-byte ncclUniqueId produced by rnla_nccl_unique_id on
- * rank 0 and broadcast by the caller. */
+ * rank 0 and broadcast by the caller. world = 1 creates a one-rank
+ * communicator: the row-sharded code paths and their NCCL collectives run on
+ * a single GPU (results equal a plain context's to rounding). */
 rnla_status rnla_ctx_create_dist(int device, int world, int rank, const void* nccl_unique_id, rnla_ctx** out);
 rnla_status rnla_nccl_unique_id(void* out128);
 /* In-process shard group: `world` contexts driven by `world` host threads of

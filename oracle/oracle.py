@@ -64,6 +64,9 @@ def lib():
         L.orc_count_sketch_mt.restype = C.c_int
         L.orc_fwht.argtypes = [_F64P, C.c_int64]
         L.orc_srht_sketch.argtypes = [_F64P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _F64P, _I64P, _F64P]
+        L.orc_srht_sketch_mt.argtypes = [_F64P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _F64P, _I64P, _F64P,
+                                         C.c_int]
+        L.orc_srht_sketch_mt.restype = C.c_int
         L.orc_mt_next.restype = C.c_uint64
         _lib = L
     return _lib
@@ -180,20 +183,25 @@ def fwht(x: np.ndarray) -> np.ndarray:
     return y
 
 
-def srht_sketch(a: np.ndarray, s: int, seed: int) -> np.ndarray:
+def srht_sketch(a: np.ndarray, s: int, seed: int, threads: int = 1) -> np.ndarray:
     """C = A S_srht (src/sketch.cpp:57-81): segments are the columns of A."""
     a = np.asarray(a, dtype=np.float64)
     n = a.shape[1]
     signs, idx = srht_operator(n, s, seed)
     segs = np.ascontiguousarray(a.T)  # n segments of length m
     out = np.empty((s, a.shape[0]), dtype=np.float64)
-    lib().orc_srht_sketch(_p(segs), n, a.shape[0], a.shape[0], s, _p(signs), _p(idx, _I64P), _p(out))
+    if threads > 1:
+        rc = lib().orc_srht_sketch_mt(_p(segs), n, a.shape[0], a.shape[0], s, _p(signs), _p(idx, _I64P), _p(out),
+                                      threads)
+        assert rc == 0, rc
+    else:
+        lib().orc_srht_sketch(_p(segs), n, a.shape[0], a.shape[0], s, _p(signs), _p(idx, _I64P), _p(out))
     return out.T
 
 
-def srht_rows(m: np.ndarray, s: int, seed: int) -> np.ndarray:
+def srht_rows(m: np.ndarray, s: int, seed: int, threads: int = 1) -> np.ndarray:
     """S^T M for row-major tall M (rows are the segments)."""
-    return srht_sketch(np.asarray(m, dtype=np.float64).T, s, seed).T
+    return srht_sketch(np.asarray(m, dtype=np.float64).T, s, seed, threads).T
 
 
 def combined_sketch(a: np.ndarray, s_cs: int, seed: int, stage2_kind: str, s2: int, seed2: int) -> np.ndarray:

@@ -89,7 +89,7 @@ class Context:
         if group is not None:
             _check(lib.rnla_ctx_create_grouped(device, group.handle, rank, C.byref(h)))
             world = group.world
-        elif world > 1:
+        elif world > 1 or nccl_id is not None:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _check(lib.rnla_ctx_create_dist(device, world, rank, buf, C.byref(h)))
         else:

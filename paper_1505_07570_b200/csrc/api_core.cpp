@@ -360,7 +360,7 @@ rnla_status rnla_ctx_create_dist(int device, int world, int rank, const void* nc
     ctx_init(c.get(), device);
     c->world = world;
     c->rank = rank;
-    if (world > 1) {
+    {  // world 1 too: a one-rank communicator runs the sharded paths over NCCL
       ncclUniqueId id;
       std::memcpy(&id, nccl_unique_id, sizeof(id));
       ncclComm_t comm;

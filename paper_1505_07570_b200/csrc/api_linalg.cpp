@@ -384,7 +384,7 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   local.s = s;
   // Row-sharded A: U comes back as this rank's rows,
   // sigma and V replicated.
-  const bool sharded = ctx->world > 1;
+  const bool sharded = is_sharded(ctx);
   require(!sharded || local.kind == RNLA_SKETCH_GAUSSIAN,
           "prototype_ksvd: row-sharded contexts support the Gaussian test matrix");
   require(!sharded || m >= s, "prototype_ksvd: every row shard needs at least s rows");
@@ -840,7 +840,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
       gemm_f32_f64acc(ctx, d, d, n, 1.0, M.as<float>(), M.cs, M.rs, M.as<float>(), M.rs, M.cs, 0.0, G.as<double>(), 1,
                       d);
     trace_mark(ctx, "leverage_rows: gram");
-    if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(d * d), RNLA_F64);
+    if (is_sharded(ctx)) allreduce_sum(ctx, G.p, (size_t)(d * d), RNLA_F64);
     if (!cholesky_upper(ctx, d, G.as<double>()))
       throw NumericError("leverage_sample_rows: M'M is not positive definite (rank-deficient M)");
     upper_inverse(ctx, d, G.as<double>(), Rinv.as<double>());
@@ -927,7 +927,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
       } else {
         std::vector<double> all_scores;
         const double* w = scores;
-        if (ctx->world > 1) {
+        if (is_sharded(ctx)) {
           DevBuf g(sizeof(double) * n_total, ctx->stream);
           RNLA_CUDA(cudaMemsetAsync(g.p, 0, sizeof(double) * n_total, ctx->stream));
           if (n > 0)

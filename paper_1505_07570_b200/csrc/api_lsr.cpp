@@ -66,7 +66,7 @@ struct Pass {
   HVec operator()(double beta, const HVec& x, double* res2 = nullptr) {
     RNLA_CUDA(cudaMemcpyAsync(w.p, x.data(), sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream));
     normal_gemv<T>(ctx, n, d, A.as<T>(), A.rs, b, b_stride, beta, w.as<double>(), g.as<double>(), rr.as<double>());
-    if (ctx->world > 1) {
+    if (is_sharded(ctx)) {
       allreduce_sum(ctx, g.p, (size_t)d, RNLA_F64);
       allreduce_sum(ctx, rr.p, 1, RNLA_F64);
     }
@@ -201,7 +201,7 @@ void lsr_preconditioned_impl(rnla_ctx* ctx, const rnla_mat* a, const rnla_mat* b
       gemm<double>(ctx, d, d, n, 1.0, A.as<double>(), 1, A.rs, A.as<double>(), A.rs, 1, 0.0, G.as<double>(), 1, d);
     else  // exact products + fp64 accumulation: T'GT amplifies Gram errors by |T|^2
       gemm_f32_in_f64(ctx, d, d, n, 1.0, A.as<float>(), 1, A.rs, A.as<float>(), A.rs, 1, 0.0, G.as<double>(), 1, d);
-    if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(d * d), RNLA_F64);
+    if (is_sharded(ctx)) allreduce_sum(ctx, G.p, (size_t)(d * d), RNLA_F64);
     upper_inverse(ctx, d, R.as<double>(), Tm.as<double>());
     gemm<double>(ctx, d, d, d, 1.0, G.as<double>(), 1, d, Tm.as<double>(), 1, d, 0.0, GT.as<double>(), 1, d);
     gemm<double>(ctx, d, d, d, 1.0, Tm.as<double>(), d, 1, GT.as<double>(), 1, d, 0.0, M.as<double>(), 1, d);

@@ -176,7 +176,7 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
       RNLA_CUDA(cudaStreamWaitEvent(gemm_st, ev[(size_t)c], 0));
       StreamScope on_aux(ctx, gemm_st);
       const int owner = (int)(c % ctx->world);
-      if (ctx->world > 1) reduce_to(ctx, mid.as<T>() + b0 * ldm, (size_t)((b1 - b0) * ldm), dt, owner);
+      if (is_sharded(ctx)) reduce_to(ctx, mid.as<T>() + b0 * ldm, (size_t)((b1 - b0) * ldm), dt, owner);
       if (owner == ctx->rank) {
         gaussian_chunk<T>(ctx, g, mid.as<T>(), ldm, s, Lo, s2, b0, first, acc.as<T>(), Lo, 1);
         first = false;
@@ -195,7 +195,7 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
     throw;
   }
   for (auto& e : ev) cudaEventDestroy(e);  // destruction is deferred until the events complete
-  if (ctx->world > 1) allreduce_sum(ctx, acc.p, (size_t)(s2 * Lo), dt);
+  if (is_sharded(ctx)) allreduce_sum(ctx, acc.p, (size_t)(s2 * Lo), dt);
   copy2d<T>(ctx, s2, Lo, acc.as<T>(), Lo, 1, out, o_rs, o_cs);
 }
 
@@ -234,7 +234,7 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
                      const rnla_sketch_spec* spec, int64_t row_offset, T* out, int64_t o_rs, int64_t o_cs) {
   const int64_t Lo = L + (extra ? 1 : 0);
   const int kind = spec->kind;
-  const bool sharded = ctx->world > 1;
+  const bool sharded = is_sharded(ctx);
   const bool chunked = spec->kind == RNLA_SKETCH_COMBINED && gauss_kc_for(ctx, spec->s) < spec->s;
   if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN &&
       (sharded || chunked)) {
@@ -347,7 +347,7 @@ void sketch_rows_entry(rnla_ctx* ctx, const rnla_mat* m, const rnla_mat* extra, 
     const int64_t s = spec->s;
     DevBuf mid(sizeof(T) * (size_t)(s * Lo), ctx->stream);
     count_rows_streamed<T>(ctx, m, extra, s, spec->seed, row_offset, mid.as<T>(), Lo);
-    if (ctx->world > 1) allreduce_sum(ctx, mid.p, (size_t)(s * Lo), m->dtype);
+    if (is_sharded(ctx)) allreduce_sum(ctx, mid.p, (size_t)(s * Lo), m->dtype);
     if (spec->kind == RNLA_SKETCH_COUNT)
       copy2d<T>(ctx, s, Lo, mid.as<T>(), Lo, 1, o.dev.as<T>(), o.dev.rs, o.dev.cs);
     else

@@ -44,7 +44,7 @@ Landmarks landmarks(rnla_ctx* ctx, const DevMat& X, int64_t s, uint64_t seed, in
   sq_norms<T>(ctx, n, d, X.as<T>(), X.rs, X.cs, nullptr, L.sq.as<T>());
   L.Xs = alloc_dense(ctx, s, d, true, X.dtype);
   gather_rows<T>(ctx, s, d, X.as<T>(), X.rs, X.cs, L.dsel.as<int64_t>(), L.Xs.as<T>(), L.Xs.rs, L.Xs.cs);
-  if (ctx->world > 1) allreduce_sum(ctx, L.Xs.p, (size_t)(s * d), X.dtype);
+  if (is_sharded(ctx)) allreduce_sum(ctx, L.Xs.p, (size_t)(s * d), X.dtype);
   L.sqS = DevBuf(sizeof(T) * s, ctx->stream);
   sq_norms<T>(ctx, s, d, L.Xs.as<T>(), L.Xs.rs, L.Xs.cs, nullptr, L.sqS.as<T>());
   RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // `loc` leaves scope
@@ -262,7 +262,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
       gemm_f32_in_f64(ctx, s, s, rows, 1.0, Cb.as<float>(), rows, 1, Cb.as<float>(), 1, rows, 1.0, G.as<double>(), 1,
                       s);
   }
-  if (ctx->world > 1) allreduce_sum(ctx, G.p, (size_t)(s * s), RNLA_F64);  // C'C over row shards
+  if (is_sharded(ctx)) allreduce_sum(ctx, G.p, (size_t)(s * s), RNLA_F64);  // C'C over row shards
   trace_mark(ctx, "nystrom_eig: C'C gram");
   if (overlap) {
     eig_thread.join();

@@ -102,7 +102,7 @@ static void nccl_check(ncclResult_t r, const char* what) {
 }
 
 void allreduce_sum(rnla_ctx* ctx, void* buf, size_t count, int dtype) {
-  if (ctx->world <= 1 || count == 0) return;
+  if (!is_sharded(ctx) || count == 0) return;
   if (ctx->group) return group_reduce(ctx, buf, count, dtype, -1);
   nccl_check(ncclAllReduce(buf, buf, count, dtype == RNLA_F64 ? ncclFloat64 : ncclFloat32, ncclSum,
                            static_cast<ncclComm_t>(ctx->nccl), ctx->stream),
@@ -110,7 +110,7 @@ void allreduce_sum(rnla_ctx* ctx, void* buf, size_t count, int dtype) {
 }
 
 void reduce_to(rnla_ctx* ctx, void* buf, size_t count, int dtype, int root) {
-  if (ctx->world <= 1 || count == 0) return;
+  if (!is_sharded(ctx) || count == 0) return;
   if (ctx->group) return group_reduce(ctx, buf, count, dtype, root);
   nccl_check(ncclReduce(buf, buf, count, dtype == RNLA_F64 ? ncclFloat64 : ncclFloat32, ncclSum, root,
                         static_cast<ncclComm_t>(ctx->nccl), ctx->stream),
@@ -118,7 +118,7 @@ void reduce_to(rnla_ctx* ctx, void* buf, size_t count, int dtype, int root) {
 }
 
 int64_t global_row_offset(rnla_ctx* ctx, int64_t local_rows, int64_t* total_rows) {
-  if (ctx->world <= 1) {
+  if (!is_sharded(ctx)) {
     if (total_rows) *total_rows = local_rows;
     return 0;
   }
@@ -146,7 +146,7 @@ int64_t global_row_offset(rnla_ctx* ctx, int64_t local_rows, int64_t* total_rows
 }
 
 double allreduce_scalar(rnla_ctx* ctx, double v) {
-  if (ctx->world <= 1) return v;
+  if (!is_sharded(ctx)) return v;
   DevBuf b(sizeof(double), ctx->stream);
   RNLA_CUDA(cudaMemcpyAsync(b.p, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   allreduce_sum(ctx, b.p, 1, RNLA_F64);
@@ -160,7 +160,7 @@ void allgather_blocks(rnla_ctx* ctx, const void* mine, void* all, size_t count, 
   RNLA_CUDA(cudaMemsetAsync(all, 0, es * count * (size_t)ctx->world, ctx->stream));
   RNLA_CUDA(cudaMemcpyAsync(static_cast<char*>(all) + es * count * (size_t)ctx->rank, mine, es * count,
                             cudaMemcpyDeviceToDevice, ctx->stream));
-  if (ctx->world <= 1) return;
+  if (!is_sharded(ctx)) return;
   if (ctx->group) return group_reduce(ctx, all, count * (size_t)ctx->world, dtype, -1);
   nccl_check(ncclAllGather(mine, all, count,
                            dtype == RNLA_F32 ? ncclFloat32 : (dtype == RNLA_F64 ? ncclFloat64 : ncclInt64),

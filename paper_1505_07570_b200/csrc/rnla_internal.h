@@ -226,4 +226,9 @@ void scale_inplace(rnla_ctx* ctx, T* p, int64_t count, double divisor);
 
 inline void note_launch(rnla_ctx* ctx, int64_t k = 1) { ctx->launches += k; }
 
+// Row-sharded context: more than one rank, or any NCCL context (a world-1
+// NCCL context runs the sharded code paths and their collectives over a
+// one-rank communicator, so the NCCL transport is exercised on one GPU).
+inline bool is_sharded(const rnla_ctx* c) { return c->world > 1 || c->nccl != nullptr; }
+
 }  // namespace rnla
