@@ -177,6 +177,23 @@ int64_t rnla_sketch_output_cols(const rnla_sketch_spec* spec, int64_t n);
  * sharding); rows are hashed / signed by their global index. */
 rnla_status rnla_sketch_rows(rnla_ctx* ctx, const rnla_mat* m, const rnla_mat* extra, const rnla_sketch_spec* spec,
                              int64_t row_offset, rnla_mat* out);
+/* count_sketch_stream, sketch.hpp:75-76 (src/sketch.cpp:83-92): a single
+ * pass over n columns of length m delivered in order by the caller. begin
+ * opens a device-resident m x s accumulator; push appends the next chunk of
+ * columns (an m x k matrix holding columns j .. j+k-1, host or device; the
+ * call returns once the chunk buffer may be reused); end writes C (m x s)
+ * and frees the stream (also on error); abort frees it without a result.
+ * fp64 results are bit-identical to the reference's sequential loop. */
+typedef struct rnla_count_stream rnla_count_stream;
+rnla_status rnla_count_stream_begin(rnla_ctx* ctx, int64_t m, int64_t n, int64_t s, uint64_t seed, int32_t dtype,
+                                    rnla_count_stream** out);
+rnla_status rnla_count_stream_push(rnla_count_stream* stream, const rnla_mat* columns);
+rnla_status rnla_count_stream_end(rnla_count_stream* stream, rnla_mat* c);
+void rnla_count_stream_abort(rnla_count_stream* stream);
+/* fwht_inplace, sketch.hpp:70 (src/sketch.cpp:44-55) applied to every
+ * column of x in place (column length a power of two); same butterflies in
+ * the same stage order as the reference loop (bit-identical). */
+rnla_status rnla_fwht(rnla_ctx* ctx, rnla_mat* x);
 /* uniform_sample_columns, sketch.hpp:89-90: indices[s] + gathered c. */
 rnla_status rnla_uniform_sample_columns(rnla_ctx* ctx, const rnla_mat* a, int64_t s, uint64_t seed, rnla_mat* c,
                                         int64_t* indices);
@@ -258,6 +275,17 @@ rnla_status rnla_rbf_kernel(rnla_ctx* ctx, const rnla_mat* x1, const rnla_mat* x
  * *entries = kernel entries evaluated (KernelView::entries_evaluated). */
 rnla_status rnla_nystrom(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed, int64_t target_k,
                          rnla_mat* l, int64_t* selected, int64_t* kept, int64_t* entries);
+/* nystrom(const DenseMatrix& K, s, seed, target_k), spsd.hpp:123-124
+ * (src/spsd.cpp:224-228, DenseSpsdSource): K n x n; l (nullable) n x
+ * target_k (or ceil(0.8 s)); selected[s]; *kept as rnla_nystrom. */
+rnla_status rnla_nystrom_dense(rnla_ctx* ctx, const rnla_mat* k, int64_t s, uint64_t seed, int64_t target_k,
+                               rnla_mat* l, int64_t* selected, int64_t* kept);
+/* nystrom(const SpsdSource&, ...), spsd.hpp:119-120 (src/spsd.cpp:181-217)
+ * for any caller-side source: c = K[:, selected] (n x s) already evaluated,
+ * selected[s] strictly increasing (the reference draws them with
+ * sample_without_replacement(n, s, make_rng(derive_seed(seed, 1)))). */
+rnla_status rnla_nystrom_columns(rnla_ctx* ctx, const rnla_mat* c, const int64_t* selected, int64_t target_k,
+                                 rnla_mat* l, int64_t* kept);
 /* approx_eig, spsd.hpp:135 (src/spsd.cpp:257-265): u n x k, lam[k]. */
 rnla_status rnla_approx_eig(rnla_ctx* ctx, const rnla_mat* l, int64_t k, rnla_mat* u, double* lam);
 /* nystrom followed by approx_eig(L, k) without materializing C or L (Gram

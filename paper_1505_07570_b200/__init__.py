@@ -29,7 +29,7 @@ __all__ = [
     "KsvdResult", "KsvdOptions", "LsrSolution", "KernelSpec", "KernelView", "NystromFactor", "NumericError",
     "CudaError", "splitmix64", "derive_seed", "count_sketch_hashes", "gaussian_matrix",
     "sample_without_replacement", "sample_with_replacement", "srht_operator", "gaussian_sketch", "srht_sketch",
-    "count_sketch", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
+    "count_sketch", "count_sketch_stream", "fwht_inplace", "nystrom_columns", "combined_sketch", "apply_sketch", "sketch_rows", "uniform_sample_columns", "leverage_scores",
     "leverage_sample_columns", "leverage_sample_rows", "thin_qr", "condensed_svd", "truncated_svd",
     "pseudo_inverse", "prototype_ksvd", "faster_ksvd", "lsr_sketched", "lsr_cg", "lsr_preconditioned", "PreconditionedOptions", "rbf_kernel", "nystrom", "approx_eig", "nystrom_eig", "SpsdSketch", "spsd_faster", "CurFactors", "cur_faster_kernel",
     "shard_rows",
@@ -434,6 +434,55 @@ def sketch_rows(m, spec: SketchSpec, extra=None, row_offset: int = 0, out=None, 
     return out
 
 
+def count_sketch_stream(m: int, n: int, s: int, seed: int, column, chunk: int = 4096, dtype=np.float64,
+                        ctx: Optional[Context] = None) -> np.ndarray:
+    """Single pass over the n columns delivered by column(j), each called
+    exactly once in j order (src/sketch.cpp:83-92); columns are packed into
+    chunks and accumulated on the device. Returns C (m x s, column-major);
+    fp64 is bit-identical to the reference's sequential loop."""
+    if s < 1:
+        raise ValueError("count_sketch: s < 1")
+    lib = _abi.lib()
+    c = _ctx(ctx)
+    st = C.c_void_p()
+    _check(lib.rnla_count_stream_begin(c.handle, m, n, s, C.c_uint64(seed),
+                                       _abi.RNLA_F64 if np.dtype(dtype) == np.float64 else _abi.RNLA_F32,
+                                       C.byref(st)))
+    try:
+        buf = np.empty((m, max(1, min(chunk, n))), dtype=dtype, order="F")
+        j = 0
+        while j < n:
+            k = min(buf.shape[1], n - j)
+            for t in range(k):
+                buf[:, t] = np.asarray(column(j + t), dtype=dtype).reshape(m)
+            bm = _mat(buf[:, :k])
+            _check(lib.rnla_count_stream_push(st, C.byref(bm)))
+            j += k
+    except BaseException:
+        lib.rnla_count_stream_abort(st)
+        raise
+    out = np.empty((m, s), dtype=dtype, order="F")
+    om = _mat(out)
+    _check(lib.rnla_count_stream_end(st, C.byref(om)))
+    return out
+
+
+def fwht_inplace(x, ctx: Optional[Context] = None):
+    """Unnormalized Sylvester-order FWHT of x (length 2^q) or of every column
+    of a 2-D x, in place (src/sketch.cpp:44-55); returns x."""
+    if _is_torch(x):
+        x2 = x if x.dim() == 2 else x.reshape(-1, 1)
+    else:
+        if not (isinstance(x, np.ndarray) and x.dtype in (np.float32, np.float64)):
+            raise ValueError("fwht_inplace: a float32/float64 numpy array or torch tensor is required")
+        x2 = x if x.ndim == 2 else x.reshape(-1, 1)
+        if _bad_strides(x2):
+            raise ValueError("fwht_inplace: x must have positive strides")
+    xm = _mat(x2)
+    _check(_abi.lib().rnla_fwht(_ctx(ctx).handle, C.byref(xm)))
+    return x
+
+
 def uniform_sample_columns(a, s: int, seed: int, ctx: Optional[Context] = None):
     a2 = _as2d(a)
     c = _empty_like(a2, a2.shape[0], s, "F")
@@ -741,22 +790,54 @@ def rbf_kernel(x1, x2, sigma: float, ctx: Optional[Context] = None):
     return k
 
 
-def nystrom(k: KernelView, s: int, seed: int, target_k: int = 0, ctx: Optional[Context] = None) -> NystromFactor:
-    """Nystrom factor L with L L' ~ C W_k^+ C' (src/spsd.cpp:181-222)."""
-    x = k.data()
-    n = k.n()
+def nystrom(k, s: int, seed: int, target_k: int = 0, ctx: Optional[Context] = None) -> NystromFactor:
+    """Nystrom factor L with L L' ~ C W_k^+ C' (src/spsd.cpp:181-228): k is a
+    KernelView (kernel columns evaluated on the device, entries counted) or a
+    dense SPSD matrix K (the reference's nystrom(const DenseMatrix&, ...))."""
+    kk = target_k if target_k > 0 else int(math.ceil(0.8 * s))
+    sel = np.empty(s, dtype=np.int64)
+    kept = C.c_int64()
+    if isinstance(k, KernelView):
+        x = k.data()
+        n = k.n()
+        if not (1 <= kk <= s <= n):
+            raise ValueError("nystrom: need k <= s <= n")
+        L = _empty_like(x, n, kk, "F")
+        entries = C.c_int64()
+        xm, lm = _mat(x), _mat(L)
+        _check(_abi.lib().rnla_nystrom(_ctx(ctx).handle, C.byref(xm), float(k.spec().sigma), s, C.c_uint64(seed),
+                                       int(target_k), C.byref(lm), sel.ctypes.data_as(_abi._I64P), C.byref(kept),
+                                       C.byref(entries)))
+        k._add(entries.value)
+        return NystromFactor(L[:, :kept.value], sel)
+    K = _as2d(k)
+    n = K.shape[0]
+    if K.shape[0] != K.shape[1]:
+        raise ValueError("nystrom: K not square")
+    if not (1 <= kk <= s <= n):
+        raise ValueError("nystrom: need k <= s <= n")
+    L = _empty_like(K, n, kk, "F")
+    km, lm = _mat(K), _mat(L)
+    _check(_abi.lib().rnla_nystrom_dense(_ctx(ctx).handle, C.byref(km), s, C.c_uint64(seed), int(target_k),
+                                         C.byref(lm), sel.ctypes.data_as(_abi._I64P), C.byref(kept)))
+    return NystromFactor(L[:, :kept.value], sel)
+
+
+def nystrom_columns(c, selected, target_k: int = 0, ctx: Optional[Context] = None) -> NystromFactor:
+    """nystrom(const SpsdSource&, ...) for a caller-side source: c = K[:, selected]
+    (n x s) already evaluated; selected strictly increasing (src/spsd.cpp:181-217)."""
+    c2 = _as2d(c)
+    n, s = c2.shape
     kk = target_k if target_k > 0 else int(math.ceil(0.8 * s))
     if not (1 <= kk <= s <= n):
         raise ValueError("nystrom: need k <= s <= n")
-    L = _empty_like(x, n, kk, "F")
-    sel = np.empty(s, dtype=np.int64)
-    kept, entries = C.c_int64(), C.c_int64()
-    xm, lm = _mat(x), _mat(L)
-    _check(_abi.lib().rnla_nystrom(_ctx(ctx).handle, C.byref(xm), float(k.spec().sigma), s, C.c_uint64(seed),
-                                   int(target_k), C.byref(lm), sel.ctypes.data_as(_abi._I64P), C.byref(kept),
-                                   C.byref(entries)))
-    k._add(entries.value)
-    return NystromFactor(L[:, :kept.value], sel)
+    sel = np.ascontiguousarray(selected, dtype=np.int64)
+    L = _empty_like(c2, n, kk, "F")
+    kept = C.c_int64()
+    cm, lm = _mat(c2), _mat(L)
+    _check(_abi.lib().rnla_nystrom_columns(_ctx(ctx).handle, C.byref(cm), sel.ctypes.data_as(_abi._I64P),
+                                           int(target_k), C.byref(lm), C.byref(kept)))
+    return NystromFactor(L[:, :kept.value], sel.copy())
 
 
 def approx_eig(l, k: int, ctx: Optional[Context] = None):

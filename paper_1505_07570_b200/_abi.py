@@ -82,6 +82,11 @@ SIGNATURES = {
     "rnla_apply_sketch": (C.c_int, [_P, _M, _S, _M, _I64P]),
     "rnla_sketch_output_cols": (C.c_int64, [_S, C.c_int64]),
     "rnla_sketch_rows": (C.c_int, [_P, _M, _M, _S, C.c_int64, _M]),
+    "rnla_count_stream_begin": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int32, C.POINTER(_P)]),
+    "rnla_count_stream_push": (C.c_int, [_P, _M]),
+    "rnla_count_stream_end": (C.c_int, [_P, _M]),
+    "rnla_count_stream_abort": (None, [_P]),
+    "rnla_fwht": (C.c_int, [_P, _M]),
     "rnla_uniform_sample_columns": (C.c_int, [_P, _M, C.c_int64, C.c_uint64, _M, _I64P]),
     "rnla_leverage_scores": (C.c_int, [_P, _M, C.c_int64, _F64P]),
     "rnla_leverage_sample_columns": (
@@ -101,6 +106,8 @@ SIGNATURES = {
         C.c_int, [_P, _M, _M, C.c_double, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _F64P, _F64P, _I32P, _F64P]),
     "rnla_rbf_kernel": (C.c_int, [_P, _M, _M, C.c_double, _M]),
     "rnla_nystrom": (C.c_int, [_P, _M, C.c_double, C.c_int64, C.c_uint64, C.c_int64, _M, _I64P, _I64P, _I64P]),
+    "rnla_nystrom_dense": (C.c_int, [_P, _M, C.c_int64, C.c_uint64, C.c_int64, _M, _I64P, _I64P]),
+    "rnla_nystrom_columns": (C.c_int, [_P, _M, _I64P, C.c_int64, _M, _I64P]),
     "rnla_approx_eig": (C.c_int, [_P, _M, C.c_int64, _M, _F64P]),
     "rnla_nystrom_eig": (
         C.c_int, [_P, _M, C.c_double, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, _M, _F64P, _I64P, _I64P]),

@@ -109,25 +109,19 @@ DevBuf whitened(rnla_ctx* ctx, const EigW& e, int64_t s) {
   return T;
 }
 
+// The reference's generic nystrom(SpsdSource) body (src/spsd.cpp:181-217)
+// given C = K[:, S] on the device (n x s col-major, ld n, compute dtype T) and
+// the landmarks' rows dsel inside C: W = rows S of C, eig(0.5 (W + W')),
+// eigenvalue floor, L = C U_k Lambda_k^-1/2.
 template <class T>
-void nystrom_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed, int64_t target_k,
-                  const rnla_mat* l_out, int64_t* selected, int64_t* kept_out, int64_t* entries) {
-  DevMat X = to_device(ctx, x);
-  const int64_t n = X.rows;
-  const int64_t kk = target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
-  require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
-  require(ctx->world == 1, "nystrom: row-sharded contexts use nystrom_eig");
-  Landmarks L = landmarks<T>(ctx, X, s, seed, n, 0);
-  // C = K[:, S] (n x s, col-major, compute dtype), W = rows S of C
-  DevBuf C(sizeof(T) * n * s, ctx->stream);
-  kernel_columns<T>(ctx, X, L, 0, n, sigma, C.as<T>(), 1, n);
+void nystrom_from_columns(rnla_ctx* ctx, const T* C, const int64_t* dsel, int64_t n, int64_t s, int64_t kk,
+                          const rnla_mat* l_out, int64_t* kept_out) {
   DevBuf W(sizeof(double) * s * s, ctx->stream);
-  DevBuf W64;
   if constexpr (std::is_same<T, double>::value) {
-    gather_rows<double>(ctx, s, s, C.as<double>(), 1, n, L.dsel.as<int64_t>(), W.as<double>(), 1, s);
+    gather_rows<double>(ctx, s, s, C, 1, n, dsel, W.as<double>(), 1, s);
   } else {
     DevBuf Wf(sizeof(float) * s * s, ctx->stream);
-    gather_rows<float>(ctx, s, s, C.as<float>(), 1, n, L.dsel.as<int64_t>(), Wf.as<float>(), 1, s);
+    gather_rows<float>(ctx, s, s, C, 1, n, dsel, Wf.as<float>(), 1, s);
     copy2d_cast<float, double>(ctx, s, s, Wf.as<float>(), 1, s, W.as<double>(), 1, s);
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
   }
@@ -136,20 +130,74 @@ void nystrom_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uin
   if (l_out) {
     OutMat lo(ctx, l_out, n, kk, "nystrom: L", false);
     if constexpr (std::is_same<T, double>::value) {
-      gemm<double>(ctx, n, e.kept, s, 1.0, C.as<double>(), 1, n, Tm.as<double>(), 1, s, 0.0, lo.dev.as<double>(),
-                   lo.dev.rs, lo.dev.cs);
+      gemm<double>(ctx, n, e.kept, s, 1.0, C, 1, n, Tm.as<double>(), 1, s, 0.0, lo.dev.as<double>(), lo.dev.rs,
+                   lo.dev.cs);
     } else {
       DevBuf Tf(sizeof(float) * s * e.kept, ctx->stream);
       copy2d_cast<double, float>(ctx, s, e.kept, Tm.as<double>(), 1, s, Tf.as<float>(), 1, s);
-      gemm<float>(ctx, n, e.kept, s, 1.f, C.as<float>(), 1, n, Tf.as<float>(), 1, s, 0.f, lo.dev.as<float>(),
-                  lo.dev.rs, lo.dev.cs);
+      gemm<float>(ctx, n, e.kept, s, 1.f, C, 1, n, Tf.as<float>(), 1, s, 0.f, lo.dev.as<float>(), lo.dev.rs,
+                  lo.dev.cs);
     }
     lo.finish(ctx);
   }
-  std::copy(L.sel.begin(), L.sel.end(), selected);
   *kept_out = e.kept;
-  if (entries) *entries = n * s;
   RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static int64_t nystrom_k(int64_t target_k, int64_t s) {
+  return target_k > 0 ? target_k : (int64_t)std::ceil(0.8 * static_cast<double>(s));
+}
+
+template <class T>
+void nystrom_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s, uint64_t seed, int64_t target_k,
+                  const rnla_mat* l_out, int64_t* selected, int64_t* kept_out, int64_t* entries) {
+  DevMat X = to_device(ctx, x);
+  const int64_t n = X.rows;
+  const int64_t kk = nystrom_k(target_k, s);
+  require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
+  require(ctx->world == 1, "nystrom: row-sharded contexts use nystrom_eig");
+  Landmarks L = landmarks<T>(ctx, X, s, seed, n, 0);
+  // C = K[:, S] (n x s, col-major, compute dtype) from the KernelView
+  DevBuf C(sizeof(T) * n * s, ctx->stream);
+  kernel_columns<T>(ctx, X, L, 0, n, sigma, C.as<T>(), 1, n);
+  nystrom_from_columns<T>(ctx, C.as<T>(), L.dsel.as<int64_t>(), n, s, kk, l_out, kept_out);
+  std::copy(L.sel.begin(), L.sel.end(), selected);
+  if (entries) *entries = n * s;
+}
+
+// nystrom(const DenseMatrix& K, ...) (src/spsd.cpp:224-228): DenseSpsdSource
+// columns K[:, S] gathered on the device.
+template <class T>
+void nystrom_dense_impl(rnla_ctx* ctx, const rnla_mat* k, int64_t s, uint64_t seed, int64_t target_k,
+                        const rnla_mat* l_out, int64_t* selected, int64_t* kept_out) {
+  require(k->rows == k->cols, "nystrom: K not square");
+  const int64_t n = k->rows, kk = nystrom_k(target_k, s);
+  require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
+  DevMat K = to_device(ctx, k);
+  const std::vector<int64_t> sel = sample_without_replacement_host(derive_seed(seed, 1), n, s);
+  DevBuf dsel(sizeof(int64_t) * s, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(dsel.p, sel.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+  DevBuf C(sizeof(T) * n * s, ctx->stream);
+  gather_columns<T>(ctx, n, s, K.as<T>(), K.rs, K.cs, dsel.as<int64_t>(), nullptr, C.as<T>(), 1, n);
+  nystrom_from_columns<T>(ctx, C.as<T>(), dsel.as<int64_t>(), n, s, kk, l_out, kept_out);
+  std::copy(sel.begin(), sel.end(), selected);
+}
+
+// nystrom(const SpsdSource&, ...) for a caller-provided source: C = K[:, S]
+// already evaluated by the caller (the landmarks drawn as the reference does).
+template <class T>
+void nystrom_columns_impl(rnla_ctx* ctx, const rnla_mat* c, const int64_t* selected, int64_t target_k,
+                          const rnla_mat* l_out, int64_t* kept_out) {
+  const int64_t n = c->rows, s = c->cols, kk = nystrom_k(target_k, s);
+  require(kk >= 1 && kk <= s && s <= n, "nystrom: need k <= s <= n");
+  for (int64_t t = 0; t < s; ++t)
+    require(selected[t] >= 0 && selected[t] < n && (t == 0 || selected[t] > selected[t - 1]),
+            "nystrom: selected indices must be strictly increasing and < n");
+  DevMat C = as_colmajor(ctx, to_device(ctx, c));
+  DevMat Cd = C.cs == n ? std::move(C) : dense_copy(ctx, C, false, C.dtype);
+  DevBuf dsel(sizeof(int64_t) * s, ctx->stream);
+  RNLA_CUDA(cudaMemcpyAsync(dsel.p, selected, sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+  nystrom_from_columns<T>(ctx, Cd.as<T>(), dsel.as<int64_t>(), n, s, kk, l_out, kept_out);
 }
 
 // nystrom + approx_eig(L, k) through the Gram route:
@@ -641,6 +689,30 @@ rnla_status rnla_nystrom(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t
     require(selected && kept, "nystrom: null output");
     if (x->dtype == RNLA_F64) nystrom_impl<double>(ctx, x, sigma, s, seed, target_k, l, selected, kept, entries);
     else nystrom_impl<float>(ctx, x, sigma, s, seed, target_k, l, selected, kept, entries);
+  });
+}
+
+rnla_status rnla_nystrom_dense(rnla_ctx* ctx, const rnla_mat* k, int64_t s, uint64_t seed, int64_t target_k,
+                               rnla_mat* l, int64_t* selected, int64_t* kept) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(k, "nystrom: K");
+    require(selected && kept, "nystrom: null output");
+    require(ctx->world == 1, "nystrom: row-sharded contexts use nystrom_eig");
+    if (k->dtype == RNLA_F64) nystrom_dense_impl<double>(ctx, k, s, seed, target_k, l, selected, kept);
+    else nystrom_dense_impl<float>(ctx, k, s, seed, target_k, l, selected, kept);
+  });
+}
+
+rnla_status rnla_nystrom_columns(rnla_ctx* ctx, const rnla_mat* c, const int64_t* selected, int64_t target_k,
+                                 rnla_mat* l, int64_t* kept) {
+  return guard([&] {
+    enter(ctx);
+    check_mat(c, "nystrom: C");
+    require(selected && kept, "nystrom: null argument");
+    require(ctx->world == 1, "nystrom: row-sharded contexts use nystrom_eig");
+    if (c->dtype == RNLA_F64) nystrom_columns_impl<double>(ctx, c, selected, target_k, l, kept);
+    else nystrom_columns_impl<float>(ctx, c, selected, target_k, l, kept);
   });
 }
 

@@ -197,6 +197,10 @@ void count_sketch_segments(rnla_ctx* ctx, const T* in, int64_t ld, const T* extr
 #undef RNLA_G
 }
 
+void count_sketch_plan_release(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int64_t j0) {
+  ctx->cs_plans.erase(std::make_tuple(n, s, j0, seed));
+}
+
 template void count_sketch_segments<double>(rnla_ctx*, const double*, int64_t, const double*, int64_t, int64_t, int64_t,
                                             int64_t, uint64_t, int64_t, double*, int64_t, bool, int64_t, int64_t);
 template void count_sketch_segments<float>(rnla_ctx*, const float*, int64_t, const float*, int64_t, int64_t, int64_t,

@@ -151,6 +151,8 @@ void count_sketch_segments(rnla_ctx* ctx, const T* in, int64_t ld, const T* extr
                            int64_t L, int64_t s, uint64_t seed, int64_t j0, T* out, int64_t ldo, bool accumulate,
                            int64_t b0 = 0, int64_t b1 = -1);
 const CountSketchPlan& count_sketch_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int64_t j0);
+// Drop a cached plan (one-shot plans, e.g. the chunks of count_sketch_stream).
+void count_sketch_plan_release(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed, int64_t j0);
 
 // General strided GEMM: C[m x n] = alpha * A[m x k] * B[k x n] + beta * C, element
 // (i, j) of X at X[i*rs + j*cs].
