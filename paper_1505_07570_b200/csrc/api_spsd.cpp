@@ -219,8 +219,19 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(n_local, 16384));
   DevBuf Cb(sizeof(T) * blk * s, ctx->stream);
   DevBuf G(sizeof(double) * s * s, ctx->stream), W(sizeof(double) * s * s, ctx->stream);
+  // fp32 points: the exact int8-digit Gram on the tensor cores (gram_i8.cu);
+  // W and C'C then describe the same quantized kernel matrix.
+  const bool i8 = std::is_same<T, float>::value && gram_i8_available();
   // W = K[S, S]: its rows are the landmark rows of C (recomputed directly).
-  {
+  if (i8) {
+    DevBuf ident(sizeof(int64_t) * s, ctx->stream);
+    std::vector<int64_t> id((size_t)s);
+    for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
+    RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    rbf_digits(ctx, s, s, X.cols, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs,
+               L.sqS.as<float>(), L.sqS.as<float>(), sigma, ident.as<int64_t>(), nullptr, 0, 0, W.as<double>(), s);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
     DevBuf Wt(sizeof(T) * s * s, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
     std::vector<int64_t> id((size_t)s);
     for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
@@ -295,7 +306,24 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
     }
   } joiner{eig_thread};
   RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * s * s, ctx->stream));
-  for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
+  if (i8) {
+    // digit planes of C (3 bytes per entry) for blocks of at most ~2 GB
+    const int64_t rows_blk = std::min<int64_t>(
+        n_local, std::max<int64_t>(65536, (int64_t)(2e9 / (3.0 * (double)s)) / 64 * 64));
+    const int64_t pitch = digit_pitch(rows_blk);
+    DevBuf planes(3 * (size_t)s * (size_t)pitch, ctx->stream), diag(sizeof(int64_t) * s, ctx->stream);
+    for (int64_t r0 = 0; r0 < n_local; r0 += rows_blk) {
+      const int64_t rows = std::min(rows_blk, n_local - r0);
+      std::vector<int64_t> h(L.sel);
+      for (auto& v : h) v -= L.r_off + r0;
+      RNLA_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+      rbf_digits(ctx, rows, s, X.cols, X.as<float>() + r0 * X.rs, X.rs, X.cs, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs,
+                 L.sq.as<float>() + r0, L.sqS.as<float>(), sigma, diag.as<int64_t>(), planes.as<int8_t>(), pitch,
+                 s * pitch, nullptr, 0);
+      gram_i8(ctx, planes.as<int8_t>(), rows, s, pitch, G.as<double>(), r0 > 0);  // synchronizes
+    }
+  }
+  for (int64_t r0 = 0; r0 < (i8 ? 0 : n_local); r0 += blk) {
     const int64_t rows = std::min(blk, n_local - r0);
     kernel_columns<T>(ctx, X, L, r0, rows, sigma, Cb.as<T>(), 1, rows);
     if constexpr (std::is_same<T, double>::value)

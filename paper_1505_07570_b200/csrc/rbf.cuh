@@ -34,3 +34,18 @@ void gather_rows(rnla_ctx* ctx, int64_t cnt, int64_t cols, const T* A, int64_t a
 // out = 0.5 * (W + W') for column-major n x n fp64 W (src/spsd.cpp:195-196).
 void symmetrize(rnla_ctx* ctx, int64_t n, const double* W, double* out);
 }  // namespace rnla
+
+namespace rnla {
+// Exact int8-digit Gram route for fp32 RBF kernel columns (gram_i8.cu).
+bool gram_i8_available();
+int64_t digit_pitch(int64_t n);
+// Digits of K(i, j) (x rows vs y rows, diag_of forcing exact ones) into three
+// int8 planes (planes + d * plane_stride + j * pitch + i), or the exact
+// dequantized fp64 values into w (w[i + j * ldw]) when planes == nullptr.
+void rbf_digits(rnla_ctx* ctx, int64_t n1, int64_t n2, int64_t d, const float* X, int64_t x_rs, int64_t x_cs,
+                const float* Y, int64_t y_rs, int64_t y_cs, const float* sqx, const float* sqy, double sigma,
+                const int64_t* diag_of, int8_t* planes, int64_t pitch, int64_t plane_stride, double* w, int64_t ldw);
+// G (s x s col-major fp64; += when accumulate) = exact Gram of the digit
+// planes of an n x s matrix (plane d of column p at planes + d s pitch + p pitch).
+void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t pitch, double* G, bool accumulate);
+}  // namespace rnla
