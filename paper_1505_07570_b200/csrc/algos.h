@@ -35,7 +35,8 @@ void ritz_residual_dev(rnla_ctx* ctx, int64_t n, int64_t k, const double* YZ, co
 // V (device, n x k, matching columns). Returns false (outputs untouched) when
 // the problem is too small for a block of 2k or it did not converge; callers
 // then use the direct solver (api_linalg.cpp).
-bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, double* lam, double* V);
+bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, double* lam, double* V,
+                      bool values_only = false);
 
 // g = A'(beta*b - A w) and *rr = |beta*b - A w|^2 in one pass over the
 // row-major A (n x d, row stride ld; d <= 1024), fp64 accumulation; g and rr

@@ -223,7 +223,51 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   // W and C'C then describe the same quantized kernel matrix.
   const bool i8 = std::is_same<T, float>::value && gram_i8_available();
   // W = K[S, S]: its rows are the landmark rows of C (recomputed directly).
-  if (i8) {
+  // digit planes of C (3 bytes per entry) in row blocks of at most ~2 GB
+  const int64_t rows_blk =
+      i8 ? std::max<int64_t>(1, std::min<int64_t>(
+               n_local, std::max<int64_t>(65536, (int64_t)(2e9 / (3.0 * (double)s)) / 64 * 64)))
+         : 1;
+  const int64_t pitch = i8 ? digit_pitch(rows_blk) : 0;
+  DevBuf planes(i8 ? 3 * (size_t)s * (size_t)pitch : 0, ctx->stream);
+  // tensor-core kernel columns (d <= 64, C in one block of digit planes);
+  // otherwise W and C both come from the sequential-FMA kernel
+  const bool tc_rbf = i8 && rows_blk >= n_local && rbf_tc_available(X.cols);
+  // SMs left to the eig(W) / Cholesky route that runs on the helper stream
+  // while the tensor-core kernels below stream C (their kernels are
+  // latency-bound cuSOLVER launches that would otherwise wait for whole SMs)
+  int reserve_sms = 0;
+  auto c_digits = [&](int64_t r0, int64_t rows) {  // digit planes of rows [r0, r0 + rows) of C
+    DevBuf diag(sizeof(int64_t) * s, ctx->stream);
+    std::vector<int64_t> h(L.sel);
+    for (auto& v : h) v -= L.r_off + r0;
+    RNLA_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    if (tc_rbf)
+      rbf_tc_digits(ctx, rows, s, X.cols, X.as<float>() + r0 * X.rs, X.rs, X.cs, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs,
+                    L.sq.as<float>() + r0, L.sqS.as<float>(), sigma, diag.as<int64_t>(), planes.as<int8_t>(), pitch,
+                    s * pitch, reserve_sms);
+    else
+      rbf_digits(ctx, rows, s, X.cols, X.as<float>() + r0 * X.rs, X.rs, X.cs, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs,
+                 L.sq.as<float>() + r0, L.sqS.as<float>(), sigma, diag.as<int64_t>(), planes.as<int8_t>(), pitch,
+                 s * pitch, nullptr, 0);
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // `h` leaves scope
+  };
+  if (tc_rbf) {
+    // W = K[S, S] from the same tensor-core kernel on the landmark points: an
+    // MMA output element depends only on its row and column operands, so these
+    // digits equal the landmark rows of C's digits bit for bit (checked with
+    // RNLA_CHECK_W_DIGITS=1). W is ready before C, so the Cholesky route below
+    // overlaps the kernel columns and the Gram.
+    const int64_t pw = digit_pitch(s);
+    DevBuf wplanes(3 * (size_t)s * (size_t)pw, ctx->stream), ident(sizeof(int64_t) * s, ctx->stream);
+    std::vector<int64_t> id((size_t)s);
+    for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
+    RNLA_CUDA(cudaMemcpyAsync(ident.p, id.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
+    rbf_tc_digits(ctx, s, s, X.cols, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs,
+                  L.sqS.as<float>(), L.sqS.as<float>(), sigma, ident.as<int64_t>(), wplanes.as<int8_t>(), pw, s * pw);
+    w_from_digits(ctx, s, ident.as<int64_t>(), wplanes.as<int8_t>(), pw, s * pw, W.as<double>());
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else if (i8) {
     DevBuf ident(sizeof(int64_t) * s, ctx->stream);
     std::vector<int64_t> id((size_t)s);
     for (int64_t i = 0; i < s; ++i) id[(size_t)i] = i;
@@ -306,21 +350,33 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
     }
   } joiner{eig_thread};
   RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * s * s, ctx->stream));
-  if (i8) {
-    // digit planes of C (3 bytes per entry) for blocks of at most ~2 GB
-    const int64_t rows_blk = std::min<int64_t>(
-        n_local, std::max<int64_t>(65536, (int64_t)(2e9 / (3.0 * (double)s)) / 64 * 64));
-    const int64_t pitch = digit_pitch(rows_blk);
-    DevBuf planes(3 * (size_t)s * (size_t)pitch, ctx->stream), diag(sizeof(int64_t) * s, ctx->stream);
+  // 16 SMs measured best on config 4 (0 / 8 / 16 / 24 / 32 / 48: 13.2 / 12.4 /
+  // 11.8 / 12.0 / 12.2 / 11.9 ms)
+  reserve_sms = overlap ? 16 : 0;
+  if (tc_rbf) {
+    c_digits(0, n_local);
+    if (std::getenv("RNLA_CHECK_W_DIGITS")) {  // W's digits == the landmark rows of C's digits?
+      DevBuf W2(sizeof(double) * s * s, ctx->stream);
+      w_from_digits(ctx, s, L.dsel.as<int64_t>(), planes.as<int8_t>(), pitch, s * pitch, W2.as<double>());
+      std::vector<double> a((size_t)(s * s)), b((size_t)(s * s));
+      RNLA_CUDA(cudaMemcpyAsync(a.data(), W.p, sizeof(double) * s * s, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaMemcpyAsync(b.data(), W2.p, sizeof(double) * s * s, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::vector<int64_t> loc(L.sel);
+      int64_t bad = 0, checked = 0;
+      for (int64_t t = 0; t < s; ++t) {
+        if (loc[(size_t)t] < L.r_off || loc[(size_t)t] >= L.r_off + n_local) continue;
+        for (int64_t j = 0; j < s; ++j, ++checked) bad += a[(size_t)(t + j * s)] != b[(size_t)(t + j * s)];
+      }
+      std::fprintf(stderr, "[rnla] W digits vs C landmark-row digits: %lld of %lld differ\n", (long long)bad,
+                   (long long)checked);
+    }
+    gram_i8(ctx, planes.as<int8_t>(), n_local, s, pitch, G.as<double>(), false, reserve_sms);
+  } else if (i8) {
     for (int64_t r0 = 0; r0 < n_local; r0 += rows_blk) {
       const int64_t rows = std::min(rows_blk, n_local - r0);
-      std::vector<int64_t> h(L.sel);
-      for (auto& v : h) v -= L.r_off + r0;
-      RNLA_CUDA(cudaMemcpyAsync(diag.p, h.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, ctx->stream));
-      rbf_digits(ctx, rows, s, X.cols, X.as<float>() + r0 * X.rs, X.rs, X.cs, L.Xs.as<float>(), L.Xs.rs, L.Xs.cs,
-                 L.sq.as<float>() + r0, L.sqS.as<float>(), sigma, diag.as<int64_t>(), planes.as<int8_t>(), pitch,
-                 s * pitch, nullptr, 0);
-      gram_i8(ctx, planes.as<int8_t>(), rows, s, pitch, G.as<double>(), r0 > 0);  // synchronizes
+      c_digits(r0, rows);
+      gram_i8(ctx, planes.as<int8_t>(), rows, s, pitch, G.as<double>(), r0 > 0, reserve_sms);  // synchronizes
     }
   }
   for (int64_t r0 = 0; r0 < (i8 ? 0 : n_local); r0 += blk) {
@@ -375,7 +431,7 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   // else the full syevd.
   std::vector<double> top((size_t)k);
   DevBuf Vk(sizeof(double) * kp * k, ctx->stream);  // descending eigenvectors
-  if (!eig_top_subspace(ctx, kp, Ms.as<double>(), k, top.data(), Vk.as<double>())) {
+  if (!eig_top_subspace(ctx, kp, Ms.as<double>(), k, top.data(), Vk.as<double>(), u_out == nullptr)) {
     const double* vtop = nullptr;  // eigenvector of the largest eigenvalue; the next ones at stride -kp
     if (2 * k <= kp && !std::getenv("RNLA_EIG_FULL")) {
       const int64_t found = eig_sym_top(ctx, kp, Ms.as<double>(), k, ev.as<double>());

@@ -60,6 +60,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
                "r"(bytes)
@@ -203,19 +206,25 @@ __global__ void __launch_bounds__(256) rbf_digits_kernel(int64_t n1, int64_t n2,
   }
 }
 
-// One 128 x 96 tile (ib, jb) of G over rows [k0, k0 + kc) of C.
+// Persistent: CTA b processes work items b, b + gridDim.x, ... (item = tile +
+// ntiles * chunk: one 128 x 96 tile (ib, jb) of G over rows [k0, k0 + kc) of
+// C). The shared-memory ring runs across items; the epilogue of item i hands
+// the TMEM accumulators back (acc_empty) before the MMAs of item i + 1 start.
 __global__ void __launch_bounds__(GRAM_THREADS, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
-                   const int2* __restrict__ tiles, int ntiles, int64_t n, int64_t kc, double* __restrict__ ws) {
+                   const int2* __restrict__ tiles, int ntiles, int nitems, int64_t n, int64_t kc,
+                   double* __restrict__ ws) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GSTAGES * STAGE_BYTES);  // full[S], empty[S], done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * GSTAGES + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GSTAGES * STAGE_BYTES);  // full[S], empty[S], acc_full, acc_empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * GSTAGES + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int2 tile = tiles[blockIdx.x];
-  const int64_t k0 = (int64_t)blockIdx.y * kc;
-  const int64_t klen = n - k0 < kc ? n - k0 : kc;
-  const int nkb = klen > 0 ? (int)((klen + GBK - 1) / GBK) : 0;
+  auto item_nkb = [&](int w, int2& tile, int64_t& k0) {
+    tile = tiles[w % ntiles];
+    k0 = (int64_t)(w / ntiles) * kc;
+    const int64_t klen = n - k0 < kc ? n - k0 : kc;
+    return klen > 0 ? (int)((klen + GBK - 1) / GBK) : 0;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < GSTAGES; ++s) {
@@ -223,6 +232,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1)
       mbar_init(su32(&bars[GSTAGES + s]), 1);
     }
     mbar_init(su32(&bars[2 * GSTAGES]), 1);
+    mbar_init(su32(&bars[2 * GSTAGES + 1]), 128);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -237,65 +247,87 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % GSTAGES;
-        if (kb >= GSTAGES) mbar_wait(su32(&bars[GSTAGES + st]), (uint32_t)(((kb / GSTAGES) - 1) & 1));
-        const uint32_t full = su32(&bars[st]);
-        mbar_expect_tx(full, STAGE_BYTES);
-        const uint32_t base = su32(smem + st * STAGE_BYTES);
-        const int kx = (int)(k0 + (int64_t)kb * GBK);
+      int g = 0;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        int2 tile;
+        int64_t k0;
+        const int nkb = item_nkb(w, tile, k0);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int st = g % GSTAGES;
+          if (g >= GSTAGES) mbar_wait(su32(&bars[GSTAGES + st]), (uint32_t)(((g / GSTAGES) - 1) & 1));
+          const uint32_t full = su32(&bars[st]);
+          mbar_expect_tx(full, STAGE_BYTES);
+          const uint32_t base = su32(smem + st * STAGE_BYTES);
+          const int kx = (int)(k0 + (int64_t)kb * GBK);
 #pragma unroll
-        for (int dg = 0; dg < GND; ++dg) {
-          tma_load_3d(base + dg * A_TILE, &amap, kx, tile.x * GM, dg, full);
-          tma_load_3d(base + GND * A_TILE + dg * B_TILE, &bmap, kx, tile.y * GN, dg, full);
+          for (int dg = 0; dg < GND; ++dg) {
+            tma_load_3d(base + dg * A_TILE, &amap, kx, tile.x * GM, dg, full);
+            tma_load_3d(base + GND * A_TILE + dg * B_TILE, &bmap, kx, tile.y * GN, dg, full);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % GSTAGES;
-        mbar_wait(su32(&bars[st]), (uint32_t)((kb / GSTAGES) & 1));
+      int g = 0, it = 0;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        int2 tile;
+        int64_t k0;
+        const int nkb = item_nkb(w, tile, k0);
+        if (it > 0) mbar_wait(su32(&bars[2 * GSTAGES + 1]), (uint32_t)((it - 1) & 1));  // accumulators drained
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        const uint32_t a0 = su32(smem + st * STAGE_BYTES), b0 = a0 + GND * A_TILE;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int st = g % GSTAGES;
+          mbar_wait(su32(&bars[st]), (uint32_t)((g / GSTAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t a0 = su32(smem + st * STAGE_BYTES), b0 = a0 + GND * A_TILE;
 #pragma unroll
-        for (int kk = 0; kk < GBK / 32; ++kk) {
+          for (int kk = 0; kk < GBK / 32; ++kk) {
 #pragma unroll
-          for (int s = 0; s < GND; ++s)
+            for (int s = 0; s < GND; ++s)
 #pragma unroll
-            for (int t = 0; t < GND; ++t) {
-              const int cls = s + t;
-              // first write of accumulator `cls`: the first (s, t) of the class at k = 0
-              const bool first = kb == 0 && kk == 0 && (s == 0 || t == GND - 1);
-              mma_i8(tmem + (uint32_t)(cls * GN), desc_sw64(a0 + s * A_TILE + kk * 32),
-                     desc_sw64(b0 + t * B_TILE + kk * 32), idesc_i8(s > 0, t > 0), first ? 0u : 1u);
-            }
+              for (int t = 0; t < GND; ++t) {
+                const int cls = s + t;
+                // first write of accumulator `cls`: the first (s, t) of the class at k = 0
+                const bool first = kb == 0 && kk == 0 && (s == 0 || t == GND - 1);
+                mma_i8(tmem + (uint32_t)(cls * GN), desc_sw64(a0 + s * A_TILE + kk * 32),
+                       desc_sw64(b0 + t * B_TILE + kk * 32), idesc_i8(s > 0, t > 0), first ? 0u : 1u);
+              }
+          }
+          mma_commit(su32(&bars[GSTAGES + st]));  // stage free once these MMAs complete
         }
-        mma_commit(su32(&bars[GSTAGES + st]));  // stage free once these MMAs complete
+        mma_commit(su32(&bars[2 * GSTAGES]));  // this item's accumulators final
       }
-      mma_commit(su32(&bars[2 * GSTAGES]));  // all accumulators final
     }
   } else {  // ---------------- epilogue: warps 2-5 ----------------
     const int q = warp & 3;  // TMEM lane quarter of this warp
     const int row = 32 * q + lane;
-    mbar_wait(su32(&bars[2 * GSTAGES]), 0u);
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    double* out = ws + ((int64_t)blockIdx.y * ntiles + blockIdx.x) * (int64_t)(GN * GM);
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    int it = 0;
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+      int2 tile;
+      int64_t k0;
+      const int nkb = item_nkb(w, tile, k0);
+      mbar_wait(su32(&bars[2 * GSTAGES]), (uint32_t)(it & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      double* out = ws + (int64_t)w * (int64_t)(GN * GM);
 #pragma unroll 1
-    for (int c0 = 0; c0 < GN; c0 += 16) {
-      uint32_t v[GCLS][16];
+      for (int c0 = 0; c0 < GN; c0 += 16) {
+        uint32_t v[GCLS][16];
 #pragma unroll
-      for (int k = 0; k < GCLS; ++k) tmem_ld16(tl + (uint32_t)(k * GN + c0), v[k]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        for (int k = 0; k < GCLS; ++k) tmem_ld16(tl + (uint32_t)(k * GN + c0), v[k]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        // G = sum_k A_k 2^-(7k + 14), smallest terms first
-        double g = (double)(int)v[GCLS - 1][j];
+        for (int j = 0; j < 16; ++j) {
+          // G = sum_k A_k 2^-(7k + 14), smallest terms first
+          double g = (double)(int)v[GCLS - 1][j];
 #pragma unroll
-        for (int k = GCLS - 2; k >= 0; --k) g = g * 0.0078125 + (double)(int)v[k][j];
-        out[(int64_t)(c0 + j) * GM + row] = nkb > 0 ? g * 6.103515625e-05 : 0.0;
+          for (int k = GCLS - 2; k >= 0; --k) g = g * 0.0078125 + (double)(int)v[k][j];
+          out[(int64_t)(c0 + j) * GM + row] = nkb > 0 ? g * 6.103515625e-05 : 0.0;
+        }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      mbar_arrive(su32(&bars[2 * GSTAGES + 1]));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -350,6 +382,241 @@ void plane_map(CUtensorMap* m, const int8_t* planes, int64_t n, int64_t s, int64
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8 digit planes) failed: " + std::to_string((int)r));
 }
 
+
+// ---------------------------------------------------------------------------
+// Kernel columns on the tensor cores: D = X X_S' (K = d <= 64) with the 3xTF32
+// split (x = hi + lo, both tf32; D = Xh Sh' + Xh Sl' + Xl Sh' accumulated in
+// fp32 TMEM, ~2^-22 relative per product, the accuracy of an fp32 dot), then
+// the RBF epilogue exp((D - 0.5 (|x_i|^2 + |s_j|^2)) / sigma^2) straight into
+// the int8 digit planes. C is never stored in fp32.
+//
+// Persistent CTA = one 128-landmark column block (B hi/lo resident in shared
+// memory) x a strided list of 128-row tiles; A hi/lo double-buffered by TMA
+// (SWIZZLE_128B, two 32-column halves per operand); two TMEM accumulators so
+// the epilogue of tile t overlaps the MMAs of tile t + 1. Warp 0 = TMA, warp 1
+// = MMA, warps 2-9 = epilogue (two warps per TMEM lane quarter, 64 columns each).
+constexpr int RT_M = 128, RT_N = 128, RT_K = 64;
+constexpr int RT_HALF = RT_M * 128;                  // one 128-row x 32-fp32 SW128 box (16 KB)
+constexpr int RT_A_BYTES = 4 * RT_HALF;              // hi/lo x two k halves (64 KB)
+constexpr int RT_B_BYTES = 4 * RT_HALF;              // 128 landmarks (64 KB)
+constexpr int RT_EPI_WARPS = 16;
+constexpr int RT_XBUF = RT_EPI_WARPS * 3 * 16 * 32;  // per-warp digit transpose buffers
+constexpr int RT_SMEM = RT_B_BYTES + 2 * RT_A_BYTES + 1024 + 2048 + RT_XBUF;
+constexpr int RT_THREADS = 32 * (2 + RT_EPI_WARPS);
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// kind::tf32: D f32, A/B tf32, K-major, M = 128, N = RT_N.
+constexpr uint32_t IDESC_TF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(RT_N >> 3) << 17) |
+                                ((uint32_t)(RT_M >> 4) << 24);
+
+__global__ void tf32_split_kernel(int64_t n, int64_t d, const float* __restrict__ x, int64_t rs, int64_t cs,
+                                  float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d, k = e % d;
+    const float v = x[i * rs + k * cs];
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    const float r = v - __uint_as_float(h);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+    hi[e] = __uint_as_float(h);
+    lo[e] = __uint_as_float(l);
+  }
+}
+
+__global__ void __launch_bounds__(RT_THREADS, 1)
+    rbf_tc_digits_kernel(const __grid_constant__ CUtensorMap xh, const __grid_constant__ CUtensorMap xl,
+                         const __grid_constant__ CUtensorMap sh, const __grid_constant__ CUtensorMap sl, int64_t n,
+                         int64_t s, const float* __restrict__ sqx, const float* __restrict__ sqy, float inv,
+                         const int64_t* __restrict__ diag_of, int8_t* __restrict__ planes, int64_t pitch,
+                         int64_t plane_stride, int ncb, int nrg) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* bsm = smem;
+  uint8_t* asm_ = smem + RT_B_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RT_B_BYTES + 2 * RT_A_BYTES);
+  // bars: [0,1] a_full, [2,3] a_empty, [4,5] t_full, [6,7] t_empty, [8] b_full
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  float* sq_s = reinterpret_cast<float*>(bars + 10);          // [RT_N]
+  int64_t* dg_s = reinterpret_cast<int64_t*>(sq_s + RT_N);     // [RT_N]
+  uint8_t* xbuf = smem + RT_B_BYTES + 2 * RT_A_BYTES + 2048;   // [RT_EPI_WARPS][3][16][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cb = blockIdx.x % ncb, rg = blockIdx.x / ncb;
+  const int64_t j0 = (int64_t)cb * RT_N;
+  const int ntile = (int)((n + RT_M - 1) / RT_M);
+  const int my_tiles = rg < ntile ? (ntile - 1 - rg) / nrg + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(su32(&bars[0 + b]), 1);
+      mbar_init(su32(&bars[2 + b]), 1);
+      mbar_init(su32(&bars[4 + b]), 1);
+      mbar_init(su32(&bars[6 + b]), 32 * RT_EPI_WARPS);
+    }
+    mbar_init(su32(&bars[8]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int c = threadIdx.x; c < RT_N; c += RT_THREADS) {
+    const int64_t j = j0 + c;
+    sq_s[c] = j < s ? sqy[j] : 0.f;
+    dg_s[c] = j < s && diag_of ? diag_of[j] : -1;
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      const uint32_t bb = su32(&bars[8]);
+      mbar_expect_tx(bb, RT_B_BYTES);
+      const uint32_t b0 = su32(bsm);
+      tma_load_2d(b0 + 0 * RT_HALF, &sh, 0, (int)j0, bb);
+      tma_load_2d(b0 + 1 * RT_HALF, &sh, 32, (int)j0, bb);
+      tma_load_2d(b0 + 2 * RT_HALF, &sl, 0, (int)j0, bb);
+      tma_load_2d(b0 + 3 * RT_HALF, &sl, 32, (int)j0, bb);
+      for (int t = 0; t < my_tiles; ++t) {
+        const int buf = t & 1;
+        if (t >= 2) mbar_wait(su32(&bars[2 + buf]), (uint32_t)(((t >> 1) - 1) & 1));
+        const uint32_t full = su32(&bars[buf]);
+        mbar_expect_tx(full, RT_A_BYTES);
+        const uint32_t a0 = su32(asm_ + buf * RT_A_BYTES);
+        const int i0 = (rg + t * nrg) * RT_M;
+        tma_load_2d(a0 + 0 * RT_HALF, &xh, 0, i0, full);
+        tma_load_2d(a0 + 1 * RT_HALF, &xh, 32, i0, full);
+        tma_load_2d(a0 + 2 * RT_HALF, &xl, 0, i0, full);
+        tma_load_2d(a0 + 3 * RT_HALF, &xl, 32, i0, full);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      mbar_wait(su32(&bars[8]), 0u);
+      const uint32_t b0 = su32(bsm);
+      for (int t = 0; t < my_tiles; ++t) {
+        const int buf = t & 1;
+        mbar_wait(su32(&bars[buf]), (uint32_t)((t >> 1) & 1));
+        if (t >= 2) mbar_wait(su32(&bars[6 + buf]), (uint32_t)(((t >> 1) - 1) & 1));  // accumulator drained
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t a0 = su32(asm_ + buf * RT_A_BYTES), d = tmem + (uint32_t)(buf * RT_N);
+#pragma unroll
+        for (int kk = 0; kk < RT_K / 8; ++kk) {
+          const uint32_t off = (uint32_t)((kk >> 2) * RT_HALF + (kk & 3) * 32);
+          const uint64_t ah = desc_sw128(a0 + off), al = desc_sw128(a0 + 2 * RT_HALF + off);
+          const uint64_t bh = desc_sw128(b0 + off), bl = desc_sw128(b0 + 2 * RT_HALF + off);
+          mma_tf32(d, ah, bh, IDESC_TF32, kk > 0 ? 1u : 0u);
+          mma_tf32(d, ah, bl, IDESC_TF32, 1u);
+          mma_tf32(d, al, bh, IDESC_TF32, 1u);
+        }
+        mma_commit(su32(&bars[2 + buf]));  // A buffer free
+        mma_commit(su32(&bars[4 + buf]));  // accumulator ready
+      }
+    }
+  } else {  // ---------------- epilogue: warps 2-17 ----------------
+    // warp w: TMEM lane quarter w & 3 (rows 32q .. 32q + 31), columns
+    // 32 * part .. + 31. Digits go through a per-warp shared buffer so the
+    // stores are 4-byte words of consecutive rows (one 32-B sector per column).
+    const int q = warp & 3, part = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
+    uint8_t* tb = xbuf + (warp - 2) * (3 * 16 * 32);  // [digit][16 columns][32 rows]
+    for (int t = 0; t < my_tiles; ++t) {
+      const int buf = t & 1;
+      const int64_t ibase = (int64_t)(rg + t * nrg) * RT_M + 32 * q;
+      const int64_t i = ibase + lane;
+      mbar_wait(su32(&bars[4 + buf]), (uint32_t)((t >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const float sxi = i < n ? sqx[i] : 0.f;
+      const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * RT_N + part * 32);
+      uint32_t v[2][16];
+      tmem_ld16(tl, v[0]);
+      tmem_ld16(tl + 16u, v[1]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      mbar_arrive(su32(&bars[6 + buf]));  // accumulator drained by this thread
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c = part * 32 + h * 16 + jj;
+          const float x = dg_s[c] == i ? 1.f : exp2f((__uint_as_float(v[h][jj]) - 0.5f * (sxi + sq_s[c])) * inv);
+          int m0, m1, m2;
+          digits3(x, m0, m1, m2);
+          tb[(0 * 16 + jj) * 32 + lane] = (uint8_t)m0;
+          tb[(1 * 16 + jj) * 32 + lane] = (uint8_t)(int8_t)m1;
+          tb[(2 * 16 + jj) * 32 + lane] = (uint8_t)(int8_t)m2;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+          const int w = lane + 32 * u;
+          const int dgt = w >> 7, c = (w >> 3) & 15, wi = w & 7;
+          const int64_t j = j0 + part * 32 + h * 16 + c;
+          const int64_t r0 = ibase + 4 * wi;
+          if (j < s && r0 < n) {
+            int8_t* dst = planes + dgt * plane_stride + j * pitch + r0;
+            const uint8_t* src = tb + (dgt * 16 + c) * 32 + 4 * wi;
+            if (r0 + 4 <= n) {
+              *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(src);
+            } else {
+              for (int b = 0; r0 + b < n; ++b) dst[b] = (int8_t)src[b];
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+  }
+}
+
+// W[a, b] = dequantized digits of C at (row dsel[a], column b) for the
+// landmarks this rank owns (dsel[a] >= 0), zero otherwise.
+__global__ void w_from_digits_kernel(int64_t s, const int64_t* __restrict__ dsel, const int8_t* __restrict__ planes,
+                                     int64_t pitch, int64_t plane_stride, double* __restrict__ W) {
+  const int64_t total = s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e % s, b = e / s;
+    const int64_t r = dsel[a];
+    double v = 0.0;
+    if (r >= 0) {
+      const int8_t* p = planes + b * pitch + r;
+      v = dequant3((int)(uint8_t)p[0], (int)p[plane_stride], (int)p[2 * plane_stride]);
+    }
+    W[a + b * s] = v;
+  }
+}
 }  // namespace
 
 bool gram_i8_available() {
@@ -371,7 +638,8 @@ void rbf_digits(rnla_ctx* ctx, int64_t n1, int64_t n2, int64_t d, const float* X
   note_launch(ctx);
 }
 
-void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t pitch, double* G, bool accumulate) {
+void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t pitch, double* G, bool accumulate,
+             int reserve_sms) {
   if (s == 0) return;
   const int nib = (int)((s + GM - 1) / GM), njb = (int)((s + GN - 1) / GN);
   std::vector<int2> tl;
@@ -383,15 +651,16 @@ void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t 
         tl.push_back(make_int2(ib, jb));
       }
   const int ntiles = (int)tl.size();
-  // K chunks: at most KCHUNK rows each (s32 range), as many as fill whole
-  // waves of one CTA per SM best (the chunk index is the slow grid index, so
-  // the CTAs resident together share one chunk of the digit planes in L2)
+  const int ctas_max = std::max(1, ctx->num_sms - std::max(0, reserve_sms));
+  // K chunks: at most KCHUNK rows each (s32 range); enough work items to
+  // balance the persistent CTAs (chunk is the slow index, so the CTAs running
+  // together share one chunk of the digit planes in L2)
   const int cmin = (int)std::max<int64_t>(1, (n + KCHUNK - 1) / KCHUNK);
   int nchunks = cmin;
   double best = 1e300;
   for (int c = cmin; c <= std::max(cmin, 64); ++c) {
-    const double waves = std::ceil((double)ntiles * c / ctx->num_sms);
-    const double cost = waves / c + 0.002 * c;  // per-chunk epilogue + reduce overhead
+    const double rounds = std::ceil((double)ntiles * c / ctas_max);
+    const double cost = rounds / c + 0.002 * c;  // per-item epilogue + reduce overhead
     if (cost < best - 1e-12) {
       best = cost;
       nchunks = c;
@@ -399,8 +668,9 @@ void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t 
   }
   const int64_t kc = std::max<int64_t>(GBK, ((n + nchunks - 1) / nchunks + GBK - 1) / GBK * GBK);
   nchunks = (int)std::max<int64_t>(1, (n + kc - 1) / kc);
+  const int nitems = ntiles * nchunks;
   DevBuf dtl(sizeof(int2) * tl.size(), ctx->stream), dto(sizeof(int) * tile_of.size(), ctx->stream);
-  DevBuf ws(sizeof(double) * (size_t)nchunks * ntiles * GM * GN, ctx->stream);
+  DevBuf ws(sizeof(double) * (size_t)nitems * GM * GN, ctx->stream);
   RNLA_CUDA(cudaMemcpyAsync(dtl.p, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, ctx->stream));
   RNLA_CUDA(cudaMemcpyAsync(dto.p, tile_of.data(), sizeof(int) * tile_of.size(), cudaMemcpyHostToDevice, ctx->stream));
   if (n > 0) {
@@ -408,8 +678,8 @@ void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t 
     plane_map(&amap, planes, n, s, pitch, GM);
     plane_map(&bmap, planes, n, s, pitch, GN);
     ensure_dyn_smem((const void*)gram_i8_kernel, GRAM_SMEM);
-    gram_i8_kernel<<<dim3((unsigned)ntiles, (unsigned)nchunks), GRAM_THREADS, GRAM_SMEM, ctx->stream>>>(
-        amap, bmap, dtl.as<int2>(), ntiles, n, kc, ws.as<double>());
+    gram_i8_kernel<<<std::min(nitems, ctas_max), GRAM_THREADS, GRAM_SMEM, ctx->stream>>>(
+        amap, bmap, dtl.as<int2>(), ntiles, nitems, n, kc, ws.as<double>());
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
   } else {
@@ -420,6 +690,70 @@ void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t 
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
   RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // tl / tile_of leave scope
+}
+
+bool rbf_tc_available(int64_t d) { return d >= 1 && d <= RT_K && encode() != nullptr && tc_gemm_enabled(); }
+
+void rbf_tc_digits(rnla_ctx* ctx, int64_t n, int64_t s, int64_t d, const float* X, int64_t x_rs, int64_t x_cs,
+                   const float* Xs, int64_t s_rs, int64_t s_cs, const float* sqx, const float* sqy, double sigma,
+                   const int64_t* diag_of, int8_t* planes, int64_t pitch, int64_t plane_stride, int reserve_sms) {
+  if (n == 0 || s == 0) return;
+  require(d >= 1 && d <= RT_K, "rbf_tc_digits: d > 64");
+  // tf32 hi/lo images, row-major n x d (16-B aligned rows: d padded to 4)
+  const int64_t ld = (d + 3) / 4 * 4;
+  DevBuf xh(sizeof(float) * n * ld, ctx->stream), xl(sizeof(float) * n * ld, ctx->stream),
+      shb(sizeof(float) * s * ld, ctx->stream), slb(sizeof(float) * s * ld, ctx->stream);
+  auto split = [&](int64_t rows, const float* src, int64_t rs, int64_t cs, float* hi, float* lo) {
+    if (ld != d) {
+      RNLA_CUDA(cudaMemsetAsync(hi, 0, sizeof(float) * rows * ld, ctx->stream));
+      RNLA_CUDA(cudaMemsetAsync(lo, 0, sizeof(float) * rows * ld, ctx->stream));
+    }
+    // split into a dense n x d image, then widen the pitch if needed
+    tf32_split_kernel<<<grid_for(ctx, rows * d, 256), 256, 0, ctx->stream>>>(rows, d, src, rs, cs, hi, lo);
+    RNLA_CUDA(cudaGetLastError());
+    note_launch(ctx);
+    if (ld != d) {
+      RNLA_CUDA(cudaMemcpy2DAsync(hi, sizeof(float) * ld, hi, sizeof(float) * d, sizeof(float) * d, rows,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+      RNLA_CUDA(cudaMemcpy2DAsync(lo, sizeof(float) * ld, lo, sizeof(float) * d, sizeof(float) * d, rows,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  };
+  split(n, X, x_rs, x_cs, xh.as<float>(), xl.as<float>());
+  split(s, Xs, s_rs, s_cs, shb.as<float>(), slb.as<float>());
+  auto map = [&](CUtensorMap* m, const float* base, int64_t rows) {
+    const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {32, (cuuint32_t)RT_M};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (tf32 images) failed: " + std::to_string((int)r));
+  };
+  CUtensorMap mxh, mxl, msh, msl;
+  map(&mxh, xh.as<float>(), n);
+  map(&mxl, xl.as<float>(), n);
+  map(&msh, shb.as<float>(), s);
+  map(&msl, slb.as<float>(), s);
+  const int ncb = (int)((s + RT_N - 1) / RT_N);
+  const int ntile = (int)((n + RT_M - 1) / RT_M);
+  const int nrg = std::max(1, std::min(ntile, std::max(1, ctx->num_sms - std::max(0, reserve_sms)) / ncb));
+  ensure_dyn_smem((const void*)rbf_tc_digits_kernel, RT_SMEM);
+  rbf_tc_digits_kernel<<<ncb * nrg, RT_THREADS, RT_SMEM, ctx->stream>>>(
+      mxh, mxl, msh, msl, n, s, sqx, sqy, (float)(1.4426950408889634 / (sigma * sigma)), diag_of, planes, pitch,
+      plane_stride, ncb, nrg);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));  // the tf32 images leave scope
+}
+
+void w_from_digits(rnla_ctx* ctx, int64_t s, const int64_t* dsel, const int8_t* planes, int64_t pitch,
+                   int64_t plane_stride, double* W) {
+  if (s == 0) return;
+  w_from_digits_kernel<<<grid_for(ctx, s * s, 256), 256, 0, ctx->stream>>>(s, dsel, planes, pitch, plane_stride, W);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
 }
 
 }  // namespace rnla

@@ -58,6 +58,10 @@ void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv);
 
 // Symmetric eigen-decomposition of column-major A (n x n): A <- eigenvectors, W ascending.
 void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W);
+// Symmetric b x b H (b <= 256) by cuSOLVER syevj: lam[b] descending and Z
+// (b x b, column-major) the matching orthonormal eigenvectors; H is not
+// modified. False when b is out of range (the caller falls back to eig_sym).
+bool eig_sym_small_desc(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z);
 // The k largest eigenpairs only (syevdx, index range): W[0..k) ascending, their
 // eigenvectors in the first k columns of A. Returns the number found.
 int64_t eig_sym_top(rnla_ctx* ctx, int64_t n, double* A, int64_t k, double* W);

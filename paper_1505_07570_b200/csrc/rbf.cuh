@@ -47,5 +47,17 @@ void rbf_digits(rnla_ctx* ctx, int64_t n1, int64_t n2, int64_t d, const float* X
                 const int64_t* diag_of, int8_t* planes, int64_t pitch, int64_t plane_stride, double* w, int64_t ldw);
 // G (s x s col-major fp64; += when accumulate) = exact Gram of the digit
 // planes of an n x s matrix (plane d of column p at planes + d s pitch + p pitch).
-void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t pitch, double* G, bool accumulate);
+// reserve_sms SMs are left free (for concurrent work on another stream).
+void gram_i8(rnla_ctx* ctx, const int8_t* planes, int64_t n, int64_t s, int64_t pitch, double* G, bool accumulate,
+             int reserve_sms = 0);
+// The digit planes of K(X, X_S) from a tcgen05 3xTF32 X X_S' (d <= 64) with the
+// RBF epilogue in registers (rows i < n of the block; diag_of[j] == i -> 1).
+bool rbf_tc_available(int64_t d);
+void rbf_tc_digits(rnla_ctx* ctx, int64_t n, int64_t s, int64_t d, const float* X, int64_t x_rs, int64_t x_cs,
+                   const float* Xs, int64_t s_rs, int64_t s_cs, const float* sqx, const float* sqy, double sigma,
+                   const int64_t* diag_of, int8_t* planes, int64_t pitch, int64_t plane_stride,
+                   int reserve_sms = 0);
+// W[a, b] = dequantized digits at (row dsel[a], column b), 0 where dsel[a] < 0.
+void w_from_digits(rnla_ctx* ctx, int64_t s, const int64_t* dsel, const int8_t* planes, int64_t pitch,
+                   int64_t plane_stride, double* W);
 }  // namespace rnla
