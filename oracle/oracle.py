@@ -15,7 +15,10 @@ Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this
 module. The product library never calls it.
 
 Parity status: RNG streams, hashes, count sketch (bit-exact sequential
-order) and FWHT are pinned by golden vectors / known answers; the power
+order), SRHT and FWHT are pinned by golden vectors / known answers AND by
+fixtures the reference's own src/rng.cpp + src/sketch.cpp produced when
+compiled here unmodified against oracle/ref_shim (tests/golden/
+ref_fixtures.json, tests/test_ref_fixtures.py); the power
 iteration extension (configs 0/3) is parity-unpinned by reference tests
 (the reference has no power iteration, src/randsvd.cpp:88-110).
 """
@@ -83,6 +86,63 @@ def mt64_stream(seed: int, count: int) -> list:
     L.orc_mt_next.argtypes = [C.POINTER(MT64)]
     L.orc_mt_seed(C.byref(g), seed)
     return [int(L.orc_mt_next(C.byref(g))) for _ in range(count)]
+
+
+class _Normal(C.Structure):
+    _fields_ = [("saved", C.c_double), ("has_saved", C.c_int)]
+
+
+class Engine:
+    """A std::mt19937_64 whose state carries over between draws, for
+    restating reference call sequences on one Rng (src/rng.cpp:8-65)."""
+
+    def __init__(self, seed: int):
+        L = lib()
+        L.orc_mt_seed.argtypes = [C.POINTER(MT64), C.c_uint64]
+        L.orc_mt_next.argtypes = [C.POINTER(MT64)]
+        L.orc_normal_next.argtypes = [C.POINTER(_Normal), C.POINTER(MT64)]
+        L.orc_normal_next.restype = C.c_double
+        L.orc_uniform_real.argtypes = [C.POINTER(MT64), C.c_double, C.c_double]
+        L.orc_uniform_real.restype = C.c_double
+        L.orc_sample_without_replacement_g.argtypes = [C.POINTER(MT64), C.c_int64, C.c_int64, _I64P]
+        self.g = MT64()
+        L.orc_mt_seed(C.byref(self.g), seed)
+
+    def gaussian_matrix(self, rows: int, cols: int) -> np.ndarray:
+        nd = _Normal(0.0, 0)  # a fresh normal_distribution per call (rng.cpp:9)
+        out = np.empty((rows, cols), order="F")
+        for j in range(cols):
+            for i in range(rows):
+                out[i, j] = lib().orc_normal_next(C.byref(nd), C.byref(self.g))
+        return out
+
+    def gaussian_unit_vector(self, dim: int) -> np.ndarray:
+        nd = _Normal(0.0, 0)
+        while True:
+            v = np.array([lib().orc_normal_next(C.byref(nd), C.byref(self.g)) for _ in range(dim)])
+            n2 = 0.0
+            for x in v:
+                n2 += x * x
+            if n2 != 0.0:
+                return v / math.sqrt(n2)
+
+    def sample_without_replacement(self, n: int, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.int64)
+        lib().orc_sample_without_replacement_g(C.byref(self.g), n, count, _p(out, _I64P))
+        return out
+
+    def sample_with_replacement(self, weights, count: int) -> np.ndarray:
+        w = np.asarray(weights, dtype=np.float64)
+        cum = np.empty_like(w)
+        total = 0.0
+        for i, x in enumerate(w):  # sequential fp64 prefix sums (rng.cpp:46-52)
+            total += float(x)
+            cum[i] = total
+        out = np.empty(count, dtype=np.int64)
+        for t in range(count):
+            u = lib().orc_uniform_real(C.byref(self.g), 0.0, total)
+            out[t] = min(int(np.searchsorted(cum, u, side="right")), w.size - 1)
+        return out
 
 
 def _p(a, t=_F64P):
