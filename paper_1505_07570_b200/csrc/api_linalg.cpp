@@ -81,10 +81,19 @@ SvdDev topk_svd_wide(rnla_ctx* ctx, int64_t s, int64_t n, const double* B, int64
   if (s > 512 || k < 1 || std::getenv("RNLA_SVD_NO_GRAM")) return condensed_svd_dev(ctx, s, n, B, 1, s);
   DevBuf G(sizeof(double) * s * s, ctx->stream), lam(sizeof(double) * s, ctx->stream);
   gemm<double>(ctx, s, s, n, 1.0, B, 1, s, B, s, 1, 0.0, G.as<double>(), 1, s);
-  eig_sym(ctx, s, G.as<double>(), lam.as<double>());
   std::vector<double> h((size_t)s);
-  RNLA_CUDA(cudaMemcpyAsync(h.data(), lam.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
-  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  DevBuf Zd(sizeof(double) * s * s, ctx->stream);
+  if (s <= 32 && eig_sym_small_desc(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>())) {
+    // one-kernel batched Jacobi; back to the ascending layout used below
+    copy2d<double>(ctx, s, s, Zd.as<double>() + (s - 1) * s, 1, -s, G.as<double>(), 1, s);
+    RNLA_CUDA(cudaMemcpyAsync(h.data(), lam.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::reverse(h.begin(), h.end());
+  } else {
+    eig_sym(ctx, s, G.as<double>(), lam.as<double>());
+    RNLA_CUDA(cudaMemcpyAsync(h.data(), lam.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   const double l1 = h[(size_t)s - 1], lk = h[(size_t)(s - k)];
   if (!(l1 > 0.0) || !(lk > 1e-6 * l1)) return condensed_svd_dev(ctx, s, n, B, 1, s);
   SvdDev f;
@@ -151,6 +160,36 @@ struct KsvdWork {
     }
     if (rows >= 4 * cols && cholqr2_fast(ctx, rows, cols, Y)) return;
     householder(ctx, rows, cols, Y);
+  }
+
+  // Intermediate orthonormalization of the power iteration (only
+  // span(Q) matters there, not its sign convention or last-bit
+  // orthonormality): ONE CholeskyQR pass, |Q'Q - I| ~ kappa(Y)^2 u (config 3:
+  // kappa <= 19 per step, SURVEY hard part 7), with the full orth as the
+  // breakdown fallback. The final Q before B = Q'A always takes the full orth.
+  static void orth_light(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y, bool sharded) {
+    if (sharded || rows < 4 * cols) return orth(ctx, rows, cols, Y, sharded);
+    constexpr bool f64 = std::is_same<T, double>::value;
+    DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream);
+    DevBuf st(sizeof(int), ctx->stream), tmp(sizeof(T) * rows * cols, ctx->stream), Rt;
+    if constexpr (!f64) Rt = DevBuf(sizeof(float) * cols * cols, ctx->stream);
+    float* rt = f64 ? nullptr : Rt.as<float>();
+    RNLA_CUDA(cudaMemsetAsync(st.p, 0, sizeof(int), ctx->stream));
+    gram(ctx, rows, cols, Y, G.as<double>());
+    const double thresh = f64 ? 1e-5 : 1e-2;
+    if (cols <= kSmallCholMax)
+      small_chol_inv<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, nullptr, rows, thresh, st.as<int>());
+    else
+      chol_inv_async<T>(ctx, cols, G.as<double>(), Rinv.as<double>(), rt, nullptr, rows, thresh, st.as<int>());
+    if constexpr (f64)
+      gemm<double>(ctx, rows, cols, cols, 1.0, Y, 1, rows, Rinv.as<double>(), 1, cols, 0.0, tmp.as<double>(), 1, rows);
+    else
+      gemm<float>(ctx, rows, cols, cols, 1.f, Y, 1, rows, rt, 1, cols, 0.f, tmp.as<float>(), 1, rows);
+    int hs = 0;
+    RNLA_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hs & 3) return orth(ctx, rows, cols, Y, sharded);  // breakdown: Y untouched
+    RNLA_CUDA(cudaMemcpyAsync(Y, tmp.p, sizeof(T) * rows * cols, cudaMemcpyDeviceToDevice, ctx->stream));
   }
 
   // G = Y'Y (fp64) of a column-major rows x cols Y.
@@ -426,14 +465,14 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   const int dt = std::is_same<T, double>::value ? RNLA_F64 : RNLA_F32;
   DevBuf Z(sizeof(T) * n * s, ctx->stream);
   for (int32_t it = 0; it < q; ++it) {
-    KsvdWork<T>::orth(ctx, m, s, Y.as<T>(), sharded);
+    KsvdWork<T>::orth_light(ctx, m, s, Y.as<T>(), sharded);
     trace_mark(ctx, "ksvd: orth(Y)");
     // Z = orth(A' Q): n x s (a sum over row shards)
     gemm<T>(ctx, n, s, m, T(1), Ap, A.cs, A.rs, Y.as<T>(), 1, m, T(0), Z.as<T>(), 1, n);
     if (sharded) allreduce_sum(ctx, Z.p, (size_t)(n * s), dt);
     ++passes;
     trace_mark(ctx, "ksvd: Z = A' Q");
-    KsvdWork<T>::orth(ctx, n, s, Z.as<T>(), false);
+    KsvdWork<T>::orth_light(ctx, n, s, Z.as<T>(), false);
     trace_mark(ctx, "ksvd: orth(Z)");
     // Y = A Z
     gemm<T>(ctx, m, s, n, T(1), Ap, A.rs, A.cs, Z.as<T>(), 1, n, T(0), Y.as<T>(), 1, m);

@@ -660,13 +660,23 @@ bool eig_sym_small_desc(rnla_ctx* ctx, int64_t b, const double* H, double* lam, 
   DevBuf A(sizeof(double) * b * b, ctx->stream), w(sizeof(double) * b, ctx->stream), info(sizeof(int), ctx->stream);
   RNLA_CUDA(cudaMemcpyAsync(A.p, H, sizeof(double) * b * b, cudaMemcpyDeviceToDevice, ctx->stream));
   int lwork = 0;
-  cusolver_check(cusolverDnDsyevj_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)b, A.as<double>(),
-                                             (int)b, w.as<double>(), &lwork, params),
-                 "syevj_bufferSize");
-  DevBuf work(sizeof(double) * std::max(lwork, 1), ctx->stream);
-  cusolver_check(cusolverDnDsyevj(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)b, A.as<double>(), (int)b,
-                                  w.as<double>(), work.as<double>(), lwork, info.as<int>(), params),
-                 "syevj");
+  if (b <= 32) {  // one-kernel batched Jacobi (n <= 32)
+    cusolver_check(cusolverDnDsyevjBatched_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)b,
+                                                      A.as<double>(), (int)b, w.as<double>(), &lwork, params, 1),
+                   "syevjBatched_bufferSize");
+    DevBuf work(sizeof(double) * std::max(lwork, 1), ctx->stream);
+    cusolver_check(cusolverDnDsyevjBatched(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)b, A.as<double>(),
+                                           (int)b, w.as<double>(), work.as<double>(), lwork, info.as<int>(), params, 1),
+                   "syevjBatched");
+  } else {
+    cusolver_check(cusolverDnDsyevj_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)b,
+                                               A.as<double>(), (int)b, w.as<double>(), &lwork, params),
+                   "syevj_bufferSize");
+    DevBuf work(sizeof(double) * std::max(lwork, 1), ctx->stream);
+    cusolver_check(cusolverDnDsyevj(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)b, A.as<double>(),
+                                    (int)b, w.as<double>(), work.as<double>(), lwork, info.as<int>(), params),
+                   "syevj");
+  }
   note_launch(ctx);
   copy2d<double>(ctx, b, b, A.as<double>() + (b - 1) * b, 1, -b, Z, 1, b);  // descending columns
   copy2d<double>(ctx, b, 1, w.as<double>() + (b - 1), -1, 1, lam, 1, b);
