@@ -111,18 +111,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
       : "r"(taddr));
 }
 
-// Three exact base-128 digits of x (fp32 arithmetic is exact here: power-of-two
-// scalings and differences of nearby values).
+// Three exact balanced base-128 digits of x: N = rint(x 2^21) (one rounding
+// conversion), then integer digit extraction N = m0 2^14 + m1 2^7 + m2 with
+// m1, m2 in [-64, 63] and m0 in [0, 128] for x in [0, 1]. x_q = N 2^-21, so
+// |x - x_q| <= 2^-22; every digit step is exact integer arithmetic (only one
+// quarter-rate conversion per entry).
 __device__ __forceinline__ void digits3(float x, int& m0, int& m1, int& m2) {
   x = fminf(fmaxf(x, 0.f), 1.9921875f);  // RBF entries lie in [0, 1]; guard rounding
-  const float t0 = x * 128.f;
-  const float d0 = rintf(t0);
-  const float t1 = (t0 - d0) * 128.f;
-  const float d1 = rintf(t1);
-  const float t2 = (t1 - d1) * 128.f;
-  m0 = (int)d0;
-  m1 = (int)d1;
-  m2 = (int)rintf(t2);
+  const int N = __float2int_rn(x * 2097152.f);
+  m2 = ((N + 64) & 127) - 64;
+  const int N1 = (N - m2) >> 7;
+  m1 = ((N1 + 64) & 127) - 64;
+  m0 = (N1 - m1) >> 7;
 }
 __device__ __forceinline__ double dequant3(int m0, int m1, int m2) {
   return (double)m0 * 0.0078125 + (double)m1 * 6.103515625e-05 + (double)m2 * 4.76837158203125e-07;
@@ -400,8 +400,7 @@ constexpr int RT_HALF = RT_M * 128;                  // one 128-row x 32-fp32 SW
 constexpr int RT_A_BYTES = 4 * RT_HALF;              // hi/lo x two k halves (64 KB)
 constexpr int RT_B_BYTES = 4 * RT_HALF;              // 128 landmarks (64 KB)
 constexpr int RT_EPI_WARPS = 16;
-constexpr int RT_XBUF = RT_EPI_WARPS * 3 * 16 * 32;  // per-warp digit transpose buffers
-constexpr int RT_SMEM = RT_B_BYTES + 2 * RT_A_BYTES + 1024 + 2048 + RT_XBUF;
+constexpr int RT_SMEM = RT_B_BYTES + 2 * RT_A_BYTES + 1024 + 2048;
 constexpr int RT_THREADS = 32 * (2 + RT_EPI_WARPS);
 
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
@@ -460,9 +459,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RT_B_BYTES + 2 * RT_A_BYTES);
   // bars: [0,1] a_full, [2,3] a_empty, [4,5] t_full, [6,7] t_empty, [8] b_full
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-  float* sq_s = reinterpret_cast<float*>(bars + 10);          // [RT_N]
-  int64_t* dg_s = reinterpret_cast<int64_t*>(sq_s + RT_N);     // [RT_N]
-  uint8_t* xbuf = smem + RT_B_BYTES + 2 * RT_A_BYTES + 2048;   // [RT_EPI_WARPS][3][16][32]
+  float* sq_s = reinterpret_cast<float*>(bars + 16);          // [RT_N], 16-B aligned
+  int* dg_s = reinterpret_cast<int*>(sq_s + RT_N);             // [RT_N]: landmark's local row, -1 if none
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cb = blockIdx.x % ncb, rg = blockIdx.x / ncb;
   const int64_t j0 = (int64_t)cb * RT_N;
@@ -482,7 +480,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   for (int c = threadIdx.x; c < RT_N; c += RT_THREADS) {
     const int64_t j = j0 + c;
     sq_s[c] = j < s ? sqy[j] : 0.f;
-    dg_s[c] = j < s && diag_of ? diag_of[j] : -1;
+    const int64_t dr = j < s && diag_of ? diag_of[j] : -1;
+    dg_s[c] = dr >= 0 && dr < n ? (int)dr : -1;
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
@@ -541,11 +540,14 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     }
   } else {  // ---------------- epilogue: warps 2-17 ----------------
     // warp w: TMEM lane quarter w & 3 (rows 32q .. 32q + 31), columns
-    // 32 * part .. + 31. Digits go through a per-warp shared buffer so the
-    // stores are 4-byte words of consecutive rows (one 32-B sector per column).
+    // 32 * part .. + 31. Each lane computes its row's digits for 16 columns,
+    // packs them 4 columns per word, and a 4-lane byte transpose (shuffles)
+    // turns them into words of 4 consecutive ROWS of one column, stored
+    // straight to the column-major digit planes (one full 32-B sector per
+    // column per 8 lanes).
     const int q = warp & 3, part = (warp - 2) >> 2;
-    const int row = 32 * q + lane;
-    uint8_t* tb = xbuf + (warp - 2) * (3 * 16 * 32);  // [digit][16 columns][32 rows]
+    const int row = 32 * q + lane, sub = lane & 3, g4 = lane >> 2;
+    const uint32_t sel = (uint32_t)sub | ((uint32_t)(4 + sub) << 4);  // byte `sub` of x, byte `sub` of y
     for (int t = 0; t < my_tiles; ++t) {
       const int buf = t & 1;
       const int64_t ibase = (int64_t)(rg + t * nrg) * RT_M + 32 * q;
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       mbar_wait(su32(&bars[4 + buf]), (uint32_t)((t >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       const float sxi = i < n ? sqx[i] : 0.f;
+      const int il = (int)(i < n ? i : -2);
       const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * RT_N + part * 32);
       uint32_t v[2][16];
       tmem_ld16(tl, v[0]);
@@ -560,36 +563,56 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n");
       mbar_arrive(su32(&bars[6 + buf]));  // accumulator drained by this thread
+      if (ibase >= n) continue;           // warp-uniform
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        const int cb = part * 32 + h * 16;
+        float sq[16];
+        int dg[16];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int c = part * 32 + h * 16 + jj;
-          const float x = dg_s[c] == i ? 1.f : exp2f((__uint_as_float(v[h][jj]) - 0.5f * (sxi + sq_s[c])) * inv);
-          int m0, m1, m2;
-          digits3(x, m0, m1, m2);
-          tb[(0 * 16 + jj) * 32 + lane] = (uint8_t)m0;
-          tb[(1 * 16 + jj) * 32 + lane] = (uint8_t)(int8_t)m1;
-          tb[(2 * 16 + jj) * 32 + lane] = (uint8_t)(int8_t)m2;
+        for (int u = 0; u < 4; ++u) {
+          const float4 a4 = *reinterpret_cast<const float4*>(sq_s + cb + 4 * u);
+          const int4 d4 = *reinterpret_cast<const int4*>(dg_s + cb + 4 * u);
+          sq[4 * u] = a4.x; sq[4 * u + 1] = a4.y; sq[4 * u + 2] = a4.z; sq[4 * u + 3] = a4.w;
+          dg[4 * u] = d4.x; dg[4 * u + 1] = d4.y; dg[4 * u + 2] = d4.z; dg[4 * u + 3] = d4.w;
         }
-        __syncwarp();
+        uint32_t w[3][4];
 #pragma unroll
-        for (int u = 0; u < 12; ++u) {
-          const int w = lane + 32 * u;
-          const int dgt = w >> 7, c = (w >> 3) & 15, wi = w & 7;
-          const int64_t j = j0 + part * 32 + h * 16 + c;
-          const int64_t r0 = ibase + 4 * wi;
-          if (j < s && r0 < n) {
-            int8_t* dst = planes + dgt * plane_stride + j * pitch + r0;
-            const uint8_t* src = tb + (dgt * 16 + c) * 32 + 4 * wi;
-            if (r0 + 4 <= n) {
-              *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(src);
-            } else {
-              for (int b = 0; r0 + b < n; ++b) dst[b] = (int8_t)src[b];
-            }
+        for (int u = 0; u < 4; ++u) {
+          w[0][u] = w[1][u] = w[2][u] = 0u;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int jj = 4 * u + b;
+            const float x =
+                dg[jj] == il ? 1.f : exp2f((__uint_as_float(v[h][jj]) - 0.5f * (sxi + sq[jj])) * inv);
+            int m0, m1, m2;
+            digits3(x, m0, m1, m2);
+            w[0][u] |= (uint32_t)(m0 & 0xff) << (8 * b);
+            w[1][u] |= (uint32_t)(m1 & 0xff) << (8 * b);
+            w[2][u] |= (uint32_t)(m2 & 0xff) << (8 * b);
           }
         }
-        __syncwarp();
+#pragma unroll
+        for (int dgt = 0; dgt < 3; ++dgt)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // lane (g4, sub) gathers byte `sub` (column 4u + sub) of rows 4 g4 .. 4 g4 + 3
+            const uint32_t x0 = __shfl_sync(0xffffffffu, w[dgt][u], (lane & ~3) | 0);
+            const uint32_t x1 = __shfl_sync(0xffffffffu, w[dgt][u], (lane & ~3) | 1);
+            const uint32_t x2 = __shfl_sync(0xffffffffu, w[dgt][u], (lane & ~3) | 2);
+            const uint32_t x3 = __shfl_sync(0xffffffffu, w[dgt][u], (lane & ~3) | 3);
+            const uint32_t T = __byte_perm(__byte_perm(x0, x1, sel), __byte_perm(x2, x3, sel), 0x5410);
+            const int64_t j = j0 + cb + 4 * u + sub;
+            const int64_t r0 = ibase + 4 * g4;
+            if (j < s && r0 < n) {
+              int8_t* dst = planes + dgt * plane_stride + j * pitch + r0;
+              if (r0 + 4 <= n) {
+                *reinterpret_cast<uint32_t*>(dst) = T;
+              } else {
+                for (int b = 0; r0 + b < n; ++b) dst[b] = (int8_t)((T >> (8 * b)) & 0xff);
+              }
+            }
+          }
       }
     }
   }
