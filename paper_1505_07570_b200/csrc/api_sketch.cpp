@@ -76,7 +76,6 @@ std::shared_ptr<SrhtPlan> srht_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_
 // at 4096; without split-K: 3.17 ms at 2048, 3.16 ms at 1024).
 static constexpr int64_t kOneGpuKC = 1024;
 static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k) {
-  if (const char* e = std::getenv("RNLA_GAUSS_KC")) return std::max<int64_t>(16, std::atoll(e));
   const int64_t w = std::max(1, ctx->world);
   if (w == 1 && k >= 2 * kOneGpuKC) return kOneGpuKC;
   return std::max<int64_t>(16, (k + w - 1) / w);
@@ -96,10 +95,8 @@ void gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const T* in, int64_t 
   // Chunked stages run each chunk without split-K (one CTA per output tile):
   // under the gather that interferes least (config 1: 3.24 -> 3.16 ms). The
   // standalone and the combined stage chunk identically, so the composition
-  // stays bitwise. RNLA_GAUSS_CHUNK_SPLITS overrides the cap.
-  static const int env_splits =
-      std::getenv("RNLA_GAUSS_CHUNK_SPLITS") ? std::atoi(std::getenv("RNLA_GAUSS_CHUNK_SPLITS")) : 0;
-  const int max_splits = env_splits > 0 ? env_splits : (gauss_kc_for(ctx, n) < n ? 1 : 64);
+  // stays bitwise.
+  const int max_splits = gauss_kc_for(ctx, n) < n ? 1 : 64;
   gemm<T>(ctx, s, L, kc, T(1), g.data.as<T>() + k0, n, 1, in + k0 * ld, ld, 1, first ? T(0) : T(1), out, out_rs,
           out_cs, max_splits);
 }

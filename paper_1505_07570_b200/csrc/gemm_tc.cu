@@ -695,8 +695,7 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
   const size_t smem = STAGES * STAGE + 1024 + 8 * (3 * STAGES + 5);
   auto kern = gemm_bf16x3_kernel<A_KC, BN, STAGES, DF, TMA_A>;
   ensure_dyn_smem((const void*)kern, smem);
-  static const bool n_major_grid_off = std::getenv("RNLA_TC_M_FAST") != nullptr;
-  const bool nfast = nblk > 1 && !n_major_grid_off && (m + TC_BM - 1) / TC_BM <= 65535;
+  const bool nfast = nblk > 1 && (m + TC_BM - 1) / TC_BM <= 65535;
   if (nfast) sym |= 16;
   dim3 grid(nfast ? (unsigned)nblk : (unsigned)((m + TC_BM - 1) / TC_BM),
             nfast ? (unsigned)((m + TC_BM - 1) / TC_BM) : (unsigned)nblk, (unsigned)splits);
@@ -866,9 +865,8 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   CUtensorMap amap;
   const bool tma = make_a_map(&amap, A, m, k, a_rs, a_cs);
   // Gram via the TMA path with 128-wide tiles: B tiles come from the same
-  // tensor map (RNLA_TC_B_IMAGE=1 keeps the pre-split B image).
-  static const bool b_image = std::getenv("RNLA_TC_B_IMAGE") != nullptr;
-  const bool b_from_a = sym && tma && bn_full == TC_BM && !b_image;
+  // tensor map (the pre-split B image measured slower: 8.7 vs 8.1 ms).
+  const bool b_from_a = sym && tma && bn_full == TC_BM;
   const int flags = sym | (tri_b && !sym ? 2 : 0) | (b_from_a ? 8 : 0);
   if (a_cs == 1)
     dispatch_bn<true, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
