@@ -405,6 +405,7 @@ void rnla_ctx_clear_cache(rnla_ctx* ctx) {
   ctx->cs_plans.clear();
   ctx->gauss_ops.clear();
   ctx->srht_plans.clear();
+  ctx->landmark_sel.clear();
   cudaStreamSynchronize(ctx->stream);
 }
 

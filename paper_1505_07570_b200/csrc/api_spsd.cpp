@@ -34,7 +34,13 @@ template <class T>
 Landmarks landmarks(rnla_ctx* ctx, const DevMat& X, int64_t s, uint64_t seed, int64_t n_global, int64_t r_off) {
   Landmarks L;
   const int64_t n = X.rows, d = X.cols;
-  L.sel = sample_without_replacement_host(derive_seed(seed, 1), n_global, s);
+  {  // the landmark draw is an operator: cached per (n, s, seed) like the other random operators
+    auto key = std::make_tuple(n_global, s, seed);
+    auto it = ctx->landmark_sel.find(key);
+    if (it == ctx->landmark_sel.end())
+      it = ctx->landmark_sel.emplace(key, sample_without_replacement_host(derive_seed(seed, 1), n_global, s)).first;
+    L.sel = it->second;
+  }
   L.r_off = r_off;
   std::vector<int64_t> loc(L.sel);
   for (auto& v : loc) v = (v >= r_off && v < r_off + n) ? v - r_off : -1;

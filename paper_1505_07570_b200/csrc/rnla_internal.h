@@ -110,6 +110,8 @@ struct rnla_ctx {
   std::map<std::tuple<int64_t, int64_t, int64_t, uint64_t>, std::unique_ptr<rnla::CountSketchPlan>> cs_plans;
   std::map<std::tuple<int64_t, int64_t, uint64_t, int>, std::unique_ptr<rnla::DenseOperator>> gauss_ops;
   std::map<std::tuple<int64_t, int64_t, uint64_t>, std::shared_ptr<rnla::SrhtPlan>> srht_plans;
+  // Nystrom landmark draws sample_without_replacement(n, s, derive_seed(seed, 1)), keyed by (n, s, seed)
+  std::map<std::tuple<int64_t, int64_t, uint64_t>, std::vector<int64_t>> landmark_sel;
   // Helper context on the same device (own high-priority stream and library
   // handles) for independent work run from a second host thread, e.g. eig(W)
   // under the Nystrom C'C Gram; created lazily by side_ctx().
