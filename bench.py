@@ -382,8 +382,7 @@ def run_gpu(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if os.environ.get("NCCL_DEBUG"):
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout to the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL's own lines stay off stdout (one JSON line)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", world_size=world, rank=rank,
                                 device_id=torch.device("cuda", local))
