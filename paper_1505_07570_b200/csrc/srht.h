@@ -17,7 +17,7 @@ struct SrhtPlan {
   DevBuf out_sign;                 // block plans: (-1)^popcount(block_off & idx_t), fp64[s]
   // One-pass accumulating path (srht_acc.cu), built on first use: per-(tile,
   // row-group) sign bit masks and the packed (high, low) bits of each sample.
-  mutable DevBuf acc_mask, acc_samp;
+  mutable DevBuf acc_mask, acc_samp, acc_slot;  // one-pass SRHT: sign masks, slot -> sample, sample -> slot
   SrhtPlan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_t seed);
   // Plan of one aligned block (2^b rows at block_off, `present` of them real)
   // of a global operator whose sampled indices are idx[0..s).

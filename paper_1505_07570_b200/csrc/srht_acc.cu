@@ -133,19 +133,30 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 // bit 2 of p is set, so the gather's 16-B loads spread over all eight 4-bank
 // groups.
 template <int GS>
-__device__ __forceinline__ int swz(int r) { return r ^ ((r >> 6) & (GS - 1)); }
+__host__ __device__ __forceinline__ int swz(int r) { return r ^ ((r >> 6) & (GS - 1)); }
 
-__device__ __forceinline__ void butterfly64(float* v) {
+// 64-point butterflies on values held as 32 float2 pairs (v[i] = values 2i, 2i+1):
+// stage h = 1 pairs the two halves of one float2 (scalar adds), stages h >= 2
+// pair whole float2s, so they run as packed FADD2 (add.rn.f32x2; the
+// subtraction is x + (-1) * y with one rounding, i.e. exactly x - y).
+__device__ __forceinline__ void butterfly64(float2* v) {
 #pragma unroll
-  for (int h = 1; h < 64; h <<= 1)
+  for (int i = 0; i < 32; ++i) {
+    const float x = v[i].x, y = v[i].y;
+    v[i] = make_float2(x + y, x - y);
+  }
+  const float2 m1 = make_float2(-1.f, -1.f);
 #pragma unroll
-    for (int e = 0; e < 64; ++e)
-      if (!(e & h)) {
-        const float x = v[e], y = v[e + h];
-        v[e] = x + y;
-        v[e + h] = x - y;
+  for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (!(i & h)) {
+        const float2 x = v[i], y = v[i + h];
+        v[i] = __fadd2_rn(x, y);
+        v[i + h] = __ffma2_rn(y, m1, x);
       }
 }
+__device__ __forceinline__ float& vat(float2* v, int e) { return (e & 1) ? v[e >> 1].y : v[e >> 1].x; }
 
 template <int W>
 __global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __grid_constant__ CUtensorMap amap, AccArgs a) {
@@ -212,7 +223,7 @@ __global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __gri
   int cslot = 0;
   uint32_t cpar = 0;
   unsigned long long msk = ntiles > 0 ? a.mask[(size_t)(qt0 & (jhn - 1)) * 64 + g] : 0ull;
-  float v[64];
+  float2 v[32];
   for (int i = 0; i < ntiles; ++i) {
     const int qti = qt0 + i;
     const int q = qti >> a.jh_log, jh = qti & (jhn - 1);
@@ -228,7 +239,7 @@ __global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __gri
       for (int j = 0; j < EPC; ++j) {
         const int e = EPC * kk + j;
         const uint32_t bits = __float_as_uint(src[(g + 64 * j) * W + c]);
-        v[e] = __uint_as_float(bits ^ ((uint32_t)(msk >> e) << 31));
+        vat(v, e) = __uint_as_float(bits ^ ((uint32_t)(msk >> e) << 31));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(su32(&bars[RING + cslot]));
@@ -255,14 +266,14 @@ __global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __gri
       nissue_s = N;
     }
 #pragma unroll
-    for (int e = 0; e < 64; ++e) tile[(64 * e + (g ^ (e & (GS - 1)))) * W + (W == 8 ? (c ^ (g & 4)) : c)] = v[e];
+    for (int e = 0; e < 64; ++e) tile[(64 * e + (g ^ (e & (GS - 1)))) * W + (W == 8 ? (c ^ (g & 4)) : c)] = vat(v, e);
     __syncthreads();  // B
     // ---- phase 2: rows 64a + b (a = g), written back in place ----
 #pragma unroll
-    for (int b = 0; b < 64; ++b) v[b] = tile[(64 * g + (b ^ (g & (GS - 1)))) * W + (W == 8 ? (c ^ (b & 4)) : c)];
+    for (int b = 0; b < 64; ++b) vat(v, b) = tile[(64 * g + (b ^ (g & (GS - 1)))) * W + (W == 8 ? (c ^ (b & 4)) : c)];
     butterfly64(v);
 #pragma unroll
-    for (int b = 0; b < 64; ++b) tile[(64 * g + (b ^ (g & (GS - 1)))) * W + (W == 8 ? (c ^ (b & 4)) : c)] = v[b];
+    for (int b = 0; b < 64; ++b) tile[(64 * g + (b ^ (g & (GS - 1)))) * W + (W == 8 ? (c ^ (b & 4)) : c)] = vat(v, b);
 
     // ---- gather: samples SPT tid .. SPT tid + SPT - 1, all W columns ----
     float acc[64];
@@ -314,20 +325,21 @@ __global__ void __launch_bounds__(Cfg<W>::NT, 8 / W) srht_acc_kernel(const __gri
 }
 
 // out[t][col] = scale * sum of the run partials of col's slice, in run order.
-__global__ void srht_acc_finalize(const float* __restrict__ part, const int32_t* __restrict__ qtab, int maxl,
-                                  int W, int64_t s, int64_t L, float scale, float* __restrict__ out, int64_t out_rs,
-                                  int64_t out_cs) {
+__global__ void srht_acc_finalize(const float* __restrict__ part, const int32_t* __restrict__ qtab,
+                                  const int32_t* __restrict__ slot_of, int maxl, int W, int64_t s, int64_t L,
+                                  float scale, float* __restrict__ out, int64_t out_rs, int64_t out_cs) {
   const int GS = 32 / W;
   const int64_t total = s * L;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / L, col = e - t * L;
     const int64_t q = col >> 5;
     const int r = (int)((col & 31) / W), c = (int)(col % W);
+    const int64_t slot = slot_of[t];
     float acc = 0.f;
     for (int m = 0; m < maxl; ++m) {
       const int ent = qtab[q * maxl + m];
       if (ent < 0) break;
-      acc += part[(((size_t)ent * GS + r) * SMAX + t) * W + c];
+      acc += part[(((size_t)ent * GS + r) * SMAX + slot) * W + c];
     }
     out[t * out_rs + col * out_cs] = acc * scale;
   }
@@ -390,7 +402,8 @@ void srht_acc_launch(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64
   RNLA_CUDA(cudaGetLastError());
   const float scale = (float)(1.0 / std::sqrt((double)plan.s));
   srht_acc_finalize<<<grid_for(ctx, plan.s * L, 256), 256, 0, ctx->stream>>>(
-      part.as<float>(), dq.as<int32_t>(), maxl, W, plan.s, L, scale, out, out_rs, out_cs);
+      part.as<float>(), dq.as<int32_t>(), plan.acc_slot.as<int32_t>(), maxl, W, plan.s, L, scale, out, out_rs,
+      out_cs);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx, 2);
   // qtab was staged by the pageable cudaMemcpyAsync before it returned; the
@@ -413,11 +426,61 @@ bool srht_acc_f32(rnla_ctx* ctx, const SrhtPlan& plan, const float* in, int64_t 
         plan.signs.as<int8_t>(), plan.n, jh_count, plan.acc_mask.as<unsigned long long>());
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
+    // Sample -> accumulator slot. Slot 8 tid + k is read by lane tid % 32 at
+    // gather step k as two 16-B loads of physical tile row p; a quarter warp
+    // (8 lanes) is one smem wavefront when its 8 rows have distinct p mod 8
+    // (the 16-B bank group). Samples are bucketed by p mod 8 and
+    // each (warp, quarter, k) group takes one per bucket while buckets last.
     std::vector<uint32_t> sp(SMAX, 0u);
-    for (int64_t t = 0; t < plan.s; ++t) {
-      const int64_t ix = plan.host_idx[(size_t)t];
-      sp[(size_t)t] = (uint32_t)(ix & (ROWS - 1)) | ((uint32_t)(ix >> LO) << LO);
+    std::vector<int32_t> slot_of((size_t)plan.s, 0);
+    {
+      constexpr int GS8 = Cfg<8>::GS;
+      std::vector<std::vector<int>> bucket(8);
+      for (int64_t t = plan.s - 1; t >= 0; --t) {
+        const int64_t tl = plan.host_idx[(size_t)t] & (ROWS - 1);
+        bucket[(size_t)(swz<GS8>((int)tl) & 7)].push_back((int)t);
+      }
+      const int nt = Cfg<8>::NT, spt = Cfg<8>::SPT;
+      for (int w = 0; w < nt / 32; ++w)
+        for (int qq = 0; qq < 4; ++qq)
+          for (int k = 0; k < spt; ++k) {
+            bool used[8] = {false, false, false, false, false, false, false, false};
+            int lanes[8], nl = 0;
+            auto place = [&](int lane8, int t) {
+              const int slot = spt * (32 * w + 8 * qq + lane8) + k;
+              const int64_t ix = plan.host_idx[(size_t)t];
+              sp[(size_t)slot] = (uint32_t)(ix & (ROWS - 1)) | ((uint32_t)(ix >> LO) << LO);
+              slot_of[(size_t)t] = slot;
+            };
+            for (int b = 0; b < 8; ++b)
+              if (!bucket[(size_t)b].empty()) {
+                place(nl, bucket[(size_t)b].back());
+                bucket[(size_t)b].pop_back();
+                used[b] = true;
+                ++nl;
+              }
+            for (int l = nl; l < 8; ++l) lanes[l - nl] = l;
+            for (int l = 0; l < 8 - nl; ++l) {  // fill from the fullest bucket, else an idle row of a free class
+              int best = -1;
+              for (int b = 0; b < 8; ++b)
+                if (!bucket[(size_t)b].empty() && (best < 0 || bucket[(size_t)b].size() > bucket[(size_t)best].size()))
+                  best = b;
+              if (best >= 0) {
+                place(lanes[l], bucket[(size_t)best].back());
+                bucket[(size_t)best].pop_back();
+              } else {
+                int fc = 0;
+                while (fc < 7 && used[fc]) ++fc;
+                used[fc] = true;
+                const int slot = spt * (32 * w + 8 * qq + lanes[l]) + k;
+                sp[(size_t)slot] = (uint32_t)swz<GS8>(fc);  // tile row of class fc (swz is an involution on it)
+              }
+            }
+          }
     }
+    plan.acc_slot = DevBuf(sizeof(int32_t) * (size_t)plan.s, ctx->stream);
+    RNLA_CUDA(cudaMemcpyAsync(plan.acc_slot.p, slot_of.data(), sizeof(int32_t) * (size_t)plan.s,
+                              cudaMemcpyHostToDevice, ctx->stream));
     plan.acc_samp = DevBuf(sizeof(uint32_t) * SMAX, ctx->stream);
     RNLA_CUDA(cudaMemcpyAsync(plan.acc_samp.p, sp.data(), sizeof(uint32_t) * SMAX, cudaMemcpyHostToDevice,
                               ctx->stream));
