@@ -65,7 +65,7 @@ rnla_status guard(const std::function<void()>& f) {
 
 void trace_mark(rnla_ctx* ctx, const char* label) {
   static const bool on = std::getenv("RNLA_TRACE") != nullptr;
-  if (!on) return;
+  if (!on || ctx->capturing) return;
   static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
   cudaStreamSynchronize(ctx->stream);
   const auto now = std::chrono::steady_clock::now();
@@ -261,6 +261,7 @@ static void ctx_release(rnla_ctx* ctx) {
     ctx_release(ctx->side.get());
     ctx->side.reset();
   }
+  ctx->graphs.clear();
   ctx->cs_plans.clear();
   ctx->gauss_ops.clear();
   ctx->srht_plans.clear();
@@ -402,6 +403,7 @@ void rnla_ctx_clear_cache(rnla_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->graphs.clear();
   ctx->cs_plans.clear();
   ctx->gauss_ops.clear();
   ctx->srht_plans.clear();

@@ -249,6 +249,50 @@ struct KsvdWork {
     return true;
   }
 
+  // Host-round-trip-free variants for the speculative pipeline of
+  // prototype_ksvd_async: every factorization writes its status word to its
+  // own slot and the caller reads all of them once at the end (a breakdown
+  // there reruns the call on the checked path above).
+  static void factor_async(rnla_ctx* ctx, int64_t rows, int64_t cols, double* G, double* Rinv, float* rt, const T* y0,
+                           int* status) {
+    constexpr bool f64 = std::is_same<T, double>::value;
+    const double thresh = f64 ? 1e-5 : 1e-2;
+    if (cols <= kSmallCholMax)
+      small_chol_inv<T>(ctx, cols, G, Rinv, rt, y0, rows, thresh, status);
+    else
+      chol_inv_async<T>(ctx, cols, G, Rinv, rt, y0, rows, thresh, status);
+  }
+  static void apply_rinv(rnla_ctx* ctx, int64_t rows, int64_t cols, const T* X, const double* Rinv, const float* rt,
+                         T* out) {
+    if constexpr (std::is_same<T, double>::value)
+      gemm<double>(ctx, rows, cols, cols, 1.0, X, 1, rows, Rinv, 1, cols, 0.0, out, 1, rows);
+    else
+      gemm<float>(ctx, rows, cols, cols, 1.f, X, 1, rows, rt, 1, cols, 0.f, out, 1, rows);
+  }
+  // one CholeskyQR pass (orth_light semantics): y <- Y R^-1, the result lands in
+  // `spare` and the two pointers swap
+  static void orth1_async(rnla_ctx* ctx, int64_t rows, int64_t cols, T*& y, T*& spare, int* status) {
+    DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream), Rt;
+    if constexpr (!std::is_same<T, double>::value) Rt = DevBuf(sizeof(float) * cols * cols, ctx->stream);
+    gram(ctx, rows, cols, y, G.as<double>());
+    factor_async(ctx, rows, cols, G.as<double>(), Rinv.as<double>(), Rt.as<float>(), nullptr, status);
+    apply_rinv(ctx, rows, cols, y, Rinv.as<double>(), Rt.as<float>(), spare);
+    std::swap(y, spare);
+  }
+  // CholeskyQR2 with the reference's sign rule folded into R2^-1 (orth
+  // semantics): y <- Q in place, `spare` is scratch. status[0], status[1]: the
+  // two factorizations (bit 4 of status[1]: sign undecidable from row 0).
+  static void orth2_async(rnla_ctx* ctx, int64_t rows, int64_t cols, T* y, T* spare, int* status) {
+    DevBuf G(sizeof(double) * cols * cols, ctx->stream), Rinv(sizeof(double) * cols * cols, ctx->stream), Rt;
+    if constexpr (!std::is_same<T, double>::value) Rt = DevBuf(sizeof(float) * cols * cols, ctx->stream);
+    gram(ctx, rows, cols, y, G.as<double>());
+    factor_async(ctx, rows, cols, G.as<double>(), Rinv.as<double>(), Rt.as<float>(), nullptr, status);
+    apply_rinv(ctx, rows, cols, y, Rinv.as<double>(), Rt.as<float>(), spare);
+    gram(ctx, rows, cols, spare, G.as<double>());
+    factor_async(ctx, rows, cols, G.as<double>(), Rinv.as<double>(), Rt.as<float>(), spare, status + 1);
+    apply_rinv(ctx, rows, cols, spare, Rinv.as<double>(), Rt.as<float>(), y);
+  }
+
   static void tsqr(rnla_ctx* ctx, int64_t rows, int64_t cols, T* Y) {
     const int W = ctx->world;
     DevBuf w(sizeof(double) * rows * cols, ctx->stream), r(sizeof(double) * cols * cols, ctx->stream),
@@ -431,6 +475,201 @@ bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, doub
   return false;
 }
 
+// Gram-route core SVD from the eigenpairs of B B' (s x s), lam/Z descending
+// (desc = 1, Jacobi) or ascending (desc = 0, syevd): for the k leading pairs
+// sigma_i = sqrt(lam_i), Ubar(:, i) = z_i and Us(:, i) = z_i / sigma_i.
+// *status = 1 when the route does not apply (lam_1 <= 0 or lam_k <= 1e-6 lam_1,
+// topk_svd_wide's rule).
+static __global__ void gram_svd_post_kernel(int64_t s, int64_t k, int desc, const double* __restrict__ lam,
+                                     const double* __restrict__ Z, double* sigma, double* Ubar, double* Us,
+                                     int* status) {
+  const double l1 = desc ? lam[0] : lam[s - 1], lk = desc ? lam[k - 1] : lam[s - k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *status = (l1 > 0.0 && lk > 1e-6 * l1) ? 0 : 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % s, j = e / s, jj = desc ? j : s - 1 - j;
+    const double sg = sqrt(fmax(lam[jj], 0.0)), z = Z[i + jj * s];
+    Ubar[e] = z;
+    Us[e] = z / sg;
+    if (i == 0) sigma[j] = sg;
+  }
+}
+
+// prototype_ksvd with power iterations as one speculative device pipeline:
+// no host round trip until the end. The orthonormalizations run as in the
+// checked path (one CholeskyQR pass in the power steps, CholeskyQR2 + sign rule
+// for the final Q) and the core SVD takes the Gram route (topk_svd_wide), but
+// their breakdown tests -- Cholesky failure, diagonal ratio, an undecidable
+// sign, the Gram-route condition, eigensolver convergence -- only write status
+// words, read once together with sigma. Any flag returns false and the caller
+// reruns the checked path, so results are identical to it whenever it
+// returns true. Config 0 had six host round trips per call.
+//
+// With the one-CTA Jacobi core (s <= 32) the whole pipeline is captured once
+// per argument signature into a CUDA graph (cached in the context) and
+// replayed: ~35 launches and their stream-ordered allocations become one
+// graph launch. U, V, sigma and the status words land in buffers the graph
+// owns; the per-call work outside it is two copies into the outputs and one
+// device-to-host read.
+struct KsvdAsyncOut {
+  double *U64, *Vd, *sig;
+  int* st;
+  int slots = 0, eig_slot = 0, desc = 1;
+};
+
+template <class T>
+void prototype_ksvd_async_body(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t a_cs, int64_t m, int64_t n,
+                               int64_t kk, int64_t s, const T* omega, int32_t q, KsvdAsyncOut& o) {
+  constexpr bool f64 = std::is_same<T, double>::value;
+  RNLA_CUDA(cudaMemsetAsync(o.st, 0, sizeof(int) * (2 * q + 4), ctx->stream));
+  int slot = 0;
+  DevBuf Y0(sizeof(T) * m * s, ctx->stream), Y1(sizeof(T) * m * s, ctx->stream);
+  DevBuf Z0(sizeof(T) * n * s, ctx->stream), Z1(sizeof(T) * n * s, ctx->stream);
+  T *y = Y0.as<T>(), *ys = Y1.as<T>(), *z = Z0.as<T>(), *zs = Z1.as<T>();
+  gemm<T>(ctx, m, s, n, T(1), Ap, a_rs, a_cs, omega, 1, n, T(0), y, 1, m);
+  trace_mark(ctx, "ksvd (async): Y = A S");
+  for (int32_t it = 0; it < q; ++it) {
+    KsvdWork<T>::orth1_async(ctx, m, s, y, ys, o.st + slot++);
+    gemm<T>(ctx, n, s, m, T(1), Ap, a_cs, a_rs, y, 1, m, T(0), z, 1, n);
+    KsvdWork<T>::orth1_async(ctx, n, s, z, zs, o.st + slot++);
+    gemm<T>(ctx, m, s, n, T(1), Ap, a_rs, a_cs, z, 1, n, T(0), y, 1, m);
+  }
+  trace_mark(ctx, "ksvd (async): power iterations");
+  KsvdWork<T>::orth2_async(ctx, m, s, y, ys, o.st + slot);
+  slot += 2;
+  trace_mark(ctx, "ksvd (async): orth(Y)");
+  // B' = A'Q, stored as B (s x n, column-major)
+  DevBuf B(sizeof(T) * s * n, ctx->stream), B64;
+  gemm<T>(ctx, n, s, m, T(1), Ap, a_cs, a_rs, y, 1, m, T(0), B.as<T>(), s, 1);
+  const double* Bp;
+  if constexpr (f64) {
+    Bp = B.as<double>();
+  } else {
+    B64 = DevBuf(sizeof(double) * s * n, ctx->stream);
+    copy2d_cast<float, double>(ctx, s, n, B.as<float>(), 1, s, B64.as<double>(), 1, s);
+    Bp = B64.as<double>();
+  }
+  trace_mark(ctx, "ksvd (async): B = Q' A");
+  DevBuf G(sizeof(double) * s * s, ctx->stream), lam(sizeof(double) * s, ctx->stream),
+      Zd(sizeof(double) * s * s, ctx->stream);
+  gemm<double>(ctx, s, s, n, 1.0, Bp, 1, s, Bp, s, 1, 0.0, G.as<double>(), 1, s);
+  o.eig_slot = slot++;
+  o.desc = 1;
+  if (!eig_small_jacobi_async(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>(), o.st + o.eig_slot)) {
+    o.desc = 0;
+    RNLA_CUDA(cudaMemcpyAsync(Zd.p, G.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
+    eig_sym_async(ctx, s, Zd.as<double>(), lam.as<double>(), o.st + o.eig_slot);
+  }
+  DevBuf Ub(sizeof(double) * s * kk, ctx->stream), Us(sizeof(double) * s * kk, ctx->stream);
+  gram_svd_post_kernel<<<1, 256, 0, ctx->stream>>>(s, kk, o.desc, lam.as<double>(), Zd.as<double>(), o.sig,
+                                                   Ub.as<double>(), Us.as<double>(), o.st + slot++);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  gemm<double>(ctx, n, kk, s, 1.0, Bp, s, 1, Us.as<double>(), 1, s, 0.0, o.Vd, 1, n);  // V = B' Ubar / sigma
+  fix_column_signs(ctx, s, kk, Ub.as<double>(), 1, s, o.Vd, 1, n, n, /*pair_cols=*/true);
+  trace_mark(ctx, "ksvd (async): small SVD");
+  if constexpr (f64) {
+    gemm<double>(ctx, m, kk, s, 1.0, y, 1, m, Ub.as<double>(), 1, s, 0.0, o.U64, 1, m);
+  } else {
+    DevBuf uf(sizeof(float) * s * kk, ctx->stream), Uf(sizeof(float) * m * kk, ctx->stream);
+    copy2d_cast<double, float>(ctx, s, kk, Ub.as<double>(), 1, s, uf.as<float>(), 1, s);
+    gemm<float>(ctx, m, kk, s, 1.f, y, 1, m, uf.as<float>(), 1, s, 0.f, Uf.as<float>(), 1, m);
+    copy2d_cast<float, double>(ctx, m, kk, Uf.as<float>(), 1, m, o.U64, 1, m);
+  }
+  o.slots = slot;
+}
+
+template <class T>
+bool prototype_ksvd_async(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t a_cs, int64_t m, int64_t n, int64_t k,
+                          int64_t s, uint64_t seed, int32_t q, OutMat& uo, OutMat& vo, double* sv_out,
+                          int64_t* rank_out, int32_t* passes_out) {
+  constexpr bool f64 = std::is_same<T, double>::value;
+  if (m < 4 * s || n < 4 * s || s > 512 || q > 16 || std::getenv("RNLA_KSVD_SYNC")) return false;
+  const int64_t kk = std::min(k, s);
+  const T* omega = gaussian_operator(ctx, n, s, seed, f64 ? RNLA_F64 : RNLA_F32).data.template as<T>();
+  KsvdAsyncOut o{};
+  CachedGraph* cg = nullptr;
+  std::unique_ptr<CachedGraph> own;
+  const bool use_graph = s <= 32 && !std::getenv("RNLA_NO_GRAPH");
+  if (use_graph) {
+    char key[256];
+    std::snprintf(key, sizeof key, "ksvd:%d:%p:%lld:%lld:%lld:%lld:%lld:%lld:%p:%d", f64 ? 64 : 32, (const void*)Ap,
+                  (long long)a_rs, (long long)a_cs, (long long)m, (long long)n, (long long)kk, (long long)s,
+                  (const void*)omega, (int)q);
+    auto it = ctx->graphs.find(key);
+    if (it != ctx->graphs.end()) {
+      cg = it->second.get();
+    } else {
+      own.reset(new CachedGraph());
+      for (size_t bytes : {sizeof(double) * m * kk, sizeof(double) * n * kk, sizeof(double) * kk, sizeof(int) * 64}) {
+        void* p = nullptr;
+        RNLA_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        own->bufs.push_back(p);
+      }
+      KsvdAsyncOut oc{static_cast<double*>(own->bufs[0]), static_cast<double*>(own->bufs[1]),
+                      static_cast<double*>(own->bufs[2]), static_cast<int*>(own->bufs[3])};
+      const int64_t launches0 = ctx->launches;
+      cudaGraph_t graph = nullptr;
+      RNLA_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      ctx->capturing = true;
+      try {
+        prototype_ksvd_async_body<T>(ctx, Ap, a_rs, a_cs, m, n, kk, s, omega, q, oc);
+      } catch (...) {
+        ctx->capturing = false;
+        cudaStreamEndCapture(ctx->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      ctx->capturing = false;
+      RNLA_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      ctx->launches = launches0;
+      const cudaError_t ie = cudaGraphInstantiate(&own->exec, graph, 0);
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++own->kernels;
+      }
+      cudaGraphDestroy(graph);
+      RNLA_CUDA(ie);
+      own->meta = {oc.slots, oc.eig_slot, oc.desc};
+      cg = own.get();
+      ctx->graphs.emplace(key, std::move(own));
+    }
+    o = KsvdAsyncOut{static_cast<double*>(cg->bufs[0]), static_cast<double*>(cg->bufs[1]),
+                     static_cast<double*>(cg->bufs[2]), static_cast<int*>(cg->bufs[3]), (int)cg->meta[0],
+                     (int)cg->meta[1], (int)cg->meta[2]};
+    RNLA_CUDA(cudaGraphLaunch(cg->exec, ctx->stream));
+    note_launch(ctx, cg->kernels);
+  }
+  DevBuf U64, Vd, sig, st;
+  if (!cg) {
+    U64 = DevBuf(sizeof(double) * m * kk, ctx->stream);
+    Vd = DevBuf(sizeof(double) * n * kk, ctx->stream);
+    sig = DevBuf(sizeof(double) * kk, ctx->stream);
+    st = DevBuf(sizeof(int) * 64, ctx->stream);
+    o = KsvdAsyncOut{U64.as<double>(), Vd.as<double>(), sig.as<double>(), st.as<int>()};
+    prototype_ksvd_async_body<T>(ctx, Ap, a_rs, a_cs, m, n, kk, s, omega, q, o);
+  }
+  store_block(ctx, o.U64, m, kk, m, uo);
+  store_block(ctx, o.Vd, n, kk, n, vo);
+  std::vector<int> hs((size_t)o.slots);
+  std::vector<double> hsig((size_t)kk);
+  RNLA_CUDA(cudaMemcpyAsync(hs.data(), o.st, sizeof(int) * o.slots, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaMemcpyAsync(hsig.data(), o.sig, sizeof(double) * kk, cudaMemcpyDeviceToHost, ctx->stream));
+  RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+  trace_mark(ctx, "ksvd (async): U = Q Ubar, stores, status");
+  for (int i = 0; i < o.slots; ++i) {
+    const int v = (i == o.eig_slot && o.desc) ? (hs[(size_t)i] & 255) : hs[(size_t)i];
+    if (v != 0) return false;
+  }
+  for (int64_t i = 0; i < kk; ++i) sv_out[i] = hsig[(size_t)i];
+  *rank_out = kk;
+  *passes_out = 2 + 2 * q;
+  return true;
+}
+
 template <class T>
 void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s, uint64_t seed,
                          const rnla_sketch_spec* spec, int32_t q, const rnla_mat* u_out, double* sv_out,
@@ -449,6 +688,12 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
   require(!sharded || local.kind == RNLA_SKETCH_GAUSSIAN,
           "prototype_ksvd: row-sharded contexts support the Gaussian test matrix");
   require(!sharded || m >= s, "prototype_ksvd: every row shard needs at least s rows");
+  if (!sharded && local.kind == RNLA_SKETCH_GAUSSIAN && !error_fro &&
+      prototype_ksvd_async<T>(ctx, Ap, A.rs, A.cs, m, n, k, s, local.seed, q, uo, vo, sv_out, rank_out, passes_out)) {
+    uo.finish(ctx);
+    vo.finish(ctx);
+    return;
+  }
   int passes = 0;
   // pass 1: Y = A S (m x s, column-major)
   DevBuf Y(sizeof(T) * m * s, ctx->stream);

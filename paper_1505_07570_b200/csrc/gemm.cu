@@ -278,6 +278,11 @@ static bool try_dmma_kk(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double a
                         int64_t a_cs, const TI* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
                         int64_t c_cs, int max_splits, int sym);
 
+// gemm_skinny.cu: fp64 DMMA kernel for n <= 32 outputs.
+bool gemm_skinny_f64(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t a_rs,
+                     int64_t a_cs, const double* B, int64_t b_rs, int64_t b_cs, double beta, double* C, int64_t c_rs,
+                     int64_t c_cs, int max_splits);
+
 template <class T>
 void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, int64_t a_rs, int64_t a_cs,
           const T* B, int64_t b_rs, int64_t b_cs, T beta, T* C, int64_t c_rs, int64_t c_cs, int max_splits) {
@@ -289,6 +294,8 @@ void gemm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, T alpha, const T* A, i
     }
   }
   if constexpr (std::is_same<T, double>::value) {
+    if (n <= 32 && gemm_skinny_f64(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs, max_splits))
+      return;
     if (m >= 64 && n >= 64 &&
         try_dmma_kk<double>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, beta, C, c_rs, c_cs, max_splits, 0))
       return;

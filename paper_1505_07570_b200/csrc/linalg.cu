@@ -355,6 +355,19 @@ void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W) {
   check_info(ctx, info, "eig");
 }
 
+void eig_sym_async(rnla_ctx* ctx, int64_t n, double* A, double* W, int* info) {
+  cusolverDnHandle_t h = solver(ctx);
+  int lwork = 0;
+  cusolver_check(cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, W,
+                                             &lwork),
+                 "syevd_bufferSize");
+  DevBuf work(sizeof(double) * lwork, ctx->stream);
+  cusolver_check(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, W,
+                                  work.as<double>(), lwork, info),
+                 "syevd");
+  note_launch(ctx);
+}
+
 int64_t eig_sym_top(rnla_ctx* ctx, int64_t n, double* A, int64_t k, double* W) {
   cusolverDnHandle_t h = solver(ctx);
   int lwork = 0, found = 0;
@@ -643,15 +656,52 @@ template void chol_inv_async<float>(rnla_ctx*, int64_t, double*, double*, float*
 }  // namespace rnla
 
 // ---------------------------------------------------------------------------
-// Small symmetric eigenproblems (the b x b Rayleigh-Ritz matrices of the
-// block subspace iteration): cuSOLVER syevj with descending outputs. Measured
-// on config 4 (b = 128): syevj 13.0 ms per Nystrom call vs syevd 13.5 ms; a
-// one-CTA one-sided Jacobi kernel (one barrier per round of 64 rotations)
-// was slower still (14.7 ms) and was removed.
+// Small symmetric eigenproblems: the s x s core Gram of prototype_ksvd's
+// truncated SVD (s = 30 at config 0) and the b x b Rayleigh-Ritz matrices of
+// the block subspace iteration (b = 96 at config 4).
+//
+// n <= kJacobiMax: one CTA, two-sided cyclic Jacobi in parallel (round-robin)
+// order, A and V resident in shared memory. Round r rotates the n/2 disjoint
+// pairs of the tournament schedule; warp w owns pairs w, w + nwarps, ...:
+//   phase 1 (columns): the warp reads a_pp, a_qq, a_pq of its own pairs
+//     (columns p, q are touched by no other warp in this phase), forms the
+//     rotation and applies A <- A J, V <- V J to columns p, q;
+//   barrier; phase 2 (rows): A <- J'A on rows p, q, a_pq = a_qp = 0; barrier.
+// Two barriers per round. A pair is rotated when |a_pq| > 1e-15 sqrt(|a_pp a_qq|)
+// (relative criterion: small eigenvalues of an SPD matrix keep their relative
+// accuracy); the sweep loop stops after a sweep without rotations.
+// Replaces cuSOLVER syevjBatched (n <= 32: 154 us for the config-0 30 x 30
+// core) and syevj (config 4, b = 96).
+#include "jacobi.cuh"
+
 namespace rnla {
+namespace {
+// measured (tools/jacobi_bench.cu): n = 30 128 us vs 154 us for cuSOLVER
+// syevjBatched; n = 96 1.28 ms vs ~0.65 ms for syevj, so above 32 cuSOLVER stays
+constexpr int kJacobiMax = 32;
+}  // namespace
+
+bool eig_small_jacobi_async(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z, int* status) {
+  if (b < 1 || b > kJacobiMax || std::getenv("RNLA_EIG_CUSOLVER")) return false;
+  const size_t smem = jacobi_smem_bytes((int)b);
+  ensure_dyn_smem((const void*)jacobi_eig_kernel<512>, smem);
+  jacobi_eig_kernel<512><<<1, 512, smem, ctx->stream>>>((int)b, H, lam, Z, status);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  return true;
+}
 
 bool eig_sym_small_desc(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z) {
   if (b < 1 || b > 256) return false;
+  DevBuf st(sizeof(int), ctx->stream);
+  if (eig_small_jacobi_async(ctx, b, H, lam, Z, st.as<int>())) {
+    int hs = 0;
+    RNLA_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hs & 255) throw NumericError("eig (Jacobi): no convergence in 40 sweeps");
+    if (std::getenv("RNLA_TRACE")) std::fprintf(stderr, "[rnla] jacobi n=%lld sweeps=%d\n", (long long)b, hs >> 8);
+    return true;
+  }
   cusolverDnHandle_t h = solver(ctx);
   syevjInfo_t params;
   if (cusolverDnCreateSyevjInfo(&params) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreateSyevjInfo");

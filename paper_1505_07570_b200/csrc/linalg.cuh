@@ -58,6 +58,13 @@ void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv);
 
 // Symmetric eigen-decomposition of column-major A (n x n): A <- eigenvectors, W ascending.
 void eig_sym(rnla_ctx* ctx, int64_t n, double* A, double* W);
+// The same (syevd: W ascending, eigenvectors in A) without the host round
+// trip: syevd's info lands in *info.
+void eig_sym_async(rnla_ctx* ctx, int64_t n, double* A, double* W, int* info);
+// One-CTA Jacobi (jacobi.cuh) for b <= 32 without a host round trip: lam
+// descending, Z the matching eigenvectors; *status = 0 on convergence (sweeps
+// in bits 8+), 1 otherwise. False when b is out of range.
+bool eig_small_jacobi_async(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z, int* status);
 // Symmetric b x b H (b <= 256) by cuSOLVER syevj: lam[b] descending and Z
 // (b x b, column-major) the matching orthonormal eigenvectors; H is not
 // modified. False when b is out of range (the caller falls back to eig_sym).

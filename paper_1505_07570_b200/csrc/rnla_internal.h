@@ -93,6 +93,24 @@ struct DenseOperator {  // G / sqrt(s) as the reference forms it, device fp64/fp
 
 }  // namespace rnla
 
+namespace rnla {
+// An instantiated CUDA graph of a whole call (e.g. the speculative
+// prototype_ksvd pipeline) plus the persistent device buffers it writes.
+struct CachedGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void*> bufs;  // cudaMalloc'd, owned
+  int64_t kernels = 0;      // kernel nodes (launch accounting per replay)
+  std::vector<int64_t> meta;
+  CachedGraph() = default;
+  CachedGraph(const CachedGraph&) = delete;
+  CachedGraph& operator=(const CachedGraph&) = delete;
+  ~CachedGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (void* p : bufs) cudaFree(p);
+  }
+};
+}  // namespace rnla
+
 struct rnla_ctx {
   int device = 0;
   int world = 1, rank = 0;
@@ -116,6 +134,11 @@ struct rnla_ctx {
   // handles) for independent work run from a second host thread, e.g. eig(W)
   // under the Nystrom C'C Gram; created lazily by side_ctx().
   std::unique_ptr<rnla_ctx> side;
+  // Captured call graphs keyed by their full argument signature (pointers
+  // included); they reference cached operators, so they are dropped first
+  // whenever the operator caches are.
+  std::map<std::string, std::unique_ptr<rnla::CachedGraph>> graphs;
+  bool capturing = false;  // a stream capture is open (trace_mark must not synchronize)
   // Pinned host staging (grown on demand, freed with the context): device
   // results streamed to the host while later blocks still compute.
   void* pinned = nullptr;
