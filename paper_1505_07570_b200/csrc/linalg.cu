@@ -677,15 +677,21 @@ template void chol_inv_async<float>(rnla_ctx*, int64_t, double*, double*, float*
 namespace rnla {
 namespace {
 // measured (tools/jacobi_bench.cu): n = 30 128 us vs 154 us for cuSOLVER
-// syevjBatched; n = 96 1.28 ms vs ~0.65 ms for syevj, so above 32 cuSOLVER stays
+// syevjBatched; n = 96 1.28 ms standalone vs 1.67 ms for syevj, but config 4
+// measured slower end to end with it (11.1 vs 10.6 ms), so above 32 cuSOLVER stays
 constexpr int kJacobiMax = 32;
 }  // namespace
 
 bool eig_small_jacobi_async(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z, int* status) {
   if (b < 1 || b > kJacobiMax || std::getenv("RNLA_EIG_CUSOLVER")) return false;
   const size_t smem = jacobi_smem_bytes((int)b);
-  ensure_dyn_smem((const void*)jacobi_eig_kernel<512>, smem);
-  jacobi_eig_kernel<512><<<1, 512, smem, ctx->stream>>>((int)b, H, lam, Z, status);
+  if (b <= 32) {
+    ensure_dyn_smem((const void*)jacobi_eig_kernel<512>, smem);
+    jacobi_eig_kernel<512><<<1, 512, smem, ctx->stream>>>((int)b, H, lam, Z, status);
+  } else {
+    ensure_dyn_smem((const void*)jacobi_eig_kernel<1024>, smem);
+    jacobi_eig_kernel<1024><<<1, 1024, smem, ctx->stream>>>((int)b, H, lam, Z, status);
+  }
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
   return true;
