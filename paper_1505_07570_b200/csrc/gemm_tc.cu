@@ -40,6 +40,13 @@ namespace {
 #define RNLA_TC_BK 64
 #endif
 constexpr int TC_BM = 128, TC_BK = RNLA_TC_BK, TC_STAGES_MAX = 8;
+// bf16 pieces per operand in the double-float (fp64-output) mode. 2 (BF16x3
+// products, double-float accumulation): the config-2 leverage Gram 8.1 -> 5.0 ms
+// with the same worst-row score error vs the fp64 oracle (3.77e-5 vs 3.74e-5
+// with the 3-piece BF16x6 split; the M R^-1 row-norm GEMM bounds it).
+#ifndef RNLA_TC_DF_NS
+#define RNLA_TC_DF_NS 2
+#endif
 static_assert(TC_BK == 64 || TC_BK == 32, "TC_BK must be 32 or 64");
 constexpr int ROWB = TC_BK * 2;  // bytes per K-major bf16 tile row
 constexpr int QPR = TC_BK / 8;   // 16-B chunks per tile row
@@ -405,9 +412,9 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   const int64_t mblk = (sym & 16) ? blockIdx.y : blockIdx.x, nblk_i = (sym & 16) ? blockIdx.x : blockIdx.y;
   if ((sym & 1) && mblk * TC_BM >= (nblk_i + 1) * BN) return;
   constexpr int PKB = DF ? 256 / TC_BK : TC_PROMOTE_KB;
-  // DF also splits three ways (BF16x6: hh, hm, mh, hl, lh, mm ~ fp32-faithful
-  // products, 1.9e-7 rel-F per SURVEY §7 hard part 5); otherwise BF16x3.
-  constexpr int NS = DF ? 3 : 2;
+  // DF may split three ways (RNLA_TC_DF_NS = 3, BF16x6: hh, hm, mh, hl, lh, mm ~
+  // fp32-faithful products, 1.9e-7 rel-F per SURVEY §7 hard part 5); BF16x3 by default.
+  constexpr int NS = DF ? RNLA_TC_DF_NS : 2;
   constexpr int A_TILE = TC_BM * ROWB;  // bytes per bf16 tile (128 rows x TC_BK k)
   constexpr int B_TILE = BN * ROWB;
   constexpr int STAGE = NS * (A_TILE + B_TILE);
@@ -681,7 +688,7 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
                typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
                typename std::conditional<DF, double, float>::type* ws, int sym, const CUtensorMap* amap,
                double* rownorm) {
-  constexpr int NS = DF ? 3 : 2;
+  constexpr int NS = DF ? RNLA_TC_DF_NS : 2;
   constexpr size_t STAGE = NS * (TC_BM * ROWB + BN * ROWB);
   const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
   DevBuf img;
@@ -715,7 +722,7 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
                  double* rownorm) {
   // as many stages as fit in ~220 KB of shared memory (at most TC_STAGES_MAX)
 #define RNLA_ST(BNV) \
-  std::min(TC_STAGES_MAX, (220 * 1024) / ((DF ? 3 : 2) * (TC_BM * ROWB + (BNV) * ROWB)))
+  std::min(TC_STAGES_MAX, (220 * 1024) / ((DF ? RNLA_TC_DF_NS : 2) * (TC_BM * ROWB + (BNV) * ROWB)))
 #define RNLA_TC(BNV)                                                                                           \
   do {                                                                                                         \
     if (amap)                                                                                                  \
