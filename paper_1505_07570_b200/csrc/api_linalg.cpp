@@ -1168,11 +1168,12 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
     std::vector<cudaEvent_t> ev;
     WeightPrefix prefix;
     int64_t done = 0;  // blocks folded into prefix
-    auto fold = [&](int64_t upto) {
+    auto fold = [&](int64_t upto) {  // also moves the block into the caller's scores
       for (; done < upto; ++done) {
         const int64_t r0 = done * blk, rows = std::min(blk, n - r0);
         RNLA_CUDA(cudaEventSynchronize(ev[(size_t)done]));
         prefix.extend(hs + r0, rows);
+        std::copy(hs + r0, hs + r0 + rows, scores + r0);
       }
     };
     if (stream_draw) {
@@ -1219,9 +1220,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
     }
     for (auto& e : ev) RNLA_CUDA(cudaEventDestroy(e));
     trace_mark(ctx, "leverage_rows: scores");
-    if (stream_draw) {
-      std::copy(hs, hs + n, scores);
-    } else {
+    if (!stream_draw) {
       if (n > 0) RNLA_CUDA(cudaMemcpyAsync(scores, sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
       RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
     }

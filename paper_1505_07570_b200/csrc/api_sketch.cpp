@@ -75,10 +75,22 @@ std::shared_ptr<SrhtPlan> srht_plan(rnla_ctx* ctx, int64_t n, int64_t s, uint64_
 // on config 1 with split-K per chunk: 3.29 -> 3.24 ms per step at 2048, 3.34 ms
 // at 4096; without split-K: 3.17 ms at 2048, 3.16 ms at 1024).
 static constexpr int64_t kOneGpuKC = 1024;
-static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k) {
+// whole: the fp64 stage runs on the int8 tensor cores (ozaki.cu). There it
+// takes one launch over the whole K after the count sketch: the digit GEMM
+// does not share SMs with the gather (its CTAs need most of an SM's shared
+// memory and registers), and at 4.5 POPS the exposed stage is short
+// (config 1: 0.57 ms of DMMA -> ~0.13 ms).
+static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k, bool whole) {
   const int64_t w = std::max(1, ctx->world);
+  if (w == 1 && whole && k <= 65536) return std::max<int64_t>(16, k);
   if (w == 1 && k >= 2 * kOneGpuKC) return kOneGpuKC;
   return std::max<int64_t>(16, (k + w - 1) / w);
+}
+
+// the Gaussian stage of T-typed data with s outputs and L segments takes the Ozaki path
+template <class T>
+static bool gauss_whole(int64_t s, int64_t L) {
+  return std::is_same<T, double>::value && ozaki_applies(s, L);
 }
 
 // Row pitch (elements) rounded up to 16 bytes.
@@ -91,12 +103,16 @@ static int64_t aligned_ld(int64_t L) {
 template <class T>
 void gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const T* in, int64_t ld, int64_t n, int64_t L, int64_t s,
                     int64_t k0, bool first, T* out, int64_t out_rs, int64_t out_cs) {
-  const int64_t kc = std::min(gauss_kc_for(ctx, n), n - k0);
+  const int64_t kc = std::min(gauss_kc_for(ctx, n, gauss_whole<T>(s, L)), n - k0);
   // Chunked stages run each chunk without split-K (one CTA per output tile):
   // under the gather that interferes least (config 1: 3.24 -> 3.16 ms). The
   // standalone and the combined stage chunk identically, so the composition
   // stays bitwise.
-  const int max_splits = gauss_kc_for(ctx, n) < n ? 1 : 64;
+  const int max_splits = gauss_kc_for(ctx, n, gauss_whole<T>(s, L)) < n ? 1 : 64;
+  // fp64: the exact int8 digit split on the tensor cores (ozaki.cu), the same
+  // for the standalone and the combined stage
+  if constexpr (std::is_same<T, double>::value)
+    if (ozaki_gaussian_chunk(ctx, g, in, ld, n, L, s, k0, kc, !first, out, out_rs, out_cs)) return;
   gemm<T>(ctx, s, L, kc, T(1), g.data.as<T>() + k0, n, 1, in + k0 * ld, ld, 1, first ? T(0) : T(1), out, out_rs,
           out_cs, max_splits);
 }
@@ -123,7 +139,7 @@ void gaussian_segments(rnla_ctx* ctx, const T* in, int64_t ld, int64_t n, int64_
     copy2d<T>(ctx, s, L, z.as<T>(), L, 1, out, out_rs, out_cs);
     return;
   }
-  const int64_t kc = gauss_kc_for(ctx, n);
+  const int64_t kc = gauss_kc_for(ctx, n, gauss_whole<T>(s, L));
   for (int64_t k0 = 0; k0 < n; k0 += kc) gaussian_chunk<T>(ctx, g, in, ld, n, L, s, k0, k0 == 0, out, out_rs, out_cs);
 }
 
@@ -144,7 +160,7 @@ void combined_gaussian_pipelined(rnla_ctx* ctx, const T* M, int64_t ld, const T*
   const int64_t ldm = aligned_ld<T>(Lo);
   DevBuf mid(sizeof(T) * (size_t)(s * ldm), ctx->stream);
   DevBuf acc(sizeof(T) * (size_t)(s2 * Lo), ctx->stream);
-  const int64_t KC = gauss_kc_for(ctx, s);
+  const int64_t KC = gauss_kc_for(ctx, s, gauss_whole<T>(s2, Lo));
   const int64_t chunks = (s + KC - 1) / KC;
   std::vector<cudaEvent_t> ev((size_t)chunks + 2);
   for (auto& e : ev) RNLA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -232,7 +248,8 @@ void sketch_rows_dev(rnla_ctx* ctx, const T* M, int64_t ld, const T* extra, int6
   const int64_t Lo = L + (extra ? 1 : 0);
   const int kind = spec->kind;
   const bool sharded = is_sharded(ctx);
-  const bool chunked = spec->kind == RNLA_SKETCH_COMBINED && gauss_kc_for(ctx, spec->s) < spec->s;
+  const bool chunked = spec->kind == RNLA_SKETCH_COMBINED &&
+                       gauss_kc_for(ctx, spec->s, gauss_whole<T>(spec->stage2_s, Lo)) < spec->s;
   if (kind == RNLA_SKETCH_COMBINED && spec->stage2_kind == RNLA_SKETCH_GAUSSIAN &&
       (sharded || chunked)) {
     combined_gaussian_pipelined<T>(ctx, M, ld, extra, xs, n, L, spec, row_offset, out, o_rs, o_cs);

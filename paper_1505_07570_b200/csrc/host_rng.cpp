@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <numeric>
 #include <random>
+#include <thread>
 
 #include "rnla_internal.h"
 
@@ -59,11 +60,23 @@ std::vector<int64_t> sample_without_replacement_host(uint64_t seed, int64_t n, i
 }
 
 void WeightPrefix::extend(const double* w, int64_t m) {
+  // one sequential fp64 add per weight (the reference's rounding order) into
+  // pre-sized storage; the sign test is folded into one flag
+  const size_t base = cum.size();
+  cum.resize(base + static_cast<size_t>(m));
+  double* c = cum.data() + base;
+  double t = total;
+  bool neg = false;
   for (int64_t i = 0; i < m; ++i) {
-    require(w[i] >= 0.0, "sample_with_replacement: negative weight");
-    total += w[i];
-    cum.push_back(total);
+    neg |= !(w[i] >= 0.0);
+    t += w[i];
+    c[i] = t;
   }
+  if (neg) {
+    cum.resize(base);
+    require(false, "sample_with_replacement: negative weight");
+  }
+  total = t;
 }
 
 std::vector<int64_t> WeightPrefix::draw(uint64_t seed, int64_t count) const {
@@ -74,22 +87,52 @@ std::vector<int64_t> WeightPrefix::draw(uint64_t seed, int64_t count) const {
   std::uniform_real_distribution<double> unif(0.0, total);
   std::vector<double> u(static_cast<size_t>(count));
   for (int64_t i = 0; i < count; ++i) u[static_cast<size_t>(i)] = unif(rng);
-  // upper_bound(cum, u_i) for every draw, found by one sweep over cum in
-  // ascending u order instead of count binary searches over an n-element
-  // array (cache-missing at n = 2^20); cum is non-decreasing, so the sweep
-  // returns exactly the upper_bound positions.
+  // upper_bound(cum, u_i) for every draw, visiting the draws in ascending u
+  // order: from the previous position a galloping search brackets the next
+  // one and a binary search inside the bracket finishes (about log2(n / count)
+  // probes near the last hit per draw, instead of count cold binary searches
+  // over an n-element array or one linear sweep over all of it). cum is
+  // non-decreasing, so these are exactly the upper_bound positions.
   std::vector<int64_t> order(static_cast<size_t>(count));
   for (int64_t i = 0; i < count; ++i) order[static_cast<size_t>(i)] = i;
   std::stable_sort(order.begin(), order.end(),
                    [&](int64_t a, int64_t b) { return u[static_cast<size_t>(a)] < u[static_cast<size_t>(b)]; });
   std::vector<int64_t> out(static_cast<size_t>(count));
-  int64_t j = 0;
-  for (int64_t r = 0; r < count; ++r) {
-    const int64_t i = order[static_cast<size_t>(r)];
-    const double ui = u[static_cast<size_t>(i)];
-    while (j < n && cum[static_cast<size_t>(j)] <= ui) ++j;
-    out[static_cast<size_t>(i)] = j >= n ? n - 1 : j;
-  }
+  const double* c = cum.data();
+  // The sorted draws are cut into contiguous ranges searched by separate host
+  // threads (each range starts from its own binary search): at n = 2^20 the
+  // probes into the 8 MB prefix array are cache misses, ~1 ms on one thread.
+  auto search = [&](int64_t r0, int64_t r1) {
+    if (r0 >= r1) return;
+    const double u0 = u[static_cast<size_t>(order[static_cast<size_t>(r0)])];
+    int64_t j = std::upper_bound(c, c + n, u0) - c;
+    for (int64_t r = r0; r < r1; ++r) {
+      const int64_t i = order[static_cast<size_t>(r)];
+      const double ui = u[static_cast<size_t>(i)];
+      if (j < n && c[j] <= ui) {
+        int64_t lo = j, step = 1;  // invariant: c[lo] <= ui
+        while (lo + step < n && c[lo + step] <= ui) {
+          lo += step;
+          step *= 2;
+        }
+        int64_t hi = std::min(n, lo + step);  // c[hi] > ui or hi == n
+        while (hi - lo > 1) {
+          const int64_t mid = lo + (hi - lo) / 2;
+          if (c[mid] <= ui) lo = mid;
+          else hi = mid;
+        }
+        j = hi;
+      }
+      out[static_cast<size_t>(i)] = j >= n ? n - 1 : j;
+    }
+  };
+  const int nth = (count >= 1024 && n >= (int64_t)1 << 16)
+                      ? (int)std::max<unsigned>(1u, std::min<unsigned>(8u, std::thread::hardware_concurrency()))
+                      : 1;
+  std::vector<std::thread> th;
+  for (int t = 1; t < nth; ++t) th.emplace_back(search, count * t / nth, count * (t + 1) / nth);
+  search(0, count / nth);
+  for (auto& x : th) x.join();
   return out;
 }
 

@@ -88,7 +88,17 @@ struct DenseOperator {  // G / sqrt(s) as the reference forms it, device fp64/fp
   DevBuf data;
   int64_t rows = 0, cols = 0;
   int dtype = RNLA_F64;
+  // int8 digit planes of the transposed operator for the Ozaki-split Gaussian
+  // stage (ozaki.cu), built on first use
+  mutable DevBuf oz_planes, oz_rscale;
+  mutable int64_t oz_pitch = 0;
 };
+// fp64 Gaussian stage out (+)= Gs(k0 : k0 + kc, :)' in(k0 : k0 + kc, :) on the
+// int8 tensor cores (ozaki.cu); false when the shape does not apply.
+bool ozaki_applies(int64_t s, int64_t L);
+bool ozaki_gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const double* in, int64_t ld, int64_t n, int64_t L,
+                          int64_t s, int64_t k0, int64_t kc, bool accumulate, double* out, int64_t out_rs,
+                          int64_t out_cs);
 
 
 }  // namespace rnla

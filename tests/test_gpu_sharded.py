@@ -274,4 +274,7 @@ def test_sharded_leverage_sample_rows(ctx, world, dtype):
     # the draw is the reference sampler over the gathered scores, bit-exact
     draws = np.unique(orc.sample_with_replacement(scores, p, 17))
     assert np.array_equal(res[0][1], draws)
-    assert abs(scores.sum() - d) <= 1e-6 * d
+    # sum of scores = rank d; for fp32 the deviation is the mean relative score
+    # error (Gram in BF16x3 products + double-float accumulation: ~3e-6), well
+    # inside the 1e-4 per-score gate
+    assert abs(scores.sum() - d) <= (1e-6 if dtype == np.float64 else 1e-5) * d
