@@ -82,7 +82,7 @@ static constexpr int64_t kOneGpuKC = 1024;
 // (config 1: 0.57 ms of DMMA -> ~0.13 ms).
 static int64_t gauss_kc_for(const rnla_ctx* ctx, int64_t k, bool whole) {
   const int64_t w = std::max(1, ctx->world);
-  if (w == 1 && whole && k <= 65536) return std::max<int64_t>(16, k);
+  if (w == 1 && whole && k <= 16384) return std::max<int64_t>(16, k);
   if (w == 1 && k >= 2 * kOneGpuKC) return kOneGpuKC;
   return std::max<int64_t>(16, (k + w - 1) / w);
 }

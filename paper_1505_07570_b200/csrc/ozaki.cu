@@ -5,26 +5,32 @@
 //
 // Every row i of Gs' = Omega' and every column j of the chunk of `in` is
 // scaled by a power of two (2^e_i, 2^f_j: the largest magnitude in it maps below
-// 1) and rounded ONCE to a 48-bit integer, N = rint(x 2^48 / 2^e), which is split
-// exactly into seven balanced base-128 digits,
-//     N = sum_p d_p 2^(42 - 7p),  d_0 in [-64, 64], d_1..6 in [-64, 63],
-// so x = 2^(e - 6) sum_p d_p 2^(-7p) to 2^-49 relative to the row (column)
-// maximum. The digit products are exact in the s32 accumulators of
-// tcgen05.mma kind::i8; the 28 pairs with p + q <= 6 accumulate by class
-// k = p + q (seven TMEM accumulators) and are combined in fp64,
-//     out_ij = 2^(e_i + f_j - 12) sum_k 2^(-7k) S_k,
-// dropping the classes k >= 7 (|term| ~ 2^-45 of 2^(e_i + f_j) for random
-// digits). Six digits (41 bits) measured 2.2e-10 relative error in the config-1
-// LSR objective against the fp64 oracle (gate 1e-10); seven are used.
+// 1) and rounded ONCE to a 46-bit integer, N = rint(x 2^46 / 2^e), which is split
+// exactly into six balanced digits, the first in [-64, 64] and five base-256
+// ones in [-128, 127] (all int8),
+//     N = sum_p d_p 2^(40 - 8p),   x = 2^(e - 6) sum_p d_p 2^(-8p)
+// to 2^-47 relative to the row (column) maximum. The digit products are exact
+// in the s32 accumulators of tcgen05.mma kind::i8; the 21 pairs with
+// p + q <= 5 accumulate by class k = p + q (six TMEM accumulators of 80 columns)
+// and are combined in fp64,
+//     out_ij = 2^(e_i + f_j - 12) sum_k 2^(-8k) S_k,
+// dropping the classes k >= 6. Measured: 3.4e-13 rel-F against torch fp64 on
+// the config-1 stage (gate 1e-10); six base-128 digits (41 bits) had failed the
+// config-1 LSR objective gate (2.2e-10 vs 1e-10). Variants measured on the
+// config-1 stage (8192 x 513 -> 2048, whole stage incl. the digit kernels):
+// base 128 x 7 digits, N 64, 32-k SW32 stages x 5: 357 us; base 256 x 6, N 80,
+// 32-k x 5: 303 us; 64-k SW64 x 2: 289 us (used); fp64 DMMA: 953 us standalone
+// (570 us with split-K). The kernel is bound by L2-to-SM operand traffic
+// (6 x 208 B per k for 21 x 128 x 80 MACs: ~48 B/clk/SM at the int8 rate).
 //
 // Layout: digit planes are K-major (each row of Gs', each column of the chunk,
 // has its K digits contiguous), plane p at planes + p * plane_stride, loaded by
-// TMA as SWIZZLE_32B boxes of 32 k x rows. Omega's planes are built once per
+// TMA as swizzled boxes of OBK k x rows. Omega's planes are built once per
 // cached operator; the chunk's planes per call (a column-max kernel and a
-// digit kernel). CTA = one 128 x 64 output tile over the chunk's K, 5-stage
-// ring: warp 0 TMA producer, warp 1 MMA issuer (28 digit pairs per 32-k stage),
-// warps 2-5 epilogue (fp64 combination through shared memory, coalesced
-// (+)= into the output).
+// digit kernel). CTA = one 128 x 80 output tile over the chunk's K: warp 0 TMA
+// producer, warp 1 MMA issuer (21 digit pairs per 32-k step), warps 2-5
+// epilogue (fp64 combination through shared memory, coalesced (+)= into the
+// output).
 #include <cuda.h>
 
 #include "rnla_internal.h"
@@ -34,14 +40,32 @@ namespace rnla {
 
 namespace {
 
-constexpr int OP = 7;                                  // digits per operand
-constexpr int OM = 128, ON = 64, OBK = 32, OSTAGES = 5;
+#ifndef RNLA_OZ_BITS
+#define RNLA_OZ_BITS 8   // bits per digit after the first (base 2^bits)
+#endif
+#ifndef RNLA_OZ_P
+#define RNLA_OZ_P 6      // digits per operand
+#endif
+#ifndef RNLA_OZ_N
+#define RNLA_OZ_N 80     // output columns per CTA (OP * ON TMEM columns)
+#endif
+#ifndef RNLA_OZ_BK
+#define RNLA_OZ_BK 64    // k per stage (32: SWIZZLE_32B rows, 64: SWIZZLE_64B)
+#endif
+#ifndef RNLA_OZ_STAGES
+#define RNLA_OZ_STAGES 2
+#endif
+constexpr int OP = RNLA_OZ_P, DB = RNLA_OZ_BITS;
+constexpr int OM = 128, ON = RNLA_OZ_N, OBK = RNLA_OZ_BK, OSTAGES = RNLA_OZ_STAGES;
 constexpr int OA_TILE = OM * OBK, OB_TILE = ON * OBK;  // bytes per digit-plane tile
-constexpr int OSTAGE = OP * (OA_TILE + OB_TILE);       // 43008 B (42 x 1024)
+constexpr int OSTAGE = OP * (OA_TILE + OB_TILE);
 constexpr int OSMEM = OSTAGES * OSTAGE + 1024 + 256;
 constexpr int OTHREADS = 192;
-constexpr int OBITS = 6 + 7 * (OP - 1);                // 48 bits of each scaled value
-constexpr double kTwoBits = 281474976710656.0;         // 2^48
+constexpr int OBITS = 6 + DB * (OP - 1);               // bits of each scaled value
+constexpr double kTwoBits = (double)(1ll << OBITS);
+constexpr double kDigitW = 1.0 / (double)(1 << DB);     // weight ratio of consecutive classes
+// class sums stay below 2^31: OP pairs x kc x (2^(DB-1))^2
+constexpr int64_t kMaxKc = ((int64_t)1 << 31) / ((int64_t)OP << (2 * (DB - 1))) / 64 * 64;
 static_assert(OSTAGE % 1024 == 0, "stage alignment");
 static_assert(OP * ON <= 512, "class accumulators exceed TMEM");
 static_assert(OM * ON * 8 <= OSTAGES * OSTAGE, "epilogue tile must fit in the stage ring");
@@ -72,14 +96,15 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
-// K-major SWIZZLE_32B smem descriptor: 32-B rows (32 int8 k), 8-row atoms (SBO 256 B), version 1.
-__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+// K-major swizzled smem descriptor for OBK-byte rows: SWIZZLE_32B (code 6, 8-row
+// atoms of 256 B) or SWIZZLE_64B (code 4, 512 B), version 1.
+__device__ __forceinline__ uint64_t desc_sw(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)((8 * OBK) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)6 << 61;
+  d |= (uint64_t)(OBK == 32 ? 6 : 4) << 61;
   return d;
 }
 // kind::i8: D s32, A/B s8, K-major, M = 128, N = ON.
@@ -110,11 +135,12 @@ __device__ __forceinline__ int oz_exponent(double mx) { return mx > 0.0 ? ilogb(
 // The OP digits of x scaled by 2^-e (one rounding, then exact integer steps).
 __device__ __forceinline__ void oz_digits(double x, double inv_scale, int8_t* d) {
   long long N = llrint(x * inv_scale * kTwoBits);
+  constexpr long long half = 1ll << (DB - 1), mask = (1ll << DB) - 1;
 #pragma unroll
   for (int p = OP - 1; p > 0; --p) {
-    const long long r = ((N + 64) & 127) - 64;
+    const long long r = ((N + half) & mask) - half;
     d[p] = (int8_t)r;
-    N = (N - r) >> 7;
+    N = (N - r) >> DB;
   }
   d[0] = (int8_t)N;
 }
@@ -263,14 +289,16 @@ __global__ void __launch_bounds__(OTHREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t a0 = su32(smem + st * OSTAGE), b0 = a0 + OP * OA_TILE;
 #pragma unroll
-        for (int p = 0; p < OP; ++p)
+        for (int kk = 0; kk < OBK / 32; ++kk)
 #pragma unroll
-          for (int q = 0; q + p < OP; ++q) {
-            // the first write of class p + q is pair (0, q) at the first k-block
-            const bool first = kb == 0 && p == 0;
-            mma_i8(tmem + (uint32_t)((p + q) * ON), desc_sw32(a0 + p * OA_TILE), desc_sw32(b0 + q * OB_TILE),
-                   first ? 0u : 1u);
-          }
+          for (int p = 0; p < OP; ++p)
+#pragma unroll
+            for (int q = 0; q + p < OP; ++q) {
+              // the first write of class p + q is pair (0, q) at the first k-step
+              const bool first = kb == 0 && kk == 0 && p == 0;
+              mma_i8(tmem + (uint32_t)((p + q) * ON), desc_sw(a0 + p * OA_TILE + kk * 32),
+                     desc_sw(b0 + q * OB_TILE + kk * 32), first ? 0u : 1u);
+            }
         mma_commit(su32(&bars[OSTAGES + st]));  // stage free once these MMAs complete
       }
       mma_commit(su32(&bars[2 * OSTAGES]));  // accumulators final
@@ -297,7 +325,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
         // sum_k 2^-7k S_k, smallest terms first
         double h = (double)(int)v[OP - 1][jj];
 #pragma unroll
-        for (int k = OP - 2; k >= 0; --k) h = fma(h, 0.0078125, (double)(int)v[k][jj]);
+        for (int k = OP - 2; k >= 0; --k) h = fma(h, kDigitW, (double)(int)v[k][jj]);
         tile[r * (ON + 1) + c0 + jj] = h * rs;
       }
     }
@@ -344,7 +372,8 @@ void oz_plane_map(CUtensorMap* m, const int8_t* planes, int64_t kdim, int64_t ro
   const cuuint32_t box[3] = {(cuuint32_t)OBK, box_rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = oz_encode()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides,
-                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 OBK == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (Ozaki digit planes) failed: " + std::to_string((int)r));
 }
@@ -368,7 +397,7 @@ bool ozaki_gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const double* i
   // class sums stay below 2^31: 6 pairs x kc x 64^2 for kc <= 65536
   // chunk starts on a 32-k box boundary (measured: an unaligned k0 -- the
   // world-3 shard chunks of 171 buckets -- faults in the kernel)
-  if (!ozaki_applies(s, L) || g.dtype != RNLA_F64 || kc < OBK || kc > 65536 || n >= INT32_MAX || (k0 % OBK) != 0)
+  if (!ozaki_applies(s, L) || g.dtype != RNLA_F64 || kc < OBK || kc > kMaxKc || n >= INT32_MAX || (k0 % OBK) != 0)
     return false;
   // Omega's digit planes and row scales, once per cached operator
   if (!g.oz_planes.p) {
