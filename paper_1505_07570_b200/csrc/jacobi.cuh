@@ -86,7 +86,17 @@ __global__ void __launch_bounds__(NT) jacobi_eig_kernel(int n, const double* __r
     Q[e] = (uint8_t)max(p, q);
   }
   if (tid < 2) rotated[tid] = 0;
+  __shared__ double amax_s;
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(A[i * ld + i]));
+    amax_s = mx;
+  }
   __syncthreads();
+  // absolute floor: entries below 1e-17 max|a_ii| are left alone (eigenvalues
+  // then carry ~1e-17 ||A|| absolute error, far below what the callers need:
+  // sigma_k >= 1e-3 sigma_1 in topk_svd_wide, Ritz values relative to theta_1)
+  const double afloor = 1e-17 * amax_s;
   int sweep = 0, conv = m <= 1;
   for (; sweep < 40 && !conv; ++sweep) {
     const int flag = sweep & 1;
@@ -110,7 +120,7 @@ __global__ void __launch_bounds__(NT) jacobi_eig_kernel(int n, const double* __r
         const int p = pp[j], q = qq[j];
         if (q < n) {
           const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
-          if (apq != 0.0 && apq * apq > 1e-30 * fabs(app * aqq)) jacobi_rotation(app, aqq, apq, cs[j], sn[j]);
+          if (fabs(apq) > afloor && apq * apq > 1e-30 * fabs(app * aqq)) jacobi_rotation(app, aqq, apq, cs[j], sn[j]);
         }
       }
       __syncwarp();

@@ -677,8 +677,9 @@ template void chol_inv_async<float>(rnla_ctx*, int64_t, double*, double*, float*
 namespace rnla {
 namespace {
 // measured (tools/jacobi_bench.cu): n = 30 128 us vs 154 us for cuSOLVER
-// syevjBatched; n = 96 1.28 ms standalone vs 1.67 ms for syevj, but config 4
-// measured slower end to end with it (11.1 vs 10.6 ms), so above 32 cuSOLVER stays
+// syevjBatched; n = 96 1.02 ms standalone vs 1.67 ms for syevj, but the config-4
+// Rayleigh-Ritz matrix (clustered eigenvalues) takes 9 sweeps (2.05 ms; config 4
+// 11.1 vs 10.6 ms), so above 32 cuSOLVER stays
 constexpr int kJacobiMax = 32;
 }  // namespace
 
