@@ -580,7 +580,7 @@ void prototype_ksvd_async_body(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t
 
 template <class T>
 bool prototype_ksvd_async(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t a_cs, int64_t m, int64_t n, int64_t k,
-                          int64_t s, uint64_t seed, int32_t q, OutMat& uo, OutMat& vo, double* sv_out,
+                          int64_t s, uint64_t seed, int32_t q, bool a_stable, OutMat& uo, OutMat& vo, double* sv_out,
                           int64_t* rank_out, int32_t* passes_out) {
   constexpr bool f64 = std::is_same<T, double>::value;
   if (m < 4 * s || n < 4 * s || s > 512 || q > 16 || std::getenv("RNLA_KSVD_SYNC")) return false;
@@ -589,7 +589,9 @@ bool prototype_ksvd_async(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t a_cs
   KsvdAsyncOut o{};
   CachedGraph* cg = nullptr;
   std::unique_ptr<CachedGraph> own;
-  const bool use_graph = s <= 32 && !std::getenv("RNLA_NO_GRAPH");
+  // graphs only for the caller's own device pointer (a host input is staged
+  // through a fresh device buffer whose address is not stable across calls)
+  const bool use_graph = a_stable && s <= 32 && !std::getenv("RNLA_NO_GRAPH");
   if (use_graph) {
     char key[256];
     std::snprintf(key, sizeof key, "ksvd:%d:%p:%lld:%lld:%lld:%lld:%lld:%lld:%p:%d", f64 ? 64 : 32, (const void*)Ap,
@@ -599,6 +601,10 @@ bool prototype_ksvd_async(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t a_cs
     if (it != ctx->graphs.end()) {
       cg = it->second.get();
     } else {
+      if (ctx->graphs.size() >= 32) {  // bounded cache: drop all (stream-ordered with this call)
+        RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->graphs.clear();
+      }
       own.reset(new CachedGraph());
       for (size_t bytes : {sizeof(double) * m * kk, sizeof(double) * n * kk, sizeof(double) * kk, sizeof(int) * 64}) {
         void* p = nullptr;
@@ -689,7 +695,8 @@ void prototype_ksvd_impl(rnla_ctx* ctx, const rnla_mat* a, int64_t k, int64_t s,
           "prototype_ksvd: row-sharded contexts support the Gaussian test matrix");
   require(!sharded || m >= s, "prototype_ksvd: every row shard needs at least s rows");
   if (!sharded && local.kind == RNLA_SKETCH_GAUSSIAN && !error_fro &&
-      prototype_ksvd_async<T>(ctx, Ap, A.rs, A.cs, m, n, k, s, local.seed, q, uo, vo, sv_out, rank_out, passes_out)) {
+      prototype_ksvd_async<T>(ctx, Ap, A.rs, A.cs, m, n, k, s, local.seed, q, a->on_device != 0, uo, vo, sv_out,
+                              rank_out, passes_out)) {
     uo.finish(ctx);
     vo.finish(ctx);
     return;
