@@ -415,14 +415,16 @@ void upper_inverse(rnla_ctx* ctx, int64_t n, const double* R, double* Rinv) {
     tri_block_inv_kernel<<<(unsigned)((n + TB - 1) / TB), 256, smem, ctx->stream>>>(n, R, n, Rinv, n);
     RNLA_CUDA(cudaGetLastError());
     note_launch(ctx);
-    DevBuf T(sizeof(double) * (size_t)(n * (n / 2 + TB)), ctx->stream);
+    // Transposed forms keep both GEMMs on the K-major-A DMMA kernel:
+    //   U = X_JJ' R_IJ' (bj x bi, row-major), X_IJ' = -U X_II' (written transposed).
+    DevBuf U(sizeof(double) * (size_t)(n * (n / 2 + TB)), ctx->stream);
     for (int64_t b = TB; b < n; b *= 2) {
       for (int64_t i0 = 0; i0 + b < n; i0 += 2 * b) {
         const int64_t j0 = i0 + b, bi = b, bj = std::min<int64_t>(b, n - j0);
-        gemm<double>(ctx, bi, bj, bj, 1.0, R + i0 + j0 * n, 1, n, Rinv + j0 + j0 * n, 1, n, 0.0, T.as<double>(), 1,
-                     bi);
-        gemm<double>(ctx, bi, bj, bi, -1.0, Rinv + i0 + i0 * n, 1, n, T.as<double>(), 1, bi, 0.0, Rinv + i0 + j0 * n,
-                     1, n);
+        gemm<double>(ctx, bj, bi, bj, 1.0, Rinv + j0 + j0 * n, n, 1, R + i0 + j0 * n, n, 1, 0.0, U.as<double>(), bi,
+                     1);
+        gemm<double>(ctx, bj, bi, bi, -1.0, U.as<double>(), bi, 1, Rinv + i0 + i0 * n, n, 1, 0.0,
+                     Rinv + i0 + j0 * n, n, 1);
       }
     }
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
