@@ -423,7 +423,13 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
   // M = T'(G T) (symmetric) skips k > row; G is read through its symmetry as
   // K-major. Otherwise plain GEMMs.
   const bool tri = kp == s && cholesky_T;
-  if (!(tri && gemm_f64_structured(ctx, s, kp, s, G.as<double>(), s, 1, Tm.as<double>(), 1, s, GT.as<double>(), 1, s,
+  // Cholesky route on one GPU: both products on the int8 tensor cores with
+  // exact digit products (ozaki.cu: each row of G / T' and column of T / G T
+  // scaled by its own power of two, 46-bit digits), 0.83 -> see DESIGN §3.5
+  const bool oz = tri && !std::getenv("RNLA_NYSTROM_DMMA_M") &&
+                  ozaki_gemm_rowcol(ctx, s, s, s, G.as<double>(), s, Tm.as<double>(), s, GT.as<double>(), 1, s) &&
+                  ozaki_gemm_rowcol(ctx, s, s, s, Tm.as<double>(), s, GT.as<double>(), s, M.as<double>(), 1, kp);
+  if (!oz && !(tri && gemm_f64_structured(ctx, s, kp, s, G.as<double>(), s, 1, Tm.as<double>(), 1, s, GT.as<double>(), 1, s,
                                    2) &&
         gemm_f64_structured(ctx, kp, kp, s, Tm.as<double>(), s, 1, GT.as<double>(), 1, s, M.as<double>(), 1, kp,
                             1 | 4))) {

@@ -433,4 +433,33 @@ bool ozaki_gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const double* i
   return true;
 }
 
+// C (m x n; element (i, j) at C[i * c_rs + j * c_cs]) = A B in fp64 through the
+// same exact digit products, with A given by rows (A(i, k) = A[i * a_ld + k])
+// and B by columns (B(k, j) = B[j * b_ld + k]): both digit sets come from the
+// row-digit kernel (each row of A / column of B scaled by its own power of
+// two). Used for the dense Nystrom products G T and T'(G T). False when the
+// shape does not apply.
+bool ozaki_gemm_rowcol(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t a_ld, const double* B,
+                       int64_t b_ld, double* C, int64_t c_rs, int64_t c_cs) {
+  if (!ozaki_available() || m < 1 || n < 16 || k < OBK || k > kMaxKc || m >= INT32_MAX || n >= INT32_MAX) return false;
+  const int64_t pitch = (k + 15) / 16 * 16;
+  DevBuf ap((size_t)OP * (size_t)m * (size_t)pitch, ctx->stream), bp((size_t)OP * (size_t)n * (size_t)pitch, ctx->stream);
+  DevBuf rs(sizeof(double) * (size_t)m, ctx->stream), cs(sizeof(double) * (size_t)n, ctx->stream);
+  oz_row_digits<<<(unsigned)m, 256, 0, ctx->stream>>>(k, A, a_ld, ap.as<int8_t>(), pitch, m * pitch, rs.as<double>());
+  RNLA_CUDA(cudaGetLastError());
+  oz_row_digits<<<(unsigned)n, 256, 0, ctx->stream>>>(k, B, b_ld, bp.as<int8_t>(), pitch, n * pitch, cs.as<double>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx, 2);
+  CUtensorMap amap, bmap;
+  oz_plane_map(&amap, ap.as<int8_t>(), k, m, pitch, OM);
+  oz_plane_map(&bmap, bp.as<int8_t>(), k, n, pitch, ON);
+  ensure_dyn_smem((const void*)oz_gemm_kernel, OSMEM);
+  dim3 grid((unsigned)((n + ON - 1) / ON), (unsigned)((m + OM - 1) / OM));
+  oz_gemm_kernel<<<grid, OTHREADS, OSMEM, ctx->stream>>>(amap, bmap, m, n, 0, (int)((k + OBK - 1) / OBK),
+                                                         rs.as<double>(), cs.as<double>(), C, c_rs, c_cs, 0);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  return true;
+}
+
 }  // namespace rnla

@@ -96,6 +96,8 @@ struct DenseOperator {  // G / sqrt(s) as the reference forms it, device fp64/fp
 // fp64 Gaussian stage out (+)= Gs(k0 : k0 + kc, :)' in(k0 : k0 + kc, :) on the
 // int8 tensor cores (ozaki.cu); false when the shape does not apply.
 bool ozaki_applies(int64_t s, int64_t L);
+bool ozaki_gemm_rowcol(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t a_ld, const double* B,
+                       int64_t b_ld, double* C, int64_t c_rs, int64_t c_cs);
 bool ozaki_gaussian_chunk(rnla_ctx* ctx, const DenseOperator& g, const double* in, int64_t ld, int64_t n, int64_t L,
                           int64_t s, int64_t k0, int64_t kc, bool accumulate, double* out, int64_t out_rs,
                           int64_t out_cs);
