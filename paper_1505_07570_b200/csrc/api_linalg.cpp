@@ -410,14 +410,36 @@ bool eig_top_subspace(rnla_ctx* ctx, int64_t n, const double* A, int64_t k, doub
   hash_uniform_dev(ctx, n * b, 0x6a09e667f3bcc909ull, Y.as<double>());
   std::vector<double> ht((size_t)b), hr((size_t)k), td((size_t)k);
   int next_rr = values_only ? 5 : 2, rr_count = 0;
+  // Between checkpoints the CholeskyQR passes run without host round trips
+  // (one-CTA Cholesky + inverse, status words read at the next checkpoint);
+  // a breakdown there abandons this route (the caller falls back).
+  const bool async_qr = b <= kSmallCholMax && !std::getenv("RNLA_EIG_SYNC_QR");
+  DevBuf Gq(sizeof(double) * b * b, ctx->stream), Rq(sizeof(double) * b * b, ctx->stream),
+      qst(sizeof(int) * (kMaxIt + 1), ctx->stream);
+  if (async_qr) RNLA_CUDA(cudaMemsetAsync(qst.p, 0, sizeof(int) * (kMaxIt + 1), ctx->stream));
+  int nq = 0;
   for (int it = 0; it < kMaxIt; ++it) {
     // Q = orth(Y) (CholeskyQR2 + Householder fallback at checkpoints, one
     // CholeskyQR pass in between); Y = A Q
     const bool rr = it == next_rr;
-    RNLA_CUDA(cudaMemcpyAsync(Q.p, Y.p, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (rr || !cholqr_inplace(ctx, n, b, Q.as<double>())) {
+    if (!rr && async_qr) {
+      gemm<double>(ctx, b, b, n, 1.0, Y.as<double>(), n, 1, Y.as<double>(), 1, n, 0.0, Gq.as<double>(), 1, b);
+      small_chol_inv<double>(ctx, b, Gq.as<double>(), Rq.as<double>(), nullptr, nullptr, n, 0.0,
+                             qst.as<int>() + nq++);
+      gemm<double>(ctx, n, b, b, 1.0, Y.as<double>(), 1, n, Rq.as<double>(), 1, b, 0.0, Q.as<double>(), 1, n);
+    } else {
       RNLA_CUDA(cudaMemcpyAsync(Q.p, Y.p, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, ctx->stream));
-      KsvdWork<double>::orth(ctx, n, b, Q.as<double>(), false);
+      if (rr || !cholqr_inplace(ctx, n, b, Q.as<double>())) {
+        RNLA_CUDA(cudaMemcpyAsync(Q.p, Y.p, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, ctx->stream));
+        KsvdWork<double>::orth(ctx, n, b, Q.as<double>(), false);
+      }
+    }
+    if (rr && nq > 0) {  // the passes since the last checkpoint factored cleanly?
+      std::vector<int> hq((size_t)nq);
+      RNLA_CUDA(cudaMemcpyAsync(hq.data(), qst.p, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+      RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int v : hq)
+        if (v & 1) return false;
     }
     gemm<double>(ctx, n, b, n, 1.0, A, 1, n, Q.as<double>(), 1, n, 0.0, Y.as<double>(), 1, n);
     trace_mark(ctx, rr ? "eig_top_subspace: orth + A Q (RR step)" : "eig_top_subspace: cholqr + A Q");
