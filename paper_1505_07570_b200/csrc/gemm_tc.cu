@@ -682,6 +682,206 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   }
 }
 
+// Persistent variant for short K (at most two TC_PROMOTE_KB chunks per tile):
+// the leverage-score product M R^-1 (K <= 1024, 8 N tiles per M tile) and the
+// CholeskyQR applies Y R^-1 of config 3 (K = 150). A CTA walks tiles
+// blockIdx.x, + gridDim.x, ... (N-tile fastest, so the N tiles of one M tile run
+// on neighbouring CTAs and share its A rows through L2). The TMA ring and the
+// converter groups run across tile boundaries, and the fp32 TMEM accumulators
+// are double-buffered by tile parity, so the epilogue of tile i overlaps the
+// loads, conversion and MMAs of tile i + 1 (the one-tile kernel serializes
+// TMA -> convert -> MMA -> epilogue per 128-row tile and pays its setup per
+// tile). Chunk sums are combined exactly as the promoting kernel does (fp32
+// adds of the <= 512-k partials). sym bit 1: B upper triangular (k < n0 + BN).
+template <bool A_KC, int BN, int STAGES, int CH>
+__global__ void __launch_bounds__(TC_THREADS + 32, 1)
+    gemm_bf16x3_persist(int64_t M, int64_t N, int64_t K, const float* __restrict__ A, const uint8_t* __restrict__ bimg,
+                        int64_t nkb_total, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, int sym,
+                        const __grid_constant__ CUtensorMap amap, double* rownorm, int ntm, int ntn) {
+  constexpr int NS = 2;
+  constexpr int A_TILE = TC_BM * ROWB, B_TILE = BN * ROWB, STAGE = NS * (A_TILE + B_TILE);
+  constexpr uint32_t TCOLS = 2 * CH * BN;
+  constexpr uint32_t TMEM_COLS = TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512);
+  static_assert(TCOLS <= 512, "double-buffered accumulators exceed TMEM");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // full[S], empty[S], tfull[S], accfull[2], accfree[2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* accfull = bars + 3 * STAGES;
+  uint64_t* accfree = bars + 3 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = ntm * ntn;
+  auto tile_of = [&](int t, int64_t& m0, int64_t& n0, int& nbi, int& nkb) {
+    const int mb = t / ntn;
+    nbi = t % ntn;
+    m0 = (int64_t)mb * TC_BM;
+    n0 = (int64_t)nbi * BN;
+    const int64_t kend = (sym & 2) ? min(K, n0 + BN) : K;
+    nkb = (int)((kend + TC_BK - 1) / TC_BK);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), TC_GROUP);
+      mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&tfull[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&accfull[b]), 1);
+      mbar_init(smem_u32(&accfree[b]), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == TC_EPI_WARP0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < TC_EPI_WARP0) {
+    // ---------------- converters: global k-block g goes to group g % NG ----------------
+    const int grp = warp >> 2, gtid = tid & (TC_GROUP - 1);
+    int g = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int64_t m0, n0;
+      int nbi, nkb;
+      tile_of(t, m0, n0, nbi, nkb);
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        if (g % TC_NGROUPS != grp) continue;
+        const int st = g % STAGES;
+        if (g >= STAGES) mbar_wait(smem_u32(&empty[st]), (uint32_t)(((g / STAGES) - 1) & 1));
+        mbar_wait(smem_u32(&tfull[st]), (uint32_t)((g / STAGES) & 1));
+        convert_tile_inplace<A_KC, NS>(smem + st * STAGE, gtid, grp);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(smem_u32(&full[st]));
+      }
+    }
+  } else if (warp == TC_MMA_WARP + 1) {
+    // ---------------- TMA issuer ----------------
+    if (lane == 0) {
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t m0, n0;
+        int nbi, nkb;
+        tile_of(t, m0, n0, nbi, nkb);
+        const uint8_t* bsrc = bimg + (int64_t)nbi * nkb_total * (int64_t)(NS * B_TILE);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int st = g % STAGES;
+          if (g >= STAGES) mbar_wait(smem_u32(&empty[st]), (uint32_t)(((g / STAGES) - 1) & 1));
+          uint8_t* base = smem + st * STAGE;
+          const uint32_t bar = smem_u32(&tfull[st]);
+          mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 + NS * B_TILE));
+          const int k0 = kb * TC_BK;
+          if (A_KC) {
+#pragma unroll
+            for (int b = 0; b < TC_BK / 32; ++b)
+              tma_load_2d_g2s(smem_u32(base + b * TC_BM * 128), &amap, k0 + 32 * b, (int)m0, bar);
+          } else {
+            tma_load_2d_g2s(smem_u32(base), &amap, (int)m0, k0, bar);
+          }
+          bulk_copy_g2s(smem_u32(base + NS * A_TILE), bsrc + (int64_t)kb * (NS * B_TILE), NS * B_TILE, bar);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == TC_MMA_WARP) {
+    // ---------------- MMA issuer: tile i into accumulator buffer i & 1 ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BN);
+      int g = 0, i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        int64_t m0, n0;
+        int nbi, nkb;
+        tile_of(t, m0, n0, nbi, nkb);
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(smem_u32(&accfree[buf]), (uint32_t)(((i / 2) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int st = g % STAGES;
+          const int chunk = kb / TC_PROMOTE_KB, kin = kb % TC_PROMOTE_KB;
+          mbar_wait(smem_u32(&full[st]), (uint32_t)((g / STAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t dst = tmem + (uint32_t)((buf * CH + chunk) * BN);
+          const uint32_t a0 = smem_u32(smem + st * STAGE), b0 = a0 + NS * A_TILE;
+          constexpr int PI[3] = {0, 0, 1}, PJ[3] = {0, 1, 0};
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            const uint32_t koff = kk * 32;
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+              const uint32_t acc = (p > 0 || kin > 0 || kk > 0) ? 1u : 0u;
+              mma_bf16(dst, kmajor_sw128_desc(a0 + PI[p] * A_TILE + koff), kmajor_sw128_desc(b0 + PJ[p] * B_TILE + koff),
+                       idesc, acc);
+            }
+          }
+          mma_commit(smem_u32(&empty[st]));
+        }
+        mma_commit(smem_u32(&accfull[buf]));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 8-11) ----------------
+    const int quarter = warp & 3;
+    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16);
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      int64_t m0, n0;
+      int nbi, nkb;
+      tile_of(t, m0, n0, nbi, nkb);
+      const int buf = i & 1, nch = (nkb + TC_PROMOTE_KB - 1) / TC_PROMOTE_KB;
+      const int64_t row = m0 + quarter * 32 + lane;
+      mbar_wait(smem_u32(&accfull[buf]), (uint32_t)((i / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      double rsq = 0.0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t x0[16], x1[16];
+        tmem_ld16(tlane + (uint32_t)(buf * CH * BN + c0), x0);
+        if (CH > 1 && nch > 1) tmem_ld16(tlane + (uint32_t)((buf * CH + 1) * BN + c0), x1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        float acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          acc[j] = (CH > 1 && nch > 1) ? __uint_as_float(x0[j]) + __uint_as_float(x1[j]) : __uint_as_float(x0[j]);
+        if (rownorm) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n0 + c0 + j < N) {
+              const double v = alpha * (double)acc[j];
+              rsq += v * v;
+            }
+        } else if (row < M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int64_t col = n0 + c0 + j;
+            if (col < N) {
+              float* cp = C + row * c_rs + col * c_cs;
+              *cp = beta == 0.0 ? (float)(alpha * acc[j]) : (float)(alpha * acc[j] + beta * *cp);
+            }
+          }
+        }
+      }
+      if (rownorm && row < M) rownorm[nbi * M + row] = rsq;
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      mbar_arrive(smem_u32(&accfree[buf]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == TC_EPI_WARP0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 template <bool A_KC, int BN, int STAGES, bool DF, bool TMA_A>
 void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
@@ -712,6 +912,54 @@ void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, i
       amap ? *amap : dummy, rownorm);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
+}
+
+template <bool A_KC, int BN, int CH>
+void launch_tc_persist(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, const float* A, const float* B, int64_t b_rs,
+                       int64_t b_cs, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, int sym,
+                       const CUtensorMap* amap, double* rownorm) {
+  constexpr int NS = 2;
+  constexpr size_t STAGE = NS * (TC_BM * ROWB + BN * ROWB);
+  constexpr int STAGES = std::min<int>(TC_STAGES_MAX, (int)((220 * 1024) / STAGE));
+  const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
+  DevBuf img(NS * (size_t)BN * ROWB * (size_t)(nkb * nblk), ctx->stream);
+  split_b_image<NS><<<grid_for(ctx, nblk * nkb * BN * QPR, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb,
+                                                                                       nblk, img.as<uint8_t>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  const size_t smem = STAGES * STAGE + 1024 + 8 * (3 * STAGES + 4) + 16;
+  auto kern = gemm_bf16x3_persist<A_KC, BN, STAGES, CH>;
+  ensure_dyn_smem((const void*)kern, smem);
+  const int ntm = (int)((m + TC_BM - 1) / TC_BM), ntn = (int)nblk;
+  const int grid = (int)std::min<int64_t>((int64_t)ntm * ntn, ctx->num_sms);
+  kern<<<grid, TC_THREADS + 32, smem, ctx->stream>>>(m, n, k, A, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs,
+                                                      sym, *amap, rownorm, ntm, ntn);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
+// Short-K products without split-K on the persistent kernel; false when the
+// shape does not qualify (the one-tile kernel runs).
+template <bool A_KC>
+bool try_tc_persist(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, const float* A, const float* B,
+                    int64_t b_rs, int64_t b_cs, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs,
+                    int sym, const CUtensorMap* amap, double* rownorm) {
+  const int64_t nkb = (k + TC_BK - 1) / TC_BK;
+  if (k < 1 || nkb > 2 * TC_PROMOTE_KB || !amap) return false;
+  const int64_t tiles = ((m + TC_BM - 1) / TC_BM) * ((n + bn - 1) / bn);
+  if (tiles < 2 * (int64_t)ctx->num_sms) return false;
+  const bool one = nkb <= TC_PROMOTE_KB;
+#define RNLA_P(BNV, CHV) \
+  launch_tc_persist<A_KC, BNV, CHV>(ctx, m, n, k, A, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, sym, amap, rownorm)
+  if (bn <= 32) RNLA_P(32, 2);
+  else if (bn <= 64) RNLA_P(64, 2);
+  else if (bn <= 96) RNLA_P(96, 2);
+  else if (bn <= 128) RNLA_P(128, 2);
+  else if (one && bn <= 152) RNLA_P(152, 1);
+  else if (one && bn <= 160) RNLA_P(160, 1);
+  else return false;
+#undef RNLA_P
+  return true;
 }
 
 template <bool A_KC, bool DF>
@@ -881,6 +1129,16 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   // tensor map (the pre-split B image measured slower: 8.7 vs 8.1 ms).
   const bool b_from_a = sym && tma && bn_full == TC_BM;
   const int flags = sym | (tri_b && !sym ? 2 : 0) | (b_from_a ? 8 : 0);
+  if constexpr (!DF) {
+    static const bool no_persist = std::getenv("RNLA_TC_NO_PERSIST") != nullptr;
+    if (!no_persist && tma && splits == 1 && !sym) {
+      const bool ok = a_cs == 1 ? try_tc_persist<true>(ctx, bn_eff, m, n, k, A, B, b_rs, b_cs, alpha, beta, C, c_rs,
+                                                       c_cs, flags, &amap, rownorm)
+                                : try_tc_persist<false>(ctx, bn_eff, m, n, k, A, B, b_rs, b_cs, alpha, beta, C, c_rs,
+                                                        c_cs, flags, &amap, rownorm);
+      if (ok) return;
+    }
+  }
   if (a_cs == 1)
     dispatch_bn<true, DF>(ctx, bn_full, m, n, k, kchunk, (int)splits, A, a_rs, a_cs, B, b_rs, b_cs, alpha, beta, C,
                           c_rs, c_cs, ws, flags, tma ? &amap : nullptr, rownorm);
