@@ -83,8 +83,8 @@ SvdDev topk_svd_wide(rnla_ctx* ctx, int64_t s, int64_t n, const double* B, int64
   gemm<double>(ctx, s, s, n, 1.0, B, 1, s, B, s, 1, 0.0, G.as<double>(), 1, s);
   std::vector<double> h((size_t)s);
   DevBuf Zd(sizeof(double) * s * s, ctx->stream);
-  if (s <= 32 && eig_sym_small_desc(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>())) {
-    // one-kernel batched Jacobi; back to the ascending layout used below
+  if (s <= 160 && eig_sym_small_desc(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>())) {
+    // one-CTA Jacobi / tridiagonal solver; back to the ascending layout used below
     copy2d<double>(ctx, s, s, Zd.as<double>() + (s - 1) * s, 1, -s, G.as<double>(), 1, s);
     RNLA_CUDA(cudaMemcpyAsync(h.data(), lam.p, sizeof(double) * s, cudaMemcpyDeviceToHost, ctx->stream));
     RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -576,7 +576,8 @@ void prototype_ksvd_async_body(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t
   gemm<double>(ctx, s, s, n, 1.0, Bp, 1, s, Bp, s, 1, 0.0, G.as<double>(), 1, s);
   o.eig_slot = slot++;
   o.desc = 1;
-  if (!eig_small_jacobi_async(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>(), o.st + o.eig_slot)) {
+  if (!eig_small_jacobi_async(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>(), o.st + o.eig_slot) &&
+      !eig_tri_async(ctx, s, G.as<double>(), lam.as<double>(), Zd.as<double>(), o.st + o.eig_slot)) {
     o.desc = 0;
     RNLA_CUDA(cudaMemcpyAsync(Zd.p, G.p, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
     eig_sym_async(ctx, s, Zd.as<double>(), lam.as<double>(), o.st + o.eig_slot);
@@ -690,7 +691,10 @@ bool prototype_ksvd_async(rnla_ctx* ctx, const T* Ap, int64_t a_rs, int64_t a_cs
   trace_mark(ctx, "ksvd (async): U = Q Ubar, stores, status");
   for (int i = 0; i < o.slots; ++i) {
     const int v = (i == o.eig_slot && o.desc) ? (hs[(size_t)i] & 255) : hs[(size_t)i];
-    if (v != 0) return false;
+    if (v != 0) {
+      if (std::getenv("RNLA_TRACE")) std::fprintf(stderr, "[rnla] ksvd (async): status slot %d = %d, checked path\n", i, v);
+      return false;
+    }
   }
   for (int64_t i = 0; i < kk; ++i) sv_out[i] = hsig[(size_t)i];
   *rank_out = kk;

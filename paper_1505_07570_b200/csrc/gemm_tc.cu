@@ -44,6 +44,9 @@ constexpr int TC_BM = 128, TC_BK = RNLA_TC_BK, TC_STAGES_MAX = 8;
 // products, double-float accumulation): the config-2 leverage Gram 8.1 -> 5.0 ms
 // with the same worst-row score error vs the fp64 oracle (3.77e-5 vs 3.74e-5
 // with the 3-piece BF16x6 split; the M R^-1 row-norm GEMM bounds it).
+#ifndef RNLA_TC_DF_PK  // k per TMEM partial sum before the double-float promotion
+#define RNLA_TC_DF_PK 256
+#endif
 #ifndef RNLA_TC_DF_NS
 #define RNLA_TC_DF_NS 2
 #endif
@@ -411,7 +414,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
   // together and share its A rows through L2.
   const int64_t mblk = (sym & 16) ? blockIdx.y : blockIdx.x, nblk_i = (sym & 16) ? blockIdx.x : blockIdx.y;
   if ((sym & 1) && mblk * TC_BM >= (nblk_i + 1) * BN) return;
-  constexpr int PKB = DF ? 256 / TC_BK : TC_PROMOTE_KB;
+  constexpr int PKB = DF ? RNLA_TC_DF_PK / TC_BK : TC_PROMOTE_KB;
   // DF may split three ways (RNLA_TC_DF_NS = 3, BF16x6: hh, hm, mh, hl, lh, mm ~
   // fp32-faithful products, 1.9e-7 rel-F per SURVEY §7 hard part 5); BF16x3 by default.
   constexpr int NS = DF ? RNLA_TC_DF_NS : 2;
@@ -479,7 +482,9 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
       convert_tile_inplace<A_KC, NS>(smem + st * STAGE, gtid, grp);
       // Gram with B = A' (sym bit 3, BN == TC_BM): the B tile is the A operand's
       // tile at column block n0, landed by TMA and split the same way.
-      if (BN == TC_BM && (sym & 8)) convert_tile_inplace<A_KC, NS>(smem + st * STAGE + NS * A_TILE, gtid, grp);
+      // (A diagonal tile, m0 == n0, has B == A: the MMA reads the A pieces twice.)
+      if (BN == TC_BM && (sym & 8) && m0 != n0)
+        convert_tile_inplace<A_KC, NS>(smem + st * STAGE + NS * A_TILE, gtid, grp);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive(smem_u32(&bars[st]));
     }
@@ -494,7 +499,9 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         uint8_t* base = smem + st * STAGE;
         const uint32_t bar = smem_u32(&tfull[st]);
         const bool b_from_a = BN == TC_BM && (sym & 8);
-        mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 + (b_from_a ? TC_BM * TC_BK * 4 : NS * B_TILE)));
+        const bool b_is_a = b_from_a && m0 == n0;
+        mbar_arrive_expect_tx(bar, (uint32_t)(TC_BM * TC_BK * 4 +
+                                              (b_is_a ? 0 : (b_from_a ? TC_BM * TC_BK * 4 : NS * B_TILE))));
         const int k0 = (int)(kbeg + (int64_t)kb * TC_BK);
         if (A_KC) {  // one 128-row x 32-fp32 SWIZZLE_128B box per 32 k
 #pragma unroll
@@ -503,7 +510,8 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
         } else {
           tma_load_2d_g2s(smem_u32(base), &amap, (int)m0, k0, bar);
         }
-        if (b_from_a) {
+        if (b_is_a) {
+        } else if (b_from_a) {
           if (A_KC) {
 #pragma unroll
             for (int b = 0; b < TC_BK / 32; ++b)
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(TMA_A ? TC_THREADS + 32 : TC_THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;\n");
           const uint32_t dst = tmem + (uint32_t)(xb * BN);
           const uint32_t base = smem_u32(smem + st * STAGE);
-          const uint32_t a0 = base, b0 = base + NS * A_TILE;
+          const uint32_t a0 = base, b0 = (BN == TC_BM && (sym & 8) && m0 == n0) ? base : base + NS * A_TILE;
           // products (i, j) of pieces: (0,0) (0,1) (1,0) [+ (0,2) (2,0) (1,1) for NS = 3]
           constexpr int NP = NS == 3 ? 6 : 3;
           constexpr int PI[6] = {0, 0, 1, 0, 2, 1}, PJ[6] = {0, 1, 0, 2, 0, 1};

@@ -777,6 +777,7 @@ template void chol_inv_async<float>(rnla_ctx*, int64_t, double*, double*, float*
 // Replaces cuSOLVER syevjBatched (n <= 32: 154 us for the config-0 30 x 30
 // core) and syevj (config 4, b = 96).
 #include "jacobi.cuh"
+#include "syev_tri.cuh"
 
 namespace rnla {
 namespace {
@@ -802,9 +803,33 @@ bool eig_small_jacobi_async(rnla_ctx* ctx, int64_t b, const double* H, double* l
   return true;
 }
 
+// 32 < n <= kTriMax: one-CTA tridiagonal eigensolver (syev_tri.cuh), descending
+// lam / Z (Z may alias H); *status = 1 when the caller must fall back.
+// Measured (tools/tri_check.py): n = 96 0.58-0.87 ms (random .. graded spectrum)
+// vs 1.7 ms for syevj; n = 150 1.3-2.1 ms vs ~1.5 ms for syevd, so cuSOLVER
+// keeps n > kTriUse.
+constexpr int kTriUse = 128;
+bool eig_tri_async(rnla_ctx* ctx, int64_t n, const double* H, double* lam, double* Z, int* status) {
+  if (n < 3 || n > kTriUse || std::getenv("RNLA_EIG_CUSOLVER")) return false;
+  DevBuf hv(sizeof(double) * n * n, ctx->stream);
+  const size_t smem = tri_smem_bytes((int)n);
+  ensure_dyn_smem((const void*)syev_tri_kernel, smem);
+  syev_tri_kernel<<<1, kTriThreads, smem, ctx->stream>>>((int)n, H, lam, Z, hv.as<double>(), status, 1, nullptr);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  return true;
+}
+
 bool eig_sym_small_desc(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z) {
   if (b < 1 || b > 256) return false;
   DevBuf st(sizeof(int), ctx->stream);
+  if (b > kJacobiMax && eig_tri_async(ctx, b, H, lam, Z, st.as<int>())) {
+    int hs = 0;
+    RNLA_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RNLA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hs == 0) return true;
+    if (std::getenv("RNLA_TRACE")) std::fprintf(stderr, "[rnla] tridiagonal eig n=%lld: fallback\n", (long long)b);
+  }
   if (eig_small_jacobi_async(ctx, b, H, lam, Z, st.as<int>())) {
     int hs = 0;
     RNLA_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -64,6 +64,9 @@ void eig_sym_async(rnla_ctx* ctx, int64_t n, double* A, double* W, int* info);
 // One-CTA Jacobi (jacobi.cuh) for b <= 32 without a host round trip: lam
 // descending, Z the matching eigenvectors; *status = 0 on convergence (sweeps
 // in bits 8+), 1 otherwise. False when b is out of range.
+// One-CTA tridiagonal eigensolver for 32 < n <= 128 (descending, Z may alias
+// H); false when n is out of range. *status = 1: fall back (clustered spectrum).
+bool eig_tri_async(rnla_ctx* ctx, int64_t n, const double* H, double* lam, double* Z, int* status);
 bool eig_small_jacobi_async(rnla_ctx* ctx, int64_t b, const double* H, double* lam, double* Z, int* status);
 // Symmetric b x b H (b <= 256) by cuSOLVER syevj: lam[b] descending and Z
 // (b x b, column-major) the matching orthonormal eigenvectors; H is not
