@@ -890,6 +890,419 @@ __global__ void __launch_bounds__(TC_THREADS + 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// A-operand-in-TMEM variant (tcgen05.mma with [a_tmem]) for the long-K
+// projections of config 3 (Y = A Q, Z = A'Q; N <= 160 in one tile).
+//
+// Why: the smem-operand kernel above is bound by shared-memory bandwidth, not
+// by HBM or the tensor pipe (ncu, config-3 pass: LSU shared wavefronts 60 % of
+// peak with half of them arbitration conflicts against the TMA writes and the
+// UMMA operand reads; 241 KB of shared-memory traffic per 128 x 64 k-block =
+// ~1.9 k cycles at 128 B/clk against a 912-cycle MMA floor). Here the
+// converters write the bf16 hi/lo pieces of A straight into TMEM
+// (tcgen05.st), so the per-k-block shared-memory traffic drops to the TMA
+// write + one LSU read of the fp32 tile and the B pieces (161 KB): no bf16 A
+// images in shared memory and no UMMA A-operand reads from it. The raw fp32
+// ring is decoupled from the MMA: a stage is free as soon as its rows sit in
+// converter registers, so RA tiles of A stay in flight per SM.
+//
+// TMEM (512 columns): X0 | X1 (fp32 partial sums, BN columns each, double
+// buffered by 512-k chunk) | TA stages of the A pieces (32 columns hi + 32
+// columns lo per 64-k block, bf16 pairs per column, lane = tile row). The
+// promoted accumulator Y lives in the registers of eight epilogue warps
+// (lane quarter x column half), added in the same order as the kernel above.
+//   warps 0-7  : converters, two groups alternating k-blocks (thread = tile row)
+//   warps 8-15 : epilogue
+//   warp 16    : MMA issuer; warp 17: TMA issuer (lane 0: A boxes, lane 1: B images)
+constexpr int TS_RA = 3, TS_RB = 3;
+constexpr int TS_EPI_WARP0 = 8, TS_MMA_WARP = 16, TS_TMA_WARP = 17, TS_THREADS = 32 * 19;
+
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+
+// y[0 .. CH) += TMEM columns taddr .. taddr + CH of this thread's lane
+template <int CH>
+__device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* y) {
+  static_assert(CH % 4 == 0, "column halves come in multiples of 4");
+#pragma unroll
+  for (int c0 = 0; c0 + 16 <= CH; c0 += 16) {
+    uint32_t x[16];
+    tmem_ld16(taddr + (uint32_t)c0, x);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) y[c0 + j] += __uint_as_float(x[j]);
+  }
+  constexpr int R0 = CH / 16 * 16;
+  if constexpr (CH - R0 >= 8) {
+    uint32_t x[8];
+    tmem_ld8(taddr + (uint32_t)R0, x);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[R0 + j] += __uint_as_float(x[j]);
+  }
+  constexpr int R1 = CH / 8 * 8;
+  if constexpr (CH - R1 >= 4) {
+    uint32_t x[4];
+    tmem_ld4(taddr + (uint32_t)R1, x);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 4; ++j) y[R1 + j] += __uint_as_float(x[j]);
+  }
+}
+
+// Epilogue of one warp: columns [C0, C0 + CW) of its 32 lanes. Chunk partial sums X[c & 1] are
+// added into registers in chunk order, then the tile rows are stored.
+template <int BN, int C0, int CW>
+__device__ __forceinline__ void ts_epilogue(uint32_t tl, int c0, int nchunks, uint64_t* xfull, uint64_t* xfree, int64_t row,
+                                            int64_t M, int64_t N, int64_t n0, double alpha, double beta, float* C,
+                                            int64_t c_rs, int64_t c_cs, float* wsz, int dbg) {
+  float y[CW];
+#pragma unroll
+  for (int j = 0; j < CW; ++j) y[j] = 0.f;
+  for (int c = c0; c < c0 + nchunks; ++c) {
+    const int xb = c & 1;
+    mbar_wait(smem_u32(&xfull[xb]), (uint32_t)((c / 2) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (!(dbg & 4)) tmem_add_cols<CW>(tl + (uint32_t)(xb * BN + C0), y);
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    mbar_arrive(smem_u32(&xfree[xb]));
+  }
+  if (row >= M || (dbg & 16)) return;
+#pragma unroll
+  for (int j = 0; j < CW; ++j) {
+    const int64_t col = n0 + C0 + j;
+    if (col < N) {
+      if (wsz) {
+        wsz[row * N + col] = y[j];
+      } else {
+        float* cp = C + row * c_rs + col * c_cs;
+        *cp = beta == 0.0 ? (float)(alpha * y[j]) : (float)(alpha * y[j] + beta * *cp);
+      }
+    }
+  }
+}
+
+template <bool A_KC, int BN>
+__global__ void __launch_bounds__(TS_THREADS, 1)
+    gemm_bf16x3_ts_kernel(int64_t M, int64_t N, int64_t K, int64_t kchunk, const uint8_t* __restrict__ bimg,
+                          int64_t nkb_total, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, float* ws,
+                          const __grid_constant__ CUtensorMap amap, int mtiles, int nblk, int total_work, int dbg) {
+  static_assert(TC_BK == 64, "the TMEM A stages hold 64-k blocks");
+  static_assert(BN % 8 == 0 && BN <= 160, "two fp32 partial buffers + A stages must fit 512 TMEM columns");
+  constexpr int PKB = TC_PROMOTE_KB;
+  constexpr int A_RAW = TC_BM * TC_BK * 4;  // fp32 tile landed by TMA
+  constexpr int B_TILE = BN * ROWB;
+  constexpr int B_STAGE = 2 * B_TILE;       // hi | lo images
+  constexpr int TA = (512 - 2 * BN) / 64 > 4 ? 4 : (512 - 2 * BN) / 64;
+  static_assert(TA >= 2, "at least two TMEM A stages");
+  // accumulator columns per epilogue warp: halves [0, CH) and [CH, BN), both starting on
+  // an 8-column boundary
+  constexpr int CH = (BN / 2 + 7) / 8 * 8;
+  constexpr uint32_t COL_A = 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* araw = smem;                      // [TS_RA][A_RAW]
+  uint8_t* bring = smem + TS_RA * A_RAW;     // [TS_RB][B_STAGE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + TS_RB * B_STAGE);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + TS_RA;
+  uint64_t* b_full = a_empty + TS_RA;
+  uint64_t* b_empty = b_full + TS_RB;
+  uint64_t* t_full = b_empty + TS_RB;
+  uint64_t* t_empty = t_full + TA;
+  uint64_t* xfull = t_empty + TA;
+  uint64_t* xfree = xfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // Work item w = (split z, N tile, M tile), M tile fastest: the CTAs of the
+  // grid walk w = blockIdx.x, + gridDim.x, ... so at any time they share one
+  // k range of B through L2. All roles run the same list; ring stages and
+  // mbarrier phases follow the running k-block count g and chunk count cg.
+  struct Work {
+    int64_t m0, n0, kbeg;
+    int nt, z, nkb;
+  };
+  auto decode = [&](int w) {
+    Work k;
+    const int per = mtiles * nblk;
+    k.z = w / per;
+    const int rem = w - k.z * per;
+    k.nt = rem / mtiles;
+    k.m0 = (int64_t)(rem - k.nt * mtiles) * TC_BM;
+    k.n0 = (int64_t)k.nt * BN;
+    k.kbeg = (int64_t)k.z * kchunk;
+    const int64_t kend = min(K, k.kbeg + kchunk);
+    k.nkb = kend > k.kbeg ? (int)((kend - k.kbeg + TC_BK - 1) / TC_BK) : 0;
+    return k;
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < TS_RA; ++s) {
+      mbar_init(smem_u32(&a_full[s]), 1);
+      mbar_init(smem_u32(&a_empty[s]), TC_GROUP);
+    }
+    for (int s = 0; s < TS_RB; ++s) {
+      mbar_init(smem_u32(&b_full[s]), 1);
+      mbar_init(smem_u32(&b_empty[s]), 1);
+    }
+    for (int s = 0; s < TA; ++s) {
+      mbar_init(smem_u32(&t_full[s]), TC_GROUP);
+      mbar_init(smem_u32(&t_empty[s]), 1);
+    }
+    mbar_init(smem_u32(&xfull[0]), 1);
+    mbar_init(smem_u32(&xfull[1]), 1);
+    mbar_init(smem_u32(&xfree[0]), 256);
+    mbar_init(smem_u32(&xfree[1]), 256);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == TS_EPI_WARP0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < TS_EPI_WARP0) {
+    // ---------------- converters: thread = tile row (TMEM lane), group = k-block parity ----------------
+    const int grp = warp >> 2, r = (warp & 3) * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16) + COL_A;
+    int g0 = 0;
+    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      const Work wk = decode(w);
+      for (int kb = (g0 + grp) & 1; kb < wk.nkb; kb += 2) {
+        const int g = g0 + kb;
+        const int sa = g % TS_RA, ta = g % TA;
+        // The ring stages are shared by the two groups (g - RA belongs to the
+        // other group), so a parity wait could alias a phase two steps back:
+        // first make sure the previous use of the stage was consumed (then
+        // a_full is in, or past, the phase of g).
+        if (g >= TS_RA) mbar_wait(smem_u32(&a_empty[sa]), (uint32_t)(((g / TS_RA) - 1) & 1));
+        mbar_wait(smem_u32(&a_full[sa]), (uint32_t)((g / TS_RA) & 1));
+        const uint8_t* base = araw + sa * A_RAW;
+        float f[64];
+        if (dbg & 8) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) f[k] = 1.f;
+        } else if (A_KC) {  // two SWIZZLE_128B boxes of 32 k: row r at r * 128, 16-B granule gr at (gr ^ (r & 7)) * 16
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int gr = 0; gr < 8; ++gr) {
+              const float4 v =
+                  *reinterpret_cast<const float4*>(base + b * (TC_BM * 128) + r * 128 + ((gr ^ (r & 7)) << 4));
+              f[32 * b + 4 * gr] = v.x; f[32 * b + 4 * gr + 1] = v.y; f[32 * b + 4 * gr + 2] = v.z;
+              f[32 * b + 4 * gr + 3] = v.w;
+            }
+        } else {  // [64 k][128 rows]
+          const float* t = reinterpret_cast<const float*>(base);
+#pragma unroll
+          for (int k = 0; k < 64; ++k) f[k] = t[k * TC_BM + r];
+        }
+        // split before releasing the raw stage: the arrive below then depends on
+        // every loaded value (an arrive right after the loads let the TMA refill
+        // the stage under loads still in flight: nondeterministic rows)
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint4 a, b;
+          split8(f + 8 * u, a, b);
+          hi[4 * u] = a.x; hi[4 * u + 1] = a.y; hi[4 * u + 2] = a.z; hi[4 * u + 3] = a.w;
+          lo[4 * u] = b.x; lo[4 * u + 1] = b.y; lo[4 * u + 2] = b.z; lo[4 * u + 3] = b.w;
+        }
+        {
+          uint32_t dep = 0;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) dep |= lo[u];
+          asm volatile("" ::"r"(dep) : "memory");  // all splits done (hence all loads returned)
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(smem_u32(&a_empty[sa]));
+        if (g >= TA) {  // same for the TMEM stage: g - TA written by the other group, then read by its MMAs
+          mbar_wait(smem_u32(&t_full[ta]), (uint32_t)(((g / TA) - 1) & 1));
+          mbar_wait(smem_u32(&t_empty[ta]), (uint32_t)(((g / TA) - 1) & 1));
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        if (!(dbg & 2)) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // 32 k -> 16 columns of hi and of lo
+          tmem_st16(tl + (uint32_t)(ta * 64 + 16 * h), hi + 16 * h);
+          tmem_st16(tl + (uint32_t)(ta * 64 + 32 + 16 * h), lo + 16 * h);
+        }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        mbar_arrive(smem_u32(&t_full[ta]));
+      }
+      g0 += wk.nkb;
+    }
+  } else if (warp == TS_TMA_WARP) {
+    if (lane == 0) {  // A: fp32 boxes into the raw ring
+      int g0 = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        const Work wk = decode(w);
+        for (int kb = 0; kb < wk.nkb; ++kb) {
+          const int g = g0 + kb, sa = g % TS_RA;
+          if (g >= TS_RA) mbar_wait(smem_u32(&a_empty[sa]), (uint32_t)(((g / TS_RA) - 1) & 1));
+          const uint32_t bar = smem_u32(&a_full[sa]);
+          if (dbg & 512) {
+            mbar_arrive(bar);
+            continue;
+          }
+          mbar_arrive_expect_tx(bar, (uint32_t)A_RAW);
+          const int k0 = (int)(wk.kbeg + (int64_t)kb * TC_BK);
+          uint8_t* base = araw + sa * A_RAW;
+          if (A_KC) {
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+              tma_load_2d_g2s(smem_u32(base + b * TC_BM * 128), &amap, k0 + 32 * b, (int)wk.m0, bar);
+          } else {
+            tma_load_2d_g2s(smem_u32(base), &amap, (int)wk.m0, k0, bar);
+          }
+        }
+        g0 += wk.nkb;
+      }
+    }
+  } else if (warp == TS_TMA_WARP + 1) {
+    if (lane == 0) {  // B: pre-split hi/lo images
+      int g0 = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        const Work wk = decode(w);
+        const uint8_t* bsrc = bimg + ((int64_t)wk.nt * nkb_total + wk.kbeg / TC_BK) * (int64_t)B_STAGE;
+        for (int kb = 0; kb < wk.nkb; ++kb) {
+          const int g = g0 + kb, sb = g % TS_RB;
+          if (g >= TS_RB) mbar_wait(smem_u32(&b_empty[sb]), (uint32_t)(((g / TS_RB) - 1) & 1));
+          const uint32_t bar = smem_u32(&b_full[sb]);
+          if (dbg & 32) {
+            mbar_arrive(bar);
+          } else {
+            mbar_arrive_expect_tx(bar, (uint32_t)B_STAGE);
+            bulk_copy_g2s(smem_u32(bring + sb * B_STAGE), bsrc + (int64_t)kb * B_STAGE, B_STAGE, bar);
+          }
+        }
+        g0 += wk.nkb;
+      }
+    }
+    __syncwarp();
+  } else if (warp == TS_MMA_WARP) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BN);
+      int g0 = 0, c0 = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        const Work wk = decode(w);
+        for (int kb = 0; kb < wk.nkb; ++kb) {
+          const int g = g0 + kb, sb = g % TS_RB, ta = g % TA;
+          const int cg = c0 + kb / PKB, xb = cg & 1, kin = kb % PKB;
+          if (kin == 0 && cg >= 2) mbar_wait(smem_u32(&xfree[xb]), (uint32_t)(((cg / 2) - 1) & 1));
+          mbar_wait(smem_u32(&b_full[sb]), (uint32_t)((g / TS_RB) & 1));
+          mbar_wait(smem_u32(&t_full[ta]), (uint32_t)((g / TA) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t dst = tmem + (uint32_t)(xb * BN);
+          const uint32_t acol = tmem + COL_A + (uint32_t)(ta * 64);
+          const uint32_t bbase = smem_u32(bring + sb * B_STAGE);
+          constexpr int PI[3] = {0, 0, 1}, PJ[3] = {0, 1, 0};  // hi*hi, hi*lo, lo*hi
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+              const uint32_t acc = (p > 0 || kin > 0 || kk > 0) ? 1u : 0u;
+              if (!(dbg & 1))
+              mma_bf16_ts(dst, acol + (uint32_t)(PI[p] * 32 + kk * 8),
+                          kmajor_sw128_desc(bbase + PJ[p] * B_TILE + kk * 32), idesc, acc);
+            }
+          }
+          if (dbg & 1024) {
+            mbar_arrive(smem_u32(&t_empty[ta]));
+            mbar_arrive(smem_u32(&b_empty[sb]));
+            if (kin == PKB - 1 || kb == wk.nkb - 1) mbar_arrive(smem_u32(&xfull[xb]));
+            continue;
+          }
+          mma_commit(smem_u32(&t_empty[ta]));
+          mma_commit(smem_u32(&b_empty[sb]));
+          if (kin == PKB - 1 || kb == wk.nkb - 1) mma_commit(smem_u32(&xfull[xb]));
+        }
+        g0 += wk.nkb;
+        c0 += (wk.nkb + PKB - 1) / PKB;
+      }
+      // drain: the commits to t_empty / b_empty of the last k-blocks must have
+      // arrived before the CTA exits
+      for (int g = max(0, g0 - TA); g < g0; ++g) mbar_wait(smem_u32(&t_empty[g % TA]), (uint32_t)((g / TA) & 1));
+      for (int g = max(0, g0 - TS_RB); g < g0; ++g)
+        mbar_wait(smem_u32(&b_empty[g % TS_RB]), (uint32_t)((g / TS_RB) & 1));
+    }
+    __syncwarp();
+  } else if (warp < TS_MMA_WARP) {
+    // ---------------- epilogue: Y in registers, lane quarter x column half ----------------
+    const int quarter = warp & 3;
+    const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
+    int c0 = 0;
+    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      const Work wk = decode(w);
+      const int64_t row = wk.m0 + quarter * 32 + lane;
+      const int nchunks = (wk.nkb + PKB - 1) / PKB;
+      float* wsz = ws ? ws + (int64_t)wk.z * M * N : nullptr;
+      if (warp - TS_EPI_WARP0 < 4)
+        ts_epilogue<BN, 0, CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz, dbg);
+      else
+        ts_epilogue<BN, CH, BN - CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz, dbg);
+      c0 += nchunks;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == TS_EPI_WARP0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <bool A_KC, int BN>
+void launch_tc_ts(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* B,
+                  int64_t b_rs, int64_t b_cs, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, float* ws,
+                  const CUtensorMap* amap) {
+  const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
+  DevBuf img(2 * (size_t)BN * ROWB * (size_t)(nkb * nblk), ctx->stream);
+  split_b_image<2><<<grid_for(ctx, nblk * nkb * BN * QPR, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb,
+                                                                                       nblk, img.as<uint8_t>());
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+  const size_t smem = (size_t)TS_RA * TC_BM * TC_BK * 4 + (size_t)TS_RB * 2 * BN * ROWB + 1024 + 8 * 32 + 16;
+  auto kern = gemm_bf16x3_ts_kernel<A_KC, BN>;
+  ensure_dyn_smem((const void*)kern, smem);
+  const int64_t mtiles = (m + TC_BM - 1) / TC_BM, total = mtiles * nblk * splits;
+  const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
+  if (std::getenv("RNLA_TS_TRACE"))
+    std::fprintf(stderr, "[ts] A_KC=%d BN=%d m=%lld n=%lld k=%lld kchunk=%lld splits=%d grid=%d total=%lld ws=%p C=%p c_rs=%lld c_cs=%lld\n",
+                 (int)A_KC, BN, (long long)m, (long long)n, (long long)k, (long long)kchunk, splits, grid, (long long)total,
+                 (void*)ws, (void*)C, (long long)c_rs, (long long)c_cs);
+  kern<<<grid, TS_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs, ws,
+                                                *amap, (int)mtiles, (int)nblk, (int)total,
+                                                std::getenv("RNLA_TS_DBG") ? std::atoi(std::getenv("RNLA_TS_DBG")) : 0);
+  RNLA_CUDA(cudaGetLastError());
+  note_launch(ctx);
+}
+
 template <bool A_KC, int BN, int STAGES, bool DF, bool TMA_A>
 void launch_tc(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* A,
                int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double alpha, double beta,
@@ -989,6 +1402,20 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
                                                     b_cs, alpha, beta, C, c_rs, c_cs, ws, sym, nullptr,        \
                                                     rownorm);                                                  \
   } while (0)
+  if constexpr (!DF) {
+    // plain products with one wide N tile: the A-in-TMEM kernel (see above)
+    static const bool no_ts = std::getenv("RNLA_TC_NO_TS") != nullptr;
+    const int dbgsel = std::getenv("RNLA_TS_DBG") ? std::atoi(std::getenv("RNLA_TS_DBG")) : 0;
+    const bool dbg_skip = ((dbgsel & 64) && !A_KC) || ((dbgsel & 128) && A_KC);
+    if (!dbg_skip && !no_ts && amap && sym == 0 && !rownorm && bn > 128 &&
+        ((m + TC_BM - 1) / TC_BM) * ((n + bn - 1) / bn) * splits < ((int64_t)1 << 30)) {
+      if (bn <= 152)
+        launch_tc_ts<A_KC, 152>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
+      else
+        launch_tc_ts<A_KC, 160>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
+      return;
+    }
+  }
   if (bn <= 32) RNLA_TC(32);
   else if (bn <= 64) RNLA_TC(64);
   else if (bn <= 96) RNLA_TC(96);
