@@ -913,7 +913,7 @@ __global__ void __launch_bounds__(TC_THREADS + 32, 1)
 // (lane quarter x column half), added in the same order as the kernel above.
 //   warps 0-7  : converters, two groups alternating k-blocks (thread = tile row)
 //   warps 8-15 : epilogue
-//   warp 16    : MMA issuer; warp 17: TMA issuer (lane 0: A boxes, lane 1: B images)
+//   warp 16    : MMA issuer; warp 17: TMA issuer of the A boxes; warp 18: bulk copies of the B images
 constexpr int TS_RA = 3, TS_RB = 3;
 constexpr int TS_EPI_WARP0 = 8, TS_MMA_WARP = 16, TS_TMA_WARP = 17, TS_THREADS = 32 * 19;
 
@@ -932,39 +932,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
                : "r"(taddr));
 }
 
-__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* v) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-               : "r"(taddr));
-}
-
-// y[0 .. CH) += TMEM columns taddr .. taddr + CH of this thread's lane
+// y[0 .. CH) += TMEM columns taddr .. taddr + CH of this thread's lane (8 columns per load:
+// the accumulator already takes most of the 96 registers a thread of this kernel has)
 template <int CH>
 __device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* y) {
-  static_assert(CH % 4 == 0, "column halves come in multiples of 4");
+  static_assert(CH % 8 == 0, "column halves come in multiples of 8");
 #pragma unroll
-  for (int c0 = 0; c0 + 16 <= CH; c0 += 16) {
-    uint32_t x[16];
-    tmem_ld16(taddr + (uint32_t)c0, x);
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 16; ++j) y[c0 + j] += __uint_as_float(x[j]);
-  }
-  constexpr int R0 = CH / 16 * 16;
-  if constexpr (CH - R0 >= 8) {
+  for (int c0 = 0; c0 < CH; c0 += 8) {
     uint32_t x[8];
-    tmem_ld8(taddr + (uint32_t)R0, x);
+    tmem_ld8(taddr + (uint32_t)c0, x);
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-    for (int j = 0; j < 8; ++j) y[R0 + j] += __uint_as_float(x[j]);
-  }
-  constexpr int R1 = CH / 8 * 8;
-  if constexpr (CH - R1 >= 4) {
-    uint32_t x[4];
-    tmem_ld4(taddr + (uint32_t)R1, x);
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 4; ++j) y[R1 + j] += __uint_as_float(x[j]);
+    for (int j = 0; j < 8; ++j) y[c0 + j] += __uint_as_float(x[j]);
   }
 }
 
@@ -973,7 +952,7 @@ __device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* y) {
 template <int BN, int C0, int CW>
 __device__ __forceinline__ void ts_epilogue(uint32_t tl, int c0, int nchunks, uint64_t* xfull, uint64_t* xfree, int64_t row,
                                             int64_t M, int64_t N, int64_t n0, double alpha, double beta, float* C,
-                                            int64_t c_rs, int64_t c_cs, float* wsz, int dbg) {
+                                            int64_t c_rs, int64_t c_cs, float* wsz) {
   float y[CW];
 #pragma unroll
   for (int j = 0; j < CW; ++j) y[j] = 0.f;
@@ -981,11 +960,11 @@ __device__ __forceinline__ void ts_epilogue(uint32_t tl, int c0, int nchunks, ui
     const int xb = c & 1;
     mbar_wait(smem_u32(&xfull[xb]), (uint32_t)((c / 2) & 1));
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (!(dbg & 4)) tmem_add_cols<CW>(tl + (uint32_t)(xb * BN + C0), y);
+    tmem_add_cols<CW>(tl + (uint32_t)(xb * BN + C0), y);
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     mbar_arrive(smem_u32(&xfree[xb]));
   }
-  if (row >= M || (dbg & 16)) return;
+  if (row >= M) return;
 #pragma unroll
   for (int j = 0; j < CW; ++j) {
     const int64_t col = n0 + C0 + j;
@@ -1004,7 +983,7 @@ template <bool A_KC, int BN>
 __global__ void __launch_bounds__(TS_THREADS, 1)
     gemm_bf16x3_ts_kernel(int64_t M, int64_t N, int64_t K, int64_t kchunk, const uint8_t* __restrict__ bimg,
                           int64_t nkb_total, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, float* ws,
-                          const __grid_constant__ CUtensorMap amap, int mtiles, int nblk, int total_work, int dbg) {
+                          const __grid_constant__ CUtensorMap amap, int mtiles, int nblk, int total_work) {
   static_assert(TC_BK == 64, "the TMEM A stages hold 64-k blocks");
   static_assert(BN % 8 == 0 && BN <= 160, "two fp32 partial buffers + A stages must fit 512 TMEM columns");
   constexpr int PKB = TC_PROMOTE_KB;
@@ -1102,10 +1081,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         mbar_wait(smem_u32(&a_full[sa]), (uint32_t)((g / TS_RA) & 1));
         const uint8_t* base = araw + sa * A_RAW;
         float f[64];
-        if (dbg & 8) {
-#pragma unroll
-          for (int k = 0; k < 64; ++k) f[k] = 1.f;
-        } else if (A_KC) {  // two SWIZZLE_128B boxes of 32 k: row r at r * 128, 16-B granule gr at (gr ^ (r & 7)) * 16
+        if (A_KC) {  // two SWIZZLE_128B boxes of 32 k: row r at r * 128, 16-B granule gr at (gr ^ (r & 7)) * 16
 #pragma unroll
           for (int b = 0; b < 2; ++b)
 #pragma unroll
@@ -1144,12 +1120,10 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           mbar_wait(smem_u32(&t_empty[ta]), (uint32_t)(((g / TA) - 1) & 1));
         }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        if (!(dbg & 2)) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // 32 k -> 16 columns of hi and of lo
           tmem_st16(tl + (uint32_t)(ta * 64 + 16 * h), hi + 16 * h);
           tmem_st16(tl + (uint32_t)(ta * 64 + 32 + 16 * h), lo + 16 * h);
-        }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -1166,10 +1140,6 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           const int g = g0 + kb, sa = g % TS_RA;
           if (g >= TS_RA) mbar_wait(smem_u32(&a_empty[sa]), (uint32_t)(((g / TS_RA) - 1) & 1));
           const uint32_t bar = smem_u32(&a_full[sa]);
-          if (dbg & 512) {
-            mbar_arrive(bar);
-            continue;
-          }
           mbar_arrive_expect_tx(bar, (uint32_t)A_RAW);
           const int k0 = (int)(wk.kbeg + (int64_t)kb * TC_BK);
           uint8_t* base = araw + sa * A_RAW;
@@ -1194,12 +1164,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           const int g = g0 + kb, sb = g % TS_RB;
           if (g >= TS_RB) mbar_wait(smem_u32(&b_empty[sb]), (uint32_t)(((g / TS_RB) - 1) & 1));
           const uint32_t bar = smem_u32(&b_full[sb]);
-          if (dbg & 32) {
-            mbar_arrive(bar);
-          } else {
-            mbar_arrive_expect_tx(bar, (uint32_t)B_STAGE);
-            bulk_copy_g2s(smem_u32(bring + sb * B_STAGE), bsrc + (int64_t)kb * B_STAGE, B_STAGE, bar);
-          }
+          mbar_arrive_expect_tx(bar, (uint32_t)B_STAGE);
+          bulk_copy_g2s(smem_u32(bring + sb * B_STAGE), bsrc + (int64_t)kb * B_STAGE, B_STAGE, bar);
         }
         g0 += wk.nkb;
       }
@@ -1227,16 +1193,9 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
               const uint32_t acc = (p > 0 || kin > 0 || kk > 0) ? 1u : 0u;
-              if (!(dbg & 1))
               mma_bf16_ts(dst, acol + (uint32_t)(PI[p] * 32 + kk * 8),
                           kmajor_sw128_desc(bbase + PJ[p] * B_TILE + kk * 32), idesc, acc);
             }
-          }
-          if (dbg & 1024) {
-            mbar_arrive(smem_u32(&t_empty[ta]));
-            mbar_arrive(smem_u32(&b_empty[sb]));
-            if (kin == PKB - 1 || kb == wk.nkb - 1) mbar_arrive(smem_u32(&xfull[xb]));
-            continue;
           }
           mma_commit(smem_u32(&t_empty[ta]));
           mma_commit(smem_u32(&b_empty[sb]));
@@ -1263,9 +1222,9 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       const int nchunks = (wk.nkb + PKB - 1) / PKB;
       float* wsz = ws ? ws + (int64_t)wk.z * M * N : nullptr;
       if (warp - TS_EPI_WARP0 < 4)
-        ts_epilogue<BN, 0, CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz, dbg);
+        ts_epilogue<BN, 0, CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz);
       else
-        ts_epilogue<BN, CH, BN - CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz, dbg);
+        ts_epilogue<BN, CH, BN - CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz);
       c0 += nchunks;
     }
   }
@@ -1292,13 +1251,8 @@ void launch_tc_ts(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk
   ensure_dyn_smem((const void*)kern, smem);
   const int64_t mtiles = (m + TC_BM - 1) / TC_BM, total = mtiles * nblk * splits;
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  if (std::getenv("RNLA_TS_TRACE"))
-    std::fprintf(stderr, "[ts] A_KC=%d BN=%d m=%lld n=%lld k=%lld kchunk=%lld splits=%d grid=%d total=%lld ws=%p C=%p c_rs=%lld c_cs=%lld\n",
-                 (int)A_KC, BN, (long long)m, (long long)n, (long long)k, (long long)kchunk, splits, grid, (long long)total,
-                 (void*)ws, (void*)C, (long long)c_rs, (long long)c_cs);
   kern<<<grid, TS_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs, ws,
-                                                *amap, (int)mtiles, (int)nblk, (int)total,
-                                                std::getenv("RNLA_TS_DBG") ? std::atoi(std::getenv("RNLA_TS_DBG")) : 0);
+                                                *amap, (int)mtiles, (int)nblk, (int)total);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
 }
@@ -1405,9 +1359,7 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
   if constexpr (!DF) {
     // plain products with one wide N tile: the A-in-TMEM kernel (see above)
     static const bool no_ts = std::getenv("RNLA_TC_NO_TS") != nullptr;
-    const int dbgsel = std::getenv("RNLA_TS_DBG") ? std::atoi(std::getenv("RNLA_TS_DBG")) : 0;
-    const bool dbg_skip = ((dbgsel & 64) && !A_KC) || ((dbgsel & 128) && A_KC);
-    if (!dbg_skip && !no_ts && amap && sym == 0 && !rownorm && bn > 128 &&
+    if (!no_ts && amap && sym == 0 && !rownorm && bn > 128 &&
         ((m + TC_BM - 1) / TC_BM) * ((n + bn - 1) / bn) * splits < ((int64_t)1 << 30)) {
       if (bn <= 152)
         launch_tc_ts<A_KC, 152>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);

@@ -117,6 +117,36 @@ def test_prototype_fp32(ctx):
     assert np.max(np.abs(r.factors.singular_values - so) / so) <= 1e-3
 
 
+@pytest.mark.parametrize("m,n,s,q,order", [
+    (19000, 2048, 150, 1, "C"),   # 149 row tiles (tail of 56 rows), 4 chunks of 512 k; A'Q split over K with a k tail
+    (4096, 8192, 150, 0, "C"),    # several work items per persistent CTA (split K), 15 k-blocks each
+    (5000, 3000, 137, 1, "F"),    # column-major A: the [64 k][128 rows] TMA box feeds Y = A Omega
+    (9000, 1100, 160, 0, "C"),    # N = 160 tile, K not a multiple of 64
+])
+def test_prototype_fp32_wide_sketch_tmem_operand(ctx, m, n, s, q, order):
+    """fp32 projections with 128 < s <= 160 run the A-in-TMEM tcgen05 kernel
+    (gemm_tc.cu, gemm_bf16x3_ts_kernel); sigma against the fp64 oracle with the
+    same Omega (src/randsvd.cpp:88-110), gate 1e-3 (north_star fp32)."""
+    import torch
+    rng = np.random.default_rng(m + n + s)
+    r0 = 256
+    u, _ = np.linalg.qr(rng.standard_normal((m, r0)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r0)))
+    sig = np.arange(1, r0 + 1) ** -1.5
+    a = ((u * sig) @ v.T + 1e-4 * rng.standard_normal((m, n))).astype(np.float32)
+    da = torch.from_numpy(a).cuda()
+    if order == "F":
+        da = da.t().contiguous().t()
+    k = 100
+    r = rn.prototype_ksvd(da, k, s, 11, power_iters=q, ctx=ctx)
+    _, so, _, _ = orc.prototype_ksvd(a.astype(np.float64), k, s, 11, q=q)
+    assert np.max(np.abs(r.factors.singular_values - so) / so) <= 1e-3
+    # deterministic: the same call returns the same bits (the converter/TMA ring has no data race)
+    r2 = rn.prototype_ksvd(da, k, s, 11, power_iters=q, ctx=ctx)
+    assert np.array_equal(r.factors.singular_values, r2.factors.singular_values)
+    assert torch.equal(r.factors.U, r2.factors.U)
+
+
 def test_prototype_count_spec(ctx):
     a = orc.gaussian_matrix(300, 6, 8) @ orc.gaussian_matrix(6, 200, 9)
     r = rn.prototype_ksvd(a, 6, 30, 4, spec=rn.SketchSpec.count_sketch(30, 4), opts=rn.KsvdOptions(True), ctx=ctx)
