@@ -575,14 +575,22 @@ def run_gpu(args):
 
 def ncu_traffic_from_profiles():
     """dram bytes (read + write) per launch of the gather kernel from the
-    committed ncu --set full summary, or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_cs_gather_r01.json")
-    if os.path.exists(p):
-        try:
-            with open(p) as f:
+    committed ncu --set full summaries (the round-2 capture, else round 1), or None."""
+    def _num(v):
+        x, unit = str(v).split()[:2] if " " in str(v) else (v, "byte")
+        return float(x) * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
+    p2 = os.path.join(ROOT, "profiles", "ncu_cs_gather_r02.json")
+    p1 = os.path.join(ROOT, "profiles", "ncu_cs_gather_r01.json")
+    try:
+        if os.path.exists(p2):
+            with open(p2) as f:
+                e = [k for k in json.load(f) if "cs_gather_kernel" in k.get("Kernel Name", "")][0]
+            return _num(e["dram__bytes_read.sum"]) + _num(e["dram__bytes_write.sum"])
+        if os.path.exists(p1):
+            with open(p1) as f:
                 return json.load(f).get("dram_bytes_per_launch")
-        except Exception:
-            return None
+    except Exception:
+        return None
     return None
 
 
