@@ -952,7 +952,7 @@ __device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* y) {
 template <int BN, int C0, int CW>
 __device__ __forceinline__ void ts_epilogue(uint32_t tl, int c0, int nchunks, uint64_t* xfull, uint64_t* xfree, int64_t row,
                                             int64_t M, int64_t N, int64_t n0, double alpha, double beta, float* C,
-                                            int64_t c_rs, int64_t c_cs, float* wsz) {
+                                            int64_t c_rs, int64_t c_cs, float* wsz, double* rn) {
   float y[CW];
 #pragma unroll
   for (int j = 0; j < CW; ++j) y[j] = 0.f;
@@ -965,6 +965,17 @@ __device__ __forceinline__ void ts_epilogue(uint32_t tl, int c0, int nchunks, ui
     mbar_arrive(smem_u32(&xfree[xb]));
   }
   if (row >= M) return;
+  if (rn) {  // row-norm mode: sum of squares of this half tile's columns, C not written
+    double rsq = 0.0;
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+      if (n0 + C0 + j < N) {
+        const double v = alpha * (double)y[j];
+        rsq += v * v;
+      }
+    rn[row] = rsq;
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < CW; ++j) {
     const int64_t col = n0 + C0 + j;
@@ -983,7 +994,8 @@ template <bool A_KC, int BN>
 __global__ void __launch_bounds__(TS_THREADS, 1)
     gemm_bf16x3_ts_kernel(int64_t M, int64_t N, int64_t K, int64_t kchunk, const uint8_t* __restrict__ bimg,
                           int64_t nkb_total, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, float* ws,
-                          const __grid_constant__ CUtensorMap amap, int mtiles, int nblk, int total_work) {
+                          const __grid_constant__ CUtensorMap amap, int mtiles, int nblk, int total_work, int flags,
+                          double* rownorm) {
   static_assert(TC_BK == 64, "the TMEM A stages hold 64-k blocks");
   static_assert(BN % 8 == 0 && BN <= 160, "two fp32 partial buffers + A stages must fit 512 TMEM columns");
   constexpr int PKB = TC_PROMOTE_KB;
@@ -1016,22 +1028,40 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   // grid walk w = blockIdx.x, + gridDim.x, ... so at any time they share one
   // k range of B through L2. All roles run the same list; ring stages and
   // mbarrier phases follow the running k-block count g and chunk count cg.
+  // Triangular B (flags bit 1: B(p, j) = 0 for p > j, the leverage product
+  // M R^-1): N tile j needs k < (j + 1) BN only, so a CTA takes the tiles in
+  // pairs (j, nblk - 1 - j) of equal total length, the pairs of one M tile on
+  // neighbouring CTAs (its A rows are shared through L2).
   struct Work {
     int64_t m0, n0, kbeg;
     int nt, z, nkb;
   };
-  auto decode = [&](int w) {
-    Work k;
-    const int per = mtiles * nblk;
-    k.z = w / per;
-    const int rem = w - k.z * per;
-    k.nt = rem / mtiles;
-    k.m0 = (int64_t)(rem - k.nt * mtiles) * TC_BM;
+  const bool tri = (flags & 2) != 0, pairs = tri && nblk % 2 == 0;
+  auto item = [&](int t, Work& k) -> bool {
+    int mt;
+    if (pairs) {
+      const int pw = (int)blockIdx.x + (t >> 1) * (int)gridDim.x, hp = nblk / 2;
+      if (pw >= total_work / 2) return false;
+      mt = pw / hp;
+      const int pp = pw - mt * hp;
+      k.nt = (t & 1) ? nblk - 1 - pp : pp;
+      k.z = 0;
+    } else {
+      const int w = (int)blockIdx.x + t * (int)gridDim.x;
+      if (w >= total_work) return false;
+      const int per = mtiles * nblk;
+      k.z = w / per;
+      const int rem = w - k.z * per;
+      k.nt = rem / mtiles;
+      mt = rem - k.nt * mtiles;
+    }
+    k.m0 = (int64_t)mt * TC_BM;
     k.n0 = (int64_t)k.nt * BN;
     k.kbeg = (int64_t)k.z * kchunk;
-    const int64_t kend = min(K, k.kbeg + kchunk);
+    int64_t kend = min(K, k.kbeg + kchunk);
+    if (tri) kend = min(kend, k.n0 + BN);
     k.nkb = kend > k.kbeg ? (int)((kend - k.kbeg + TC_BK - 1) / TC_BK) : 0;
-    return k;
+    return true;
   };
 
   if (tid == 0) {
@@ -1068,8 +1098,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
     const int grp = warp >> 2, r = (warp & 3) * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16) + COL_A;
     int g0 = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
-      const Work wk = decode(w);
+    Work wk;
+    for (int t = 0; item(t, wk); ++t) {
       for (int kb = (g0 + grp) & 1; kb < wk.nkb; kb += 2) {
         const int g = g0 + kb;
         const int sa = g % TS_RA, ta = g % TA;
@@ -1134,8 +1164,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   } else if (warp == TS_TMA_WARP) {
     if (lane == 0) {  // A: fp32 boxes into the raw ring
       int g0 = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
-        const Work wk = decode(w);
+      Work wk;
+      for (int t = 0; item(t, wk); ++t) {
         for (int kb = 0; kb < wk.nkb; ++kb) {
           const int g = g0 + kb, sa = g % TS_RA;
           if (g >= TS_RA) mbar_wait(smem_u32(&a_empty[sa]), (uint32_t)(((g / TS_RA) - 1) & 1));
@@ -1157,8 +1187,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   } else if (warp == TS_TMA_WARP + 1) {
     if (lane == 0) {  // B: pre-split hi/lo images
       int g0 = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
-        const Work wk = decode(w);
+      Work wk;
+      for (int t = 0; item(t, wk); ++t) {
         const uint8_t* bsrc = bimg + ((int64_t)wk.nt * nkb_total + wk.kbeg / TC_BK) * (int64_t)B_STAGE;
         for (int kb = 0; kb < wk.nkb; ++kb) {
           const int g = g0 + kb, sb = g % TS_RB;
@@ -1175,8 +1205,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(BN);
       int g0 = 0, c0 = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
-        const Work wk = decode(w);
+      Work wk;
+      for (int t = 0; item(t, wk); ++t) {
         for (int kb = 0; kb < wk.nkb; ++kb) {
           const int g = g0 + kb, sb = g % TS_RB, ta = g % TA;
           const int cg = c0 + kb / PKB, xb = cg & 1, kin = kb % PKB;
@@ -1216,15 +1246,18 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
     const int quarter = warp & 3;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     int c0 = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
-      const Work wk = decode(w);
+    Work wk;
+    for (int t = 0; item(t, wk); ++t) {
       const int64_t row = wk.m0 + quarter * 32 + lane;
       const int nchunks = (wk.nkb + PKB - 1) / PKB;
       float* wsz = ws ? ws + (int64_t)wk.z * M * N : nullptr;
+      // row norms: [2 nt + column half][row]
+      double* rn0 = rownorm ? rownorm + (int64_t)(2 * wk.nt) * M : nullptr;
       if (warp - TS_EPI_WARP0 < 4)
-        ts_epilogue<BN, 0, CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz);
+        ts_epilogue<BN, 0, CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz, rn0);
       else
-        ts_epilogue<BN, CH, BN - CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz);
+        ts_epilogue<BN, CH, BN - CH>(tl, c0, nchunks, xfull, xfree, row, M, N, wk.n0, alpha, beta, C, c_rs, c_cs, wsz,
+                                     rn0 ? rn0 + M : nullptr);
       c0 += nchunks;
     }
   }
@@ -1239,7 +1272,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
 template <bool A_KC, int BN>
 void launch_tc_ts(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk, int splits, const float* B,
                   int64_t b_rs, int64_t b_cs, double alpha, double beta, float* C, int64_t c_rs, int64_t c_cs, float* ws,
-                  const CUtensorMap* amap) {
+                  const CUtensorMap* amap, int flags = 0, double* rownorm = nullptr) {
   const int64_t nkb = std::max<int64_t>(1, (k + TC_BK - 1) / TC_BK), nblk = (n + BN - 1) / BN;
   DevBuf img(2 * (size_t)BN * ROWB * (size_t)(nkb * nblk), ctx->stream);
   split_b_image<2><<<grid_for(ctx, nblk * nkb * BN * QPR, 256), 256, 0, ctx->stream>>>(k, n, B, b_rs, b_cs, BN, nkb,
@@ -1250,11 +1283,19 @@ void launch_tc_ts(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t kchunk
   auto kern = gemm_bf16x3_ts_kernel<A_KC, BN>;
   ensure_dyn_smem((const void*)kern, smem);
   const int64_t mtiles = (m + TC_BM - 1) / TC_BM, total = mtiles * nblk * splits;
-  const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
+  const bool pairs = (flags & 2) && nblk % 2 == 0;
+  const int grid = (int)std::min<int64_t>(pairs ? total / 2 : total, ctx->num_sms);
   kern<<<grid, TS_THREADS, smem, ctx->stream>>>(m, n, k, kchunk, img.as<uint8_t>(), nkb, alpha, beta, C, c_rs, c_cs, ws,
-                                                *amap, (int)mtiles, (int)nblk, (int)total);
+                                                *amap, (int)mtiles, (int)nblk, (int)total, flags, rownorm);
   RNLA_CUDA(cudaGetLastError());
   note_launch(ctx);
+}
+
+// Row norms of A B, B upper triangular, on the A-in-TMEM kernel (128-column
+// tiles, two partial sums per tile): the leverage-score product of config 2.
+bool ts_rownorm_eligible(int64_t m, int64_t n, int64_t k) {
+  static const bool no_ts = std::getenv("RNLA_TC_NO_TS") != nullptr;
+  return !no_ts && n > 160 && k >= 1 && ((m + TC_BM - 1) / TC_BM) * ((n + 127) / 128) < ((int64_t)1 << 30);
 }
 
 template <bool A_KC, int BN, int STAGES, bool DF, bool TMA_A>
@@ -1517,6 +1558,15 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
   const bool b_from_a = sym && tma && bn_full == TC_BM;
   const int flags = sym | (tri_b && !sym ? 2 : 0) | (b_from_a ? 8 : 0);
   if constexpr (!DF) {
+    if (rownorm && tri_b && !sym && tma && splits == 1 && ts_rownorm_eligible(m, n, k)) {
+      if (a_cs == 1)
+        launch_tc_ts<true, 128>(ctx, m, n, k, kchunk, 1, B, b_rs, b_cs, alpha, 0.0, nullptr, 0, 0, nullptr, &amap, 2,
+                                rownorm);
+      else
+        launch_tc_ts<false, 128>(ctx, m, n, k, kchunk, 1, B, b_rs, b_cs, alpha, 0.0, nullptr, 0, 0, nullptr, &amap, 2,
+                                 rownorm);
+      return;
+    }
     static const bool no_persist = std::getenv("RNLA_TC_NO_PERSIST") != nullptr;
     if (!no_persist && tma && splits == 1 && !sym) {
       const bool ok = a_cs == 1 ? try_tc_persist<true>(ctx, bn_eff, m, n, k, A, B, b_rs, b_cs, alpha, beta, C, c_rs,
@@ -1574,6 +1624,10 @@ void gemm_f32_tc_tri_b(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alp
 int gemm_f32_tc_tri_b_rownorm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
                               int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double* rownorm) {
   gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, 0.f, nullptr, 0, 0, true, rownorm);
+  {  // the A-in-TMEM kernel writes two partial sums (column halves) per 128-column tile
+    CUtensorMap probe;
+    if (ts_rownorm_eligible(m, n, k) && make_a_map(&probe, A, m, k, a_rs, a_cs)) return 2 * (int)((n + 127) / 128);
+  }
   const int bn = n <= 160 ? (int)(n > 128 ? ((n + 7) / 8) * 8 : ((n + 15) / 16) * 16) : 128;
   const int bn_eff = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 96 ? 96 : bn <= 128 ? 128 : bn <= 152 ? 152 : 160;
   return (int)((n + bn_eff - 1) / bn_eff);
