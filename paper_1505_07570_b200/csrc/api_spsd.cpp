@@ -356,9 +356,12 @@ void nystrom_eig_impl(rnla_ctx* ctx, const rnla_mat* x, double sigma, int64_t s,
     }
   } joiner{eig_thread};
   RNLA_CUDA(cudaMemsetAsync(G.p, 0, sizeof(double) * s * s, ctx->stream));
-  // 16 SMs measured best on config 4 (0 / 8 / 16 / 24 / 32 / 48: 13.2 / 12.4 /
-  // 11.8 / 12.0 / 12.2 / 11.9 ms)
-  reserve_sms = overlap ? 16 : 0;
+  // Measured on config 4 once the Gram ran on the int8 tensor cores and the
+  // kernel columns on tcgen05 (8 / 16 / 24 / 32 / 40 / 44 / 48 / 56 SMs: 9.47 /
+  // 9.23 / 8.65 / 8.56 / 8.43 / 8.44 / 8.48 / 8.69 ms): the faster the tensor-core
+  // stages, the more of the latency-bound Cholesky route is exposed, so it gets
+  // about a quarter of the SMs (r01, fp64 DMMA Gram: 16 was best).
+  reserve_sms = overlap ? std::max(1, (ctx->num_sms * 40 + 74) / 148) : 0;
   if (tc_rbf) {
     c_digits(0, n_local);
     if (std::getenv("RNLA_CHECK_W_DIGITS")) {  // W's digits == the landmark rows of C's digits?
