@@ -1493,7 +1493,7 @@ template <bool DF>
 void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t a_rs,
                   int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double beta,
                   typename std::conditional<DF, double, float>::type* C, int64_t c_rs, int64_t c_cs,
-                  bool tri_b = false, double* rownorm = nullptr) {
+                  bool tri_b = false, double* rownorm = nullptr, int* rownorm_parts = nullptr) {
   using OutT = typename std::conditional<DF, double, float>::type;
   if (m == 0 || n == 0) return;
   // one N tile up to 160 columns (3 fp32 accumulators fit TMEM; 128 with the
@@ -1565,6 +1565,7 @@ void gemm_tc_impl(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, 
       else
         launch_tc_ts<false, 128>(ctx, m, n, k, kchunk, 1, B, b_rs, b_cs, alpha, 0.0, nullptr, 0, 0, nullptr, &amap, 2,
                                  rownorm);
+      if (rownorm_parts) *rownorm_parts = 2 * (int)((n + 127) / 128);  // two column halves per 128-column tile
       return;
     }
     static const bool no_persist = std::getenv("RNLA_TC_NO_PERSIST") != nullptr;
@@ -1623,11 +1624,9 @@ void gemm_f32_tc_tri_b(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alp
 // t < ntiles (returned). The caller adds the tiles in order.
 int gemm_f32_tc_tri_b_rownorm(rnla_ctx* ctx, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
                               int64_t a_rs, int64_t a_cs, const float* B, int64_t b_rs, int64_t b_cs, double* rownorm) {
-  gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, 0.f, nullptr, 0, 0, true, rownorm);
-  {  // the A-in-TMEM kernel writes two partial sums (column halves) per 128-column tile
-    CUtensorMap probe;
-    if (ts_rownorm_eligible(m, n, k) && make_a_map(&probe, A, m, k, a_rs, a_cs)) return 2 * (int)((n + 127) / 128);
-  }
+  int parts = 0;  // set by the A-in-TMEM path (two partial sums per tile)
+  gemm_tc_impl<false>(ctx, m, n, k, alpha, A, a_rs, a_cs, B, b_rs, b_cs, 0.f, nullptr, 0, 0, true, rownorm, &parts);
+  if (parts > 0) return parts;
   const int bn = n <= 160 ? (int)(n > 128 ? ((n + 7) / 8) * 8 : ((n + 15) / 16) * 16) : 128;
   const int bn_eff = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 96 ? 96 : bn <= 128 ? 128 : bn <= 152 ? 152 : 160;
   return (int)((n + bn_eff - 1) / bn_eff);
