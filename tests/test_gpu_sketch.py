@@ -306,6 +306,23 @@ def test_leverage_rows_given_identical_scores(ctx):
     assert np.max(np.abs(s32 - orc.row_leverage(m32.astype(np.float64))) / ref) <= 1e-4
 
 
+@pytest.mark.parametrize("n,d", [(20000, 200), (30000, 384), (9000, 1000)])
+def test_leverage_rows_fp32_wide_tmem_operand(ctx, n, d):
+    """fp32 row leverage with d > 160: the row norms of M R^-1 run on the A-in-TMEM
+    tcgen05 kernel (128-column tiles; d = 200: tile pairs with a column tail, d = 384:
+    odd tile count, d = 1000: four pairs). Scores against the fp64 oracle
+    (src/spsd.cpp:150 pattern), fp32 gate 1e-4; draws bit-exact given the scores."""
+    rng = np.random.default_rng(n + d)
+    m32 = rng.standard_t(3, size=(n, d)).astype(np.float32)
+    scores, idx = rn.leverage_sample_rows(dev(m32), 600, 5, ctx=ctx)
+    ref = orc.row_leverage(m32.astype(np.float64))
+    assert np.max(np.abs(scores - ref) / ref) <= 1e-4
+    assert abs(scores.sum() - d) <= 1e-4 * d
+    assert np.array_equal(idx, np.unique(orc.sample_with_replacement(scores, 600, 5)))
+    s2, _ = rn.leverage_sample_rows(dev(m32), 600, 5, ctx=ctx)
+    assert np.array_equal(scores, s2)
+
+
 # ---------------------------------------------------------------- lsr_sketched
 def test_lsr_sketched_count_matches_oracle(ctx):
     # tests/test_regression.cpp:44-52 + parity of x against the oracle on the same sketch
