@@ -1400,9 +1400,16 @@ void dispatch_bn(rnla_ctx* ctx, int bn, int64_t m, int64_t n, int64_t k, int64_t
   if constexpr (!DF) {
     // plain products with one wide N tile: the A-in-TMEM kernel (see above)
     static const bool no_ts = std::getenv("RNLA_TC_NO_TS") != nullptr;
-    if (!no_ts && amap && sym == 0 && !rownorm && bn > 128 &&
+    // (128 < N <= 160 always; 32 < N <= 128 for long K, where the A path is the bound)
+    if (!no_ts && amap && sym == 0 && !rownorm && (bn > 128 || (bn > 32 && k > 2 * TC_PROMOTE_KB * TC_BK)) &&
         ((m + TC_BM - 1) / TC_BM) * ((n + bn - 1) / bn) * splits < ((int64_t)1 << 30)) {
-      if (bn <= 152)
+      if (bn <= 64)
+        launch_tc_ts<A_KC, 64>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
+      else if (bn <= 96)
+        launch_tc_ts<A_KC, 96>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
+      else if (bn <= 128)
+        launch_tc_ts<A_KC, 128>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
+      else if (bn <= 152)
         launch_tc_ts<A_KC, 152>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
       else
         launch_tc_ts<A_KC, 160>(ctx, m, n, k, kchunk, splits, B, b_rs, b_cs, alpha, beta, C, c_rs, c_cs, ws, amap);
