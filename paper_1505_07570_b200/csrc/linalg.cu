@@ -686,10 +686,30 @@ __global__ void __launch_bounds__(kSmallCholThreads) small_chol_inv_kernel(int n
     for (int e = tid; e < cnt; e += nt) {
       const int I = e / (BS * BS), r = (e / BS) % BS, c = e % BS, J = I + d;
       const int row = I * BS + r, col = J * BS + c;
-      double acc = 0.0;
-      if (row < n && col < n)
-        for (int p = (I + 1) * BS; p <= col; ++p) acc += sm[row * ld + p] * getx(p, col);
-      Tb[e] = acc;
+      // four independent partial sums: the dependent fp64 FMA chain (up to 16 d
+      // terms) was the cost of this sweep, not the operation count. X(p, col) of
+      // the blocks between I and J sits transposed in the lower triangle
+      // (contiguous in p), the last block in Xd.
+      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+      if (row < n && col < n) {
+        const double* rr = sm + row * ld;
+        const double* xc = sm + col * ld;
+        for (int p = (I + 1) * BS; p < J * BS; p += 4) {
+          acc0 += rr[p] * xc[p];
+          acc1 += rr[p + 1] * xc[p + 1];
+          acc2 += rr[p + 2] * xc[p + 2];
+          acc3 += rr[p + 3] * xc[p + 3];
+        }
+        const double* xd = Xd + (size_t)J * BS * BS + c;
+        for (int t = 0; t <= c; ++t) {
+          const double v = rr[J * BS + t] * xd[t * BS];
+          if ((t & 3) == 0) acc0 += v;
+          else if ((t & 3) == 1) acc1 += v;
+          else if ((t & 3) == 2) acc2 += v;
+          else acc3 += v;
+        }
+      }
+      Tb[e] = (acc0 + acc1) + (acc2 + acc3);
     }
     __syncthreads();
     for (int e = tid; e < cnt; e += nt) {
