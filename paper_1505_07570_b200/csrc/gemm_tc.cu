@@ -20,8 +20,9 @@
 //                with fp32 CUDA-core adds (tcgen05.st), final alpha/beta store.
 // Global operands may be K-contiguous or MN-contiguous; the converting
 // loader always produces K-major smem, so only the K-major descriptor is used.
-// The fp32 data is read through registers because it has to be split before
-// the MMA anyway (a TMA copy would add an smem round trip).
+// The fp32 tile lands by TMA and is split by converter warps: in place into
+// shared-memory images (gemm_bf16x3_kernel / _persist) or into TMEM
+// (gemm_bf16x3_ts_kernel, the A operand then never touches shared memory again).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -891,8 +892,10 @@ __global__ void __launch_bounds__(TC_THREADS + 32, 1)
 }
 
 // ---------------------------------------------------------------------------
-// A-operand-in-TMEM variant (tcgen05.mma with [a_tmem]) for the long-K
-// projections of config 3 (Y = A Q, Z = A'Q; N <= 160 in one tile).
+// A-operand-in-TMEM variant (tcgen05.mma with [a_tmem]): the long-K
+// projections of config 3 (Y = A Q, Z = A'Q, 128 < N <= 160 in one tile), other
+// non-symmetric products with K > 1024 and 32 < N <= 128, and the leverage
+// row norms of config 2 (128-column tiles, triangular B, row-norm epilogue).
 //
 // Why: the smem-operand kernel above is bound by shared-memory bandwidth, not
 // by HBM or the tensor pipe (ncu, config-3 pass: LSU shared wavefronts 60 % of
