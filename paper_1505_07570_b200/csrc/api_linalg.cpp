@@ -1209,7 +1209,9 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
         std::copy(hs + r0, hs + r0 + rows, scores + r0);
       }
     };
+    WeightPrefix::Prepared prepared;
     if (stream_draw) {
+      prepared = WeightPrefix::prepare(seed, p);  // host work under the Gram / Cholesky already queued
       ev.resize((size_t)nblk);
       for (auto& e : ev) RNLA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       prefix.cum.reserve((size_t)n);
@@ -1261,7 +1263,7 @@ rnla_status rnla_leverage_sample_rows(rnla_ctx* ctx, const rnla_mat* m, int64_t 
     if (indices) {
       std::vector<int64_t> draws;
       if (stream_draw) {
-        draws = prefix.draw(seed, p);
+        draws = prefix.draw(prepared);
       } else {
         std::vector<double> all_scores;
         const double* w = scores;

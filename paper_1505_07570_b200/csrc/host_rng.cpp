@@ -79,24 +79,39 @@ void WeightPrefix::extend(const double* w, int64_t m) {
   total = t;
 }
 
-std::vector<int64_t> WeightPrefix::draw(uint64_t seed, int64_t count) const {
+WeightPrefix::Prepared WeightPrefix::prepare(uint64_t seed, int64_t count) {
+  require(count >= 1, "sample_with_replacement: count < 1");
+  Prepared pr;
+  std::mt19937_64 rng(seed);
+  pr.canon.resize(static_cast<size_t>(count));
+  // libstdc++'s uniform_real_distribution(a, b)(g) is generate_canonical<double, 53>(g) * (b - a) + a
+  // (bits/random.h), one engine word per draw; the scaling happens in draw()
+  for (int64_t i = 0; i < count; ++i) pr.canon[static_cast<size_t>(i)] = std::generate_canonical<double, 53>(rng);
+  pr.order.resize(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) pr.order[static_cast<size_t>(i)] = i;
+  // ascending canonical value = non-decreasing u (the scaling is monotone)
+  std::stable_sort(pr.order.begin(), pr.order.end(), [&](int64_t a, int64_t b) {
+    return pr.canon[static_cast<size_t>(a)] < pr.canon[static_cast<size_t>(b)];
+  });
+  return pr;
+}
+
+std::vector<int64_t> WeightPrefix::draw(uint64_t seed, int64_t count) const { return draw(prepare(seed, count)); }
+
+std::vector<int64_t> WeightPrefix::draw(const Prepared& pr) const {
+  const int64_t count = (int64_t)pr.canon.size();
   require(count >= 1, "sample_with_replacement: count < 1");
   require(total > 0.0, "sample_with_replacement: all weights zero");
   const int64_t n = (int64_t)cum.size();
-  std::mt19937_64 rng(seed);
-  std::uniform_real_distribution<double> unif(0.0, total);
   std::vector<double> u(static_cast<size_t>(count));
-  for (int64_t i = 0; i < count; ++i) u[static_cast<size_t>(i)] = unif(rng);
+  for (int64_t i = 0; i < count; ++i) u[static_cast<size_t>(i)] = pr.canon[static_cast<size_t>(i)] * (total - 0.0) + 0.0;
   // upper_bound(cum, u_i) for every draw, visiting the draws in ascending u
   // order: from the previous position a galloping search brackets the next
   // one and a binary search inside the bracket finishes (about log2(n / count)
   // probes near the last hit per draw, instead of count cold binary searches
   // over an n-element array or one linear sweep over all of it). cum is
   // non-decreasing, so these are exactly the upper_bound positions.
-  std::vector<int64_t> order(static_cast<size_t>(count));
-  for (int64_t i = 0; i < count; ++i) order[static_cast<size_t>(i)] = i;
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int64_t a, int64_t b) { return u[static_cast<size_t>(a)] < u[static_cast<size_t>(b)]; });
+  const std::vector<int64_t>& order = pr.order;
   std::vector<int64_t> out(static_cast<size_t>(count));
   const double* c = cum.data();
   // The sorted draws are cut into contiguous ranges searched by separate host

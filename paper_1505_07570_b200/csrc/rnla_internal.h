@@ -176,6 +176,16 @@ struct WeightPrefix {
   double total = 0.0;
   void extend(const double* w, int64_t m);
   std::vector<int64_t> draw(uint64_t seed, int64_t count) const;
+  // The part of the draw that does not depend on the weights: the engine's
+  // canonical uniforms in draw order and their ascending order. Prepared while
+  // the device still computes the scores, it leaves only the scaling by the
+  // total and the searches for draw(const Prepared&).
+  struct Prepared {
+    std::vector<double> canon;
+    std::vector<int64_t> order;
+  };
+  static Prepared prepare(uint64_t seed, int64_t count);
+  std::vector<int64_t> draw(const Prepared& pr) const;
 };
 void srht_operator_host(uint64_t seed, int64_t n, int64_t s, int8_t* signs, int64_t* idx);
 int64_t next_pow2(int64_t n);
