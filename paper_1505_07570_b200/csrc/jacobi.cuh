@@ -100,6 +100,23 @@ __global__ void __launch_bounds__(NT) jacobi_eig_kernel(int n, const double* __r
   int sweep = 0, conv = m <= 1;
   for (; sweep < 40 && !conv; ++sweep) {
     const int flag = sweep & 1;
+    // A sweep that starts with no pair above the rotation threshold rotates
+    // nothing (the matrix never changes), so it is recognized up front instead
+    // of being walked through round by round; same result, same sweep count.
+    {
+      int need = 0;
+      for (int e = tid; e < n * n; e += NT) {
+        const int p = e / n, q = e - p * n;
+        if (p != q) {  // both triangles: the rounds read A(p, q) in the tournament's order
+          const double apq = A[p * ld + q];
+          need |= fabs(apq) > afloor && apq * apq > 1e-30 * fabs(A[p * ld + p] * A[q * ld + q]);
+        }
+      }
+      if (!__syncthreads_or(need)) {
+        conv = 1;
+        break;
+      }
+    }
     for (int r = 0; r < nr; ++r) {
 #if RNLA_JACOBI_PROF
       c0 = clock64();
